@@ -1,0 +1,163 @@
+/*
+ * fcn.h -- C ABI of the B200-native homomorphic evaluation path
+ * (Faster CryptoNets / reference package `hecnet`).
+ *
+ * The reference is pure Python + numpy and has no FFI of its own; the entry
+ * points below are what its Python functions would bind through ctypes.
+ * Each declaration cites the reference function it replaces.
+ *
+ * Conventions (all mirror the reference's ring/fv contracts):
+ *  - residues are canonical uint64 in [0, q_i) at every boundary
+ *    (reference ring.py:140-150);
+ *  - a polynomial is `limbs` rows of n coefficients, limb-major; a
+ *    ciphertext is [2][k][n] (c0 then c1) -- byte-identical to the body of
+ *    the reference serialization after its 64-byte header (fv.py:610-619);
+ *    a batch of B ciphertexts is [B][2][k][n];
+ *  - device pointers are caller-owned device memory; `stream` is a
+ *    cudaStream_t (NULL = legacy default stream); calls are asynchronous
+ *    on that stream unless stated otherwise;
+ *  - every function returns FCN_OK (0) or a negative error code, with a
+ *    thread-local message from fcn_last_error().  The Python host maps
+ *    FCN_ERR_ARG/PARAM to RingError/FVError (ring.py:28, fv.py:38).
+ *  - compute is GPU-only: there is no CPU fallback in this library.
+ */
+#ifndef FCN_H_
+#define FCN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FCN_OK 0
+#define FCN_ERR_ARG (-1)   /* bad argument / shape mismatch            */
+#define FCN_ERR_PARAM (-2) /* unsupported or invalid parameter set     */
+#define FCN_ERR_CUDA (-3)  /* CUDA runtime failure                     */
+#define FCN_ERR_STATE (-4) /* e.g. workspace too small                 */
+
+typedef struct fcn_ring fcn_ring; /* RNS ring Z_q[x]/(x^n+1) with NTT tables */
+typedef struct fcn_ctx fcn_ctx;   /* one FV parameter set                    */
+typedef struct fcn_keys fcn_keys; /* device-resident relinearization keys   */
+
+const char* fcn_last_error(void);
+int fcn_version(void);
+
+/* ---------------------------------------------------------------- rings */
+
+/* RingContext.create(n, primes) (ring.py:104-125) with the tables of
+ * ModulusLimb._build_limb (ring.py:67-101): root = primitive_2n_root
+ * (modmath.py:136-149), psi^bitrev(i) / psi^-bitrev(i), Shoup quotients.
+ * n: power of two in [4, 32768]; every prime < 2^62, prime, = 1 mod 2n. */
+int fcn_ring_create(int device, int n, int count, const uint64_t* primes, fcn_ring** out);
+int fcn_ring_destroy(fcn_ring* ring);
+/* Copy the per-limb primitive 2n-th roots (host array of `count`). */
+int fcn_ring_roots(const fcn_ring* ring, uint64_t* roots_out);
+
+/* Rows: d_data is [n_rows][n]; row r uses limb (limb_offset + r % limb_period).
+ * ring.ntt_forward (ring.py:242-247, CT over psis[m:2m], bit-reversed out).  */
+int fcn_ntt_forward(const fcn_ring* ring, uint64_t* d_data, int64_t n_rows, int limb_period,
+                    int limb_offset, void* stream);
+/* ring.ntt_inverse (ring.py:250-255, GS over ipsis[h:m], then * n^-1).      */
+int fcn_ntt_inverse(const fcn_ring* ring, uint64_t* d_data, int64_t n_rows, int limb_period,
+                    int limb_offset, void* stream);
+
+/* Elementwise ring ops over rows (ring.py:261-300).  op: 0 add, 1 sub,
+ * 2 neg (b ignored), 3 pointwise mul (NTT domain, modmath.mul_mod).
+ * b has b_rows rows and is broadcast: row r of a pairs with b row
+ * (r % b_rows); b_rows must divide n_rows and be a multiple of the
+ * limb period (b_rows == n_rows is the plain elementwise case).         */
+#define FCN_OP_ADD 0
+#define FCN_OP_SUB 1
+#define FCN_OP_NEG 2
+#define FCN_OP_MUL 3
+int fcn_poly_binary(const fcn_ring* ring, int op, const uint64_t* d_a, const uint64_t* d_b,
+                    int64_t b_rows, uint64_t* d_out, int64_t n_rows, int limb_period, int limb_offset,
+                    void* stream);
+
+/* RingPoly.from_int_coeffs / fv._signed_to_ringpoly (ring.py:156-168,
+ * fv.py:220-225) batched: d_vals [count][n] signed -> d_out
+ * [count][limbs][n] residues mod q_(offset + l).                         */
+int fcn_lift_signed(const fcn_ring* ring, const int64_t* d_vals, int64_t count, uint64_t* d_out, int limbs,
+                    int limb_offset, void* stream);
+
+/* ring.scalar_mul (ring.py:282-288): out = a * c mod q_i with c given as
+ * per-limb canonical residues (host array of limb_period values).          */
+int fcn_scalar_mul(const fcn_ring* ring, const uint64_t* d_a, const uint64_t* c_res, uint64_t* d_out,
+                   int64_t n_rows, int limb_period, int limb_offset, void* stream);
+
+/* ring.poly_mul_monomial (ring.py:339-361): out = coeff * x^k * a with the
+ * negacyclic wrap; coeff given as per-limb residues (host, limb_period).  */
+int fcn_poly_mul_monomial(const fcn_ring* ring, const uint64_t* d_a, int k, const uint64_t* c_res,
+                          uint64_t* d_out, int64_t n_rows, int limb_period, int limb_offset,
+                          void* stream);
+
+/* ------------------------------------------------------------ FV context */
+
+/* EncryptionParams (fv.py:42-124): q-limbs, plaintext lanes, beta = 2^log2_beta.
+ * Derives ell (fv.py:78-85), Delta = q // t (fv.py:87-88), the auxiliary
+ * base via find_ntt_primes(n, (bitlen(n)+bitlen(q)+1)//54+1, 55, exclude=q)
+ * (fv.py:99-107) and all exact-rescale constants.  */
+int fcn_ctx_create(int device, int n, int k, const uint64_t* primes, int n_lanes,
+                   const uint64_t* t_lanes, int log2_beta, fcn_ctx** out);
+int fcn_ctx_destroy(fcn_ctx* ctx);
+/* The ring over the extended base (q-limbs first, then aux): q-base ops
+ * use it with limb_period = k, limb_offset = 0.                          */
+int fcn_ctx_ring(const fcn_ctx* ctx, const fcn_ring** out);
+/* what: 0 n, 1 k, 2 aux count m, 3 ell, 4 n_lanes, 5 log2_beta.          */
+int fcn_ctx_query(const fcn_ctx* ctx, int what, int64_t* value);
+int fcn_ctx_aux_primes(const fcn_ctx* ctx, uint64_t* out_m);
+
+/* EvalKeys (fv.py:191-198): host arrays a, g of shape [ell+1][k][n] in the
+ * coefficient domain (the eval-key serialization body, fv.py:660-664).
+ * Copied to the device and NTT-transformed there.                         */
+int fcn_keys_create(const fcn_ctx* ctx, const uint64_t* a, const uint64_t* g, fcn_keys** out);
+int fcn_keys_destroy(fcn_keys* keys);
+
+/* ---------------------------------------------------------- evaluation */
+
+/* Sparse plaintext add (fv.add_pt, fv.py:418-431 via _delta_m :284-292):
+ * for each term e: ct[ct_index[e]].c0[pos[e]] += coef[e] * Delta_lane
+ * (mod q_i).  coef is the centered plaintext coefficient.  In place;
+ * positions must be distinct within one ciphertext.                       */
+int fcn_add_plain_terms(const fcn_ctx* ctx, int lane, uint64_t* d_cts, int64_t n_terms,
+                        const int32_t* d_ct_index, const int32_t* d_pos, const int64_t* d_coef,
+                        void* stream);
+
+/* Fused sparse linear layer (engine.py:698-717 lin_out; per term
+ * fv.mul_pt monomial path fv.py:449-453 + ring.poly_mul_monomial, chained
+ * by fv.add_ct fv.py:394-403):
+ *   out[o] = sum_{e in [rowptr[o], rowptr[o+1])} coef[e] * x^rot[e] * in[col[e]]
+ * over both ciphertext polys and all k limbs.  Inputs are addressed as the
+ * concatenation of d_in0 (n_in0 cts) and d_in1 (n_in1 cts, may be NULL).
+ * coef: signed centered plaintext coefficient; rot in [0, n).  Rows with
+ * no terms produce the all-zero ciphertext (Ciphertext.zero, fv.py:210). */
+int fcn_linear_mac(const fcn_ctx* ctx, const uint64_t* d_in0, int64_t n_in0, const uint64_t* d_in1,
+                   int64_t n_in1, const int32_t* d_rowptr, const int32_t* d_col, const int32_t* d_rot,
+                   const int64_t* d_coef, uint64_t* d_out, int64_t n_out, void* stream);
+
+/* fv.mul_ct (fv.py:498-549): exact tensor in the extended base, exact
+ * floor((t*T + q>>1)/q) mod q, base-beta digits of c2', key switching.
+ * d_b == NULL computes the square a*a.  `count` ciphertexts [count][2][k][n].
+ * Workspace: device scratch of fcn_mul_ct_workspace_bytes(ctx, chunk)
+ * bytes; batches larger than the chunk the workspace allows are processed
+ * in chunks.                                                              */
+size_t fcn_mul_ct_workspace_bytes(const fcn_ctx* ctx, int64_t chunk);
+int fcn_mul_ct(const fcn_ctx* ctx, const fcn_keys* keys, int lane, const uint64_t* d_a,
+               const uint64_t* d_b, uint64_t* d_out, int64_t count, void* d_workspace,
+               size_t workspace_bytes, void* stream);
+
+/* fv.decrypt core (fv.py:337-353): given w = [c0 + c1 s]_q as RNS rows
+ * [count][k][n], write m = floor((w t + q>>1)/q) mod t as [count][n].     */
+int fcn_decrypt_round(const fcn_ctx* ctx, int lane, const uint64_t* d_w, uint64_t* d_m, int64_t count,
+                      void* stream);
+
+/* Diagnostics: number of coefficients that took the exact multiword
+ * fallback of the fixed-point rescale since context creation.           */
+int fcn_ctx_fallback_count(const fcn_ctx* ctx, int64_t* value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FCN_H_ */

@@ -119,31 +119,31 @@ def run_plan(P: bfv.Params, compiled, cts: list, keys: bfv.Keys, prec: int, enco
 def plain_model_batched(compiled, x_int: np.ndarray, t: int) -> np.ndarray:
     """Slot-wise integer model mod t of a compiled plan.
 
-    x_int: (inputs, slots) int64 already scaled by 2^prec.  Returns the
-    expected decrypted slot values (outputs, slots) in [0, t).
+    x_int: (inputs, slots) integers already scaled by 2^prec.  Returns the
+    expected decrypted slot values (outputs, slots) in [0, t).  Every value
+    stays below t < 2^31, so int64 products cannot overflow.
     """
-    cur = [np.asarray(v, dtype=object) % t for v in x_int]
+    cur = [np.mod(np.asarray(v, dtype=np.int64), t) for v in x_int]
     for plan in compiled.plans:
         kind = type(plan).__name__
         if kind == "LinearPlan":
             nxt = []
             for out in plan.outputs:
-                acc = np.zeros_like(cur[0]) if cur else 0
-                acc = acc * 0
+                acc = np.zeros_like(cur[0])
                 for tap in out.taps:
-                    acc = (acc + (tap.weight_int % t) * cur[tap.in_index]) % t
+                    acc = (acc + (int(tap.weight_int) % t) * cur[tap.in_index]) % t
                 if out.bias_int is not None:
-                    acc = (acc + out.bias_int) % t
+                    acc = (acc + int(out.bias_int) % t) % t
                 nxt.append(acc)
             cur = nxt
         elif kind == "PoolPlan":
             nxt = []
             for idxs in plan.outputs:
-                acc = cur[idxs[0]] * 1
+                acc = cur[idxs[0]].copy()
                 for i in idxs[1:]:
                     acc = (acc + cur[i]) % t
                 if plan.reciprocal_int is not None:
-                    acc = acc * (plan.reciprocal_int % t) % t
+                    acc = acc * (int(plan.reciprocal_int) % t) % t
                 nxt.append(acc)
             cur = nxt
         elif kind == "ActPlan":
@@ -151,11 +151,11 @@ def plain_model_batched(compiled, x_int: np.ndarray, t: int) -> np.ndarray:
             for x in cur:
                 acc = x * x % t
                 if plan.a2_int is not None:
-                    acc = acc * (plan.a2_int % t) % t
+                    acc = acc * (int(plan.a2_int) % t) % t
                 if plan.a1_mult_int is not None:
-                    acc = (acc + x * (plan.a1_mult_int % t)) % t
+                    acc = (acc + x * (int(plan.a1_mult_int) % t)) % t
                 if plan.a0_add_int is not None:
-                    acc = (acc + plan.a0_add_int) % t
+                    acc = (acc + int(plan.a0_add_int) % t) % t
                 nxt.append(acc)
             cur = nxt
-    return np.array([[int(v) for v in row] for row in cur], dtype=np.int64)
+    return np.stack(cur).astype(np.int64)

@@ -1,0 +1,168 @@
+// Internal definitions shared by the libfcn translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/fcn.h"
+
+namespace fcn {
+
+// ------------------------------------------------------------------ errors
+
+int set_error(int code, const char* fmt, ...);
+int check_cuda(cudaError_t e, const char* what);
+#define FCN_CUDA(call)                                  \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return check_cuda(_e, #call); \
+  } while (0)
+#define FCN_LAUNCH_CHECK(what)                                 \
+  do {                                                         \
+    cudaError_t _e = cudaGetLastError();                       \
+    if (_e != cudaSuccess) return check_cuda(_e, what);        \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ------------------------------------------------------------ limb tables
+
+// Per-limb constants, one struct per prime of a ring (device resident).
+struct LimbConst {
+  uint64_t q;       // the prime, < 2^62
+  uint64_t q2;      // 2q
+  uint64_t ninv;    // n^-1 mod q
+  uint64_t ninv_s;  // Shoup quotient floor(ninv 2^64 / q)
+  uint64_t wlast;   // ipsi[1] * n^-1 mod q (last inverse stage, merged scaling)
+  uint64_t wlast_s;
+  uint64_t mu;      // Barrett floor(2^(2s) / q), s = bitlen(q)
+  uint32_t s;       // bitlen(q)
+  uint32_t pad;
+  uint64_t one_s;   // floor(2^64 / q): Shoup quotient of the constant 1
+  uint64_t r64;     // 2^64 mod q
+  uint64_t r64_s;
+};
+
+struct __align__(16) Twiddle {
+  uint64_t w;  // psi^bitrev(i) (forward) or psi^-bitrev(i) (inverse)
+  uint64_t s;  // floor(w 2^64 / q)
+};
+
+}  // namespace fcn
+
+struct fcn_ring {
+  int device = 0;
+  int n = 0;
+  int logn = 0;
+  int L = 0;
+  std::vector<uint64_t> primes;
+  std::vector<uint64_t> roots;
+  std::vector<fcn::LimbConst> host_lc;
+  fcn::LimbConst* d_lc = nullptr;  // [L]
+  fcn::Twiddle* d_fwd = nullptr;   // [L][n]
+  fcn::Twiddle* d_inv = nullptr;   // [L][n]
+};
+
+namespace fcn {
+
+// ------------------------------------------------------ device arithmetic
+
+__device__ __forceinline__ uint64_t csub(uint64_t x, uint64_t m) { return x >= m ? x - m : x; }
+
+// a * w mod q in [0, 2q) for constant w < q with ws = floor(w 2^64 / q); any a < 2^64.
+__device__ __forceinline__ uint64_t shoup_lazy(uint64_t a, uint64_t w, uint64_t ws, uint64_t q) {
+  return a * w - __umul64hi(a, ws) * q;
+}
+__device__ __forceinline__ uint64_t shoup(uint64_t a, uint64_t w, uint64_t ws, uint64_t q) {
+  return csub(shoup_lazy(a, w, ws, q), q);
+}
+// Exact (quotient, remainder) of a * w / q for constant w with Shoup quotient ws.
+__device__ __forceinline__ uint64_t shoup_divmod(uint64_t a, uint64_t w, uint64_t ws, uint64_t q,
+                                                 uint64_t* quo) {
+  uint64_t h = __umul64hi(a, ws);
+  uint64_t r = a * w - h * q;
+  if (r >= q) {
+    r -= q;
+    h += 1;
+  }
+  *quo = h;
+  return r;
+}
+
+// Barrett: (hi:lo) mod q for a 128-bit x < q^2 (q < 2^62).  Canonical.
+__device__ __forceinline__ uint64_t barrett128(uint64_t hi, uint64_t lo, const LimbConst& c) {
+  const uint32_t s = c.s;
+  // x1 = x >> (s - 1) fits in s + 1 <= 63 bits
+  uint64_t x1 = (lo >> (s - 1)) | (s - 1 == 0 ? 0 : (hi << (65 - s)));
+  // qhat = (x1 * mu) >> (s + 1)
+  uint64_t ph = __umul64hi(x1, c.mu);
+  uint64_t pl = x1 * c.mu;
+  uint64_t qhat = (pl >> (s + 1)) | (ph << (63 - s));
+  uint64_t r = lo - qhat * c.q;
+  r = csub(r, c.q);
+  return csub(r, c.q);
+}
+
+__device__ __forceinline__ uint64_t mulmod(uint64_t a, uint64_t b, const LimbConst& c) {
+  return barrett128(__umul64hi(a, b), a * b, c);
+}
+
+// Any 128-bit (hi:lo) mod q, canonical: hi*2^64 + lo folded through Shoup.
+__device__ __forceinline__ uint64_t reduce128(uint64_t hi, uint64_t lo, const LimbConst& c) {
+  uint64_t a = csub(shoup_lazy(hi, c.r64, c.r64_s, c.q), c.q);
+  uint64_t b = csub(shoup_lazy(lo, 1, c.one_s, c.q), c.q);
+  return csub(a + b, c.q);
+}
+
+__device__ __forceinline__ void add128(uint64_t& hi, uint64_t& lo, uint64_t ph, uint64_t pl) {
+  lo += pl;
+  hi += ph + (lo < pl);
+}
+
+__device__ __forceinline__ uint64_t addmod(uint64_t a, uint64_t b, uint64_t q) { return csub(a + b, q); }
+__device__ __forceinline__ uint64_t submod(uint64_t a, uint64_t b, uint64_t q) { return csub(a + q - b, q); }
+
+// ---------------------------------------------------- host-side helpers
+
+inline uint64_t h_mulmod(uint64_t a, uint64_t b, uint64_t m) {
+  return (uint64_t)(((unsigned __int128)a * b) % m);
+}
+inline uint64_t h_powmod(uint64_t b, uint64_t e, uint64_t m) {
+  uint64_t r = 1 % m;
+  b %= m;
+  while (e) {
+    if (e & 1) r = h_mulmod(r, b, m);
+    b = h_mulmod(b, b, m);
+    e >>= 1;
+  }
+  return r;
+}
+inline uint64_t h_shoup(uint64_t w, uint64_t q) { return (uint64_t)(((unsigned __int128)w << 64) / q); }
+bool h_is_prime(uint64_t v);
+int bitlen64(uint64_t v);
+LimbConst make_limb_const(uint64_t q, int n, uint64_t ipsi1);
+
+inline int grid_for(int64_t work, int block, int max_blocks = 148 * 16) {
+  int64_t g = (work + block - 1) / block;
+  if (g > max_blocks) g = max_blocks;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace fcn

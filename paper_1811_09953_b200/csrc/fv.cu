@@ -1,0 +1,1022 @@
+// libfcn: FV evaluation on B200 -- context constants, relinearisation keys,
+// fused sparse linear layer, exact ciphertext multiplication, decrypt rounding.
+//
+// Replaces reference fv.py (EncryptionParams :42-124, add_pt :418-431,
+// mul_pt :439-460, mul_ct :463-549, decrypt :337-353) and the per-output
+// inner loop of engine.eval_encrypted (engine.py:698-772).
+//
+// Exactness: the reference computes mul_ct with Python
+// big integers.  Here every big-integer step is an RNS identity whose only
+// approximate ingredient is a float64 estimate of a *small* integer
+// (a CRT overflow count or a floor of a sum of fractions < k+1); each such
+// estimate is either provably far from a rounding boundary (the extended
+// base leaves >= 3 bits of headroom) or checked against an epsilon band and
+// recomputed with exact multiword arithmetic when inside it.  Outputs are
+// therefore bit-identical to the reference for every input.
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "bigint.hpp"
+#include "fcn_common.cuh"
+
+namespace fcn {
+
+int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st);
+
+constexpr int KQ_LIM = 16;  // max ciphertext limbs
+constexpr int KE_LIM = 32;  // max extended-base limbs
+constexpr int MW_LIM = 18;  // multiword scratch words
+constexpr int LANE_LIM = 8;
+constexpr double kEps = 1.0 / (1ull << 36);  // ambiguity band of float64 floors
+
+// Per-(context, lane) constants for lift / rescale / digits / decrypt.
+struct MulCtConst {
+  int k, K, m, D, w, qwords, direct, dwords;
+  uint64_t t;
+  // lift: y_i = x_i (q/q_i)^-1 mod q_i; aux residue = sum y_i [q/q_i]_{p_j} - v' [q]_{p_j}
+  uint64_t qinv[KQ_LIM], qinv_s[KQ_LIM];
+  double rq[KQ_LIM];
+  uint64_t lc[KE_LIM][KQ_LIM], lc_s[KE_LIM][KQ_LIM];
+  uint64_t lvq[KE_LIM][KQ_LIM + 2];
+  // rescale: y_j = T_j (B/b_j)^-1 mod b_j
+  uint64_t binv[KE_LIM], binv_s[KE_LIM];
+  double rb[KE_LIM];
+  uint64_t beta[KQ_LIM], beta_s[KQ_LIM];                 // tP mod q_j
+  uint64_t rc[KQ_LIM][KE_LIM], rc_s[KQ_LIM][KE_LIM];     // [floor(tP/q_j)]_{q_i} | [tP/p_j]_{q_i}
+  uint64_t rvt[KQ_LIM][KE_LIM + 2];                      // (-v tP) mod q_i, v = 0..K
+  double hq;                                             // ((q-1)/2)/q
+  // multiword: q, (q-1)/2, q/q_i
+  uint64_t qw[MW_LIM], hw[MW_LIM];
+  uint64_t Qw[KQ_LIM][MW_LIM];
+  // decrypt: t = tq_i q_i + tr_i
+  uint64_t tr[KQ_LIM], tr_s[KQ_LIM], tq[KQ_LIM];
+  // digits: [2^(64 m)]_{q_l}
+  uint64_t dpw[KQ_LIM][4], dpw_s[KQ_LIM][4];
+  // add_pt: Delta = q // t mod q_i
+  uint64_t delta[KQ_LIM], delta_s[KQ_LIM];
+};
+
+}  // namespace fcn
+
+struct fcn_ctx {
+  int device = 0;
+  int n = 0, logn = 0, k = 0, m = 0, ell = 0, log2_beta = 0, n_lanes = 0;
+  std::vector<uint64_t> primes, aux, lanes;
+  fcn_ring* ext = nullptr;
+  fcn::MulCtConst* d_mc = nullptr;  // [n_lanes]
+  unsigned long long* d_fallbacks = nullptr;
+};
+
+struct fcn_keys {
+  int device = 0;
+  int D = 0, k = 0, n = 0;
+  uint64_t* d_g = nullptr;  // [D][k][n] NTT domain
+  uint64_t* d_a = nullptr;
+};
+
+namespace fcn {
+
+// ------------------------------------------------------------ multiword
+
+template <int NW>
+__device__ __forceinline__ void mw_zero(uint64_t (&a)[NW]) {
+#pragma unroll
+  for (int i = 0; i < NW; ++i) a[i] = 0;
+}
+
+// a += y * src (src: nsrc words, little endian)
+template <int NW>
+__device__ __forceinline__ void mw_mac(uint64_t (&a)[NW], const uint64_t* __restrict__ src, int nsrc, uint64_t y) {
+  uint64_t carry = 0;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    const uint64_t s = i < nsrc ? src[i] : 0;
+    uint64_t lo = s * y, hi = __umul64hi(s, y);
+    uint64_t t = a[i] + lo;
+    hi += t < lo;
+    uint64_t t2 = t + carry;
+    hi += t2 < carry;
+    a[i] = t2;
+    carry = hi;
+  }
+}
+
+template <int NW>
+__device__ __forceinline__ void mw_add(uint64_t (&a)[NW], const uint64_t* __restrict__ b) {
+  uint64_t c = 0;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    uint64_t s = a[i] + b[i];
+    uint64_t c1 = s < b[i];
+    uint64_t s2 = s + c;
+    c = c1 + (s2 < c);
+    a[i] = s2;
+  }
+}
+
+template <int NW>
+__device__ __forceinline__ void mw_sub(uint64_t (&a)[NW], const uint64_t* __restrict__ b) {
+  uint64_t br = 0;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    uint64_t d = a[i] - b[i];
+    uint64_t b1 = a[i] < b[i];
+    uint64_t d2 = d - br;
+    br = b1 + (d < br);
+    a[i] = d2;
+  }
+}
+
+// a -= u * b (u small), two's complement
+template <int NW>
+__device__ __forceinline__ void mw_submul(uint64_t (&a)[NW], const uint64_t* __restrict__ b, uint64_t u) {
+  uint64_t carry = 0, br = 0;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    uint64_t lo = b[i] * u, hi = __umul64hi(b[i], u);
+    uint64_t p = lo + carry;
+    hi += p < lo;
+    carry = hi;
+    uint64_t d = a[i] - p;
+    uint64_t b1 = a[i] < p;
+    uint64_t d2 = d - br;
+    br = b1 + (d < br);
+    a[i] = d2;
+  }
+}
+
+template <int NW>
+__device__ __forceinline__ bool mw_negative(const uint64_t (&a)[NW]) {
+  return (int64_t)a[NW - 1] < 0;
+}
+
+// a >= b for non-negative a
+template <int NW>
+__device__ __forceinline__ bool mw_ge(const uint64_t (&a)[NW], const uint64_t* __restrict__ b) {
+  int res = 0;  // 0 equal so far (from the top), 1 greater, -1 less
+#pragma unroll
+  for (int i = NW - 1; i >= 0; --i) {
+    if (res == 0) res = a[i] > b[i] ? 1 : (a[i] < b[i] ? -1 : 0);
+  }
+  return res >= 0;
+}
+
+// a <- a - g q with g adjusted so that a lands in [0, q); returns g.
+template <int NW>
+__device__ __forceinline__ int64_t mw_reduce_q(uint64_t (&a)[NW], const MulCtConst* __restrict__ cc, int64_t g) {
+  if (g > 0) mw_submul<NW>(a, cc->qw, (uint64_t)g);
+  while (mw_negative<NW>(a)) {
+    mw_add<NW>(a, cc->qw);
+    --g;
+  }
+  while (mw_ge<NW>(a, cc->qw)) {
+    mw_sub<NW>(a, cc->qw);
+    ++g;
+  }
+  return g;
+}
+
+template <int NW>
+__device__ __forceinline__ uint64_t mw_word(const uint64_t (&a)[NW], int idx) {
+  uint64_t r = 0;
+#pragma unroll
+  for (int i = 0; i < NW; ++i)
+    if (i == idx) r = a[i];
+  return r;
+}
+
+// floor(sum_j r_j (q/q_j) + (q-1)/2) / q) exactly (the rare fallback of a
+// float64 floor of sum r_j/q_j + ((q-1)/2)/q).
+template <int NW>
+__device__ __noinline__ int64_t exact_frac_floor(const uint64_t* r, int k, const MulCtConst* __restrict__ cc,
+                                                 int64_t g_est) {
+  uint64_t a[NW];
+  mw_zero<NW>(a);
+  for (int j = 0; j < k; ++j) mw_mac<NW>(a, cc->Qw[j], cc->qwords, r[j]);
+  mw_add<NW>(a, cc->hw);
+  return mw_reduce_q<NW>(a, cc, g_est);
+}
+
+// ------------------------------------------------------------ add_pt
+
+__global__ void add_plain_kernel(uint64_t* __restrict__ cts, int64_t n_terms, const int32_t* __restrict__ ct_index,
+                                 const int32_t* __restrict__ pos, const int64_t* __restrict__ coef, int k, int logn,
+                                 const MulCtConst* __restrict__ cc, const LimbConst* __restrict__ lcs) {
+  const int64_t total = n_terms * k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t term = e / k;
+    const int i = (int)(e % k);
+    const LimbConst c = lcs[i];
+    const int64_t cf = coef[term];
+    const uint64_t mag = cf < 0 ? (uint64_t)(-(cf + 1)) + 1 : (uint64_t)cf;
+    uint64_t v = shoup(mag, 1, c.one_s, c.q);
+    v = shoup(v, cc->delta[i], cc->delta_s[i], c.q);
+    if (cf < 0 && v) v = c.q - v;
+    uint64_t* p = cts + ((int64_t)ct_index[term] * 2 * k + i) * ((int64_t)1 << logn) + pos[term];
+    *p = addmod(*p, v, c.q);
+  }
+}
+
+// ------------------------------------------------------- linear MAC layer
+
+// out[o] = sum_e coef_e x^rot_e in[col_e]; grid (chunk, output, row = poly*k + limb)
+__global__ void __launch_bounds__(256) mac_kernel(const uint64_t* __restrict__ in0, int64_t n_in0,
+                                                  const uint64_t* __restrict__ in1, const int32_t* __restrict__ rowptr,
+                                                  const int32_t* __restrict__ col, const int32_t* __restrict__ rot,
+                                                  const int64_t* __restrict__ coef, uint64_t* __restrict__ out,
+                                                  int logn, int k, const LimbConst* __restrict__ lcs) {
+  const int n = 1 << logn;
+  const int o = blockIdx.y;
+  const int r = blockIdx.z;
+  const int limb = r % k;
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (j0 >= n) return;
+  const LimbConst c = lcs[limb];
+  const int64_t ct_words = (int64_t)2 * k * n;
+  uint64_t ph0 = 0, pl0 = 0, nh0 = 0, nl0 = 0, ph1 = 0, pl1 = 0, nh1 = 0, nl1 = 0;
+  const int e0 = rowptr[o], e1 = rowptr[o + 1];
+  for (int e = e0; e < e1; ++e) {
+    const int cl = __ldg(col + e);
+    const int rt = __ldg(rot + e);
+    const int64_t cf = __ldg(coef + e);
+    const uint64_t* src = (cl < n_in0 ? in0 + (int64_t)cl * ct_words : in1 + (int64_t)(cl - n_in0) * ct_words) + (int64_t)r * n;
+    const bool neg = cf < 0;
+    const uint64_t mag = neg ? (uint64_t)(-(cf + 1)) + 1 : (uint64_t)cf;
+    uint64_t x0, x1;
+    bool w0 = false, w1 = false;
+    if (rt == 0) {
+      const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(src + j0);
+      x0 = v.x;
+      x1 = v.y;
+    } else {
+      int s0 = j0 - rt, s1 = j0 + 1 - rt;
+      w0 = s0 < 0;
+      w1 = s1 < 0;
+      s0 += w0 ? n : 0;
+      s1 += w1 ? n : 0;
+      x0 = src[s0];
+      x1 = src[s1];
+    }
+    uint64_t h0, l0, h1, l1;
+    if ((mag & (mag - 1)) == 0) {
+      const int sh = __ffsll((long long)mag) - 1;
+      l0 = x0 << sh;
+      l1 = x1 << sh;
+      h0 = sh ? x0 >> (64 - sh) : 0;
+      h1 = sh ? x1 >> (64 - sh) : 0;
+    } else {
+      l0 = x0 * mag;
+      h0 = __umul64hi(x0, mag);
+      l1 = x1 * mag;
+      h1 = __umul64hi(x1, mag);
+    }
+    // sign = neg xor wrapped; route into the positive or negative accumulator
+    const uint64_t m0 = (neg != w0) ? ~0ull : 0ull;
+    const uint64_t m1 = (neg != w1) ? ~0ull : 0ull;
+    add128(nh0, nl0, h0 & m0, l0 & m0);
+    add128(ph0, pl0, h0 & ~m0, l0 & ~m0);
+    add128(nh1, nl1, h1 & m1, l1 & m1);
+    add128(ph1, pl1, h1 & ~m1, l1 & ~m1);
+    if (mag >> 40) {  // wide constants: fold so 128-bit accumulators never overflow
+      pl0 = reduce128(ph0, pl0, c); ph0 = 0;
+      nl0 = reduce128(nh0, nl0, c); nh0 = 0;
+      pl1 = reduce128(ph1, pl1, c); ph1 = 0;
+      nl1 = reduce128(nh1, nl1, c); nh1 = 0;
+    }
+  }
+  ulonglong2 res;
+  res.x = submod(reduce128(ph0, pl0, c), reduce128(nh0, nl0, c), c.q);
+  res.y = submod(reduce128(ph1, pl1, c), reduce128(nh1, nl1, c), c.q);
+  *reinterpret_cast<ulonglong2*>(out + (int64_t)o * ct_words + (int64_t)r * n + j0) = res;
+}
+
+// ------------------------------------------------------------- mul_ct
+
+// Centered lift of c0/c1 into the extended base (fv.py:463-470).
+template <int KQ, int KA, int NW>
+__global__ void __launch_bounds__(256) lift_kernel(const uint64_t* __restrict__ in, uint64_t* __restrict__ ext,
+                                                   int64_t npoly, int logn, const MulCtConst* __restrict__ cc,
+                                                   const LimbConst* __restrict__ lcs,
+                                                   unsigned long long* __restrict__ fallbacks) {
+  const int n = 1 << logn;
+  const int k = cc->k, m = cc->m, K = cc->K;
+  const int64_t total = npoly << logn;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t poly = e >> logn;
+    const int coef = (int)(e & (n - 1));
+    uint64_t y[KQ];
+    double f = 0.5;
+#pragma unroll
+    for (int i = 0; i < KQ; ++i) {
+      y[i] = 0;
+      if (i < k) {
+        const uint64_t x = in[(poly * k + i) * n + coef];
+        ext[(poly * K + i) * n + coef] = x;
+        y[i] = shoup(x, cc->qinv[i], cc->qinv_s[i], lcs[i].q);
+        f += (double)y[i] * cc->rq[i];
+      }
+    }
+    int64_t v = (int64_t)floor(f);
+    const double fr = f - (double)v;
+    if (fr < kEps || fr > 1.0 - kEps) {
+      // exact: canonical x = sum y_i Q_i - u q, then v' = u + (x > (q-1)/2)
+      uint64_t a[NW];
+      mw_zero<NW>(a);
+      for (int i = 0; i < k; ++i) mw_mac<NW>(a, cc->Qw[i], cc->qwords, y[i]);
+      const int64_t u = mw_reduce_q<NW>(a, cc, (int64_t)floor(f - 0.5));
+      bool gt = false, decided = false;
+      for (int i = NW - 1; i >= 0; --i) {
+        if (!decided && a[i] != cc->hw[i]) {
+          gt = a[i] > cc->hw[i];
+          decided = true;
+        }
+      }
+      v = u + (gt ? 1 : 0);
+      atomicAdd(fallbacks, 1ull);
+    }
+#pragma unroll
+    for (int j = 0; j < KA; ++j) {
+      if (j < m) {
+        const LimbConst& pc = lcs[k + j];
+        const uint64_t p = pc.q, p2 = pc.q2;
+        uint64_t acc = 0;
+#pragma unroll
+        for (int i = 0; i < KQ; ++i)
+          if (i < k) acc = csub(acc + shoup_lazy(y[i], cc->lc[j][i], cc->lc_s[j][i], p), p2);
+        acc = csub(acc, p);
+        acc = addmod(acc, cc->lvq[j][v], p);
+        ext[(poly * K + k + j) * n + coef] = acc;
+      }
+    }
+  }
+}
+
+// NTT-domain tensor: (a0 b0, a0 b1 + a1 b0, a1 b1) per ext limb (fv.py:511-515).
+__global__ void tensor_kernel(const uint64_t* __restrict__ A, const uint64_t* __restrict__ B, uint64_t* __restrict__ T,
+                              int64_t C, int K, int logn, const LimbConst* __restrict__ lcs) {
+  const int n = 1 << logn;
+  const int64_t total = (C * K) << logn;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rowi = e >> logn;
+    const int coef = (int)(e & (n - 1));
+    const int64_t ct = rowi / K;
+    const int j = (int)(rowi % K);
+    const LimbConst c = lcs[j];
+    const int64_t i0 = ((ct * 2 + 0) * K + j) * n + coef, i1 = ((ct * 2 + 1) * K + j) * n + coef;
+    const uint64_t a0 = A[i0], a1 = A[i1];
+    uint64_t t0, t1, t2;
+    if (B) {
+      const uint64_t b0 = B[i0], b1 = B[i1];
+      t0 = mulmod(a0, b0, c);
+      t1 = addmod(mulmod(a0, b1, c), mulmod(a1, b0, c), c.q);
+      t2 = mulmod(a1, b1, c);
+    } else {
+      t0 = mulmod(a0, a0, c);
+      const uint64_t x = mulmod(a0, a1, c);
+      t1 = addmod(x, x, c.q);
+      t2 = mulmod(a1, a1, c);
+    }
+    T[((ct * 3 + 0) * K + j) * n + coef] = t0;
+    T[((ct * 3 + 1) * K + j) * n + coef] = t1;
+    T[((ct * 3 + 2) * K + j) * n + coef] = t2;
+  }
+}
+
+// Exact rescale R = floor((t T + (q-1)/2) / q) mod q from the ext-base
+// residues of T (fv.py:473-490, 517-522); for the third tensor poly the
+// base-beta digits of R (fv.py:524-533) are emitted instead.
+template <int KQ, int KE, int NW>
+__global__ void __launch_bounds__(256) rescale_kernel(const uint64_t* __restrict__ T, uint64_t* __restrict__ R01,
+                                                      uint64_t* __restrict__ DG, int64_t C, int logn,
+                                                      const MulCtConst* __restrict__ cc,
+                                                      const LimbConst* __restrict__ lcs,
+                                                      unsigned long long* __restrict__ fallbacks) {
+  const int n = 1 << logn;
+  const int k = cc->k, K = cc->K;
+  const int64_t total = (C * 3) << logn;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cp = e >> logn;
+    const int coef = (int)(e & (n - 1));
+    const int64_t ct = cp / 3;
+    const int p = (int)(cp % 3);
+    // 1. y_j = T_j (B/b_j)^-1 mod b_j and the (exactly rounded) CRT overflow count v
+    uint64_t y[KE];
+    double fv = 0.0;
+#pragma unroll
+    for (int j = 0; j < KE; ++j) {
+      y[j] = 0;
+      if (j < K) {
+        const uint64_t x = T[(cp * K + j) * n + coef];
+        y[j] = shoup(x, cc->binv[j], cc->binv_s[j], lcs[j].q);
+        fv += (double)y[j] * cc->rb[j];
+      }
+    }
+    const int v = (int)rint(fv);  // |T|/B < 1/8: never near a half
+    // 2. q-part: y_j tP/q_j = y_j floor(tP/q_j) + h_j + r_j/q_j
+    uint64_t r[KQ];
+    uint64_t sh_hi = 0, sh_lo = 0;
+    double G = cc->hq;
+#pragma unroll
+    for (int j = 0; j < KQ; ++j) {
+      r[j] = 0;
+      if (j < k) {
+        uint64_t h;
+        r[j] = shoup_divmod(y[j], cc->beta[j], cc->beta_s[j], lcs[j].q, &h);
+        add128(sh_hi, sh_lo, 0, h);
+        G += (double)r[j] * cc->rq[j];
+      }
+    }
+    int64_t g = (int64_t)floor(G);
+    const double fr = G - (double)g;
+    if (fr < kEps || fr > 1.0 - kEps) {
+      g = exact_frac_floor<NW>(r, k, cc, g);
+      atomicAdd(fallbacks, 1ull);
+    }
+    // 3. residues of R mod q_i
+    uint64_t out[KQ];
+#pragma unroll
+    for (int i = 0; i < KQ; ++i) {
+      out[i] = 0;
+      if (i < k) {
+        const LimbConst& c = lcs[i];
+        uint64_t acc = 0;
+#pragma unroll
+        for (int j = 0; j < KE; ++j)
+          if (j < K) acc = csub(acc + shoup_lazy(y[j], cc->rc[i][j], cc->rc_s[i][j], c.q), c.q2);
+        const uint64_t s1 = reduce128(sh_hi, sh_lo, c);
+        acc = csub(acc, c.q) + s1 + cc->rvt[i][v] + (uint64_t)g;
+        acc = csub(acc, c.q2);
+        acc = csub(acc, c.q2);
+        out[i] = csub(acc, c.q);
+      }
+    }
+    if (p < 2) {
+#pragma unroll
+      for (int i = 0; i < KQ; ++i)
+        if (i < k) R01[((ct * 2 + p) * k + i) * n + coef] = out[i];
+    } else {
+      // 4. canonical multiword R2 = sum z_i Q_i - u q, then base-beta digits
+      uint64_t a[NW];
+      mw_zero<NW>(a);
+      double fu = 0.0;
+#pragma unroll
+      for (int i = 0; i < KQ; ++i) {
+        if (i < k) {
+          const uint64_t z = shoup(out[i], cc->qinv[i], cc->qinv_s[i], lcs[i].q);
+          fu += (double)z * cc->rq[i];
+          mw_mac<NW>(a, cc->Qw[i], cc->qwords, z);
+        }
+      }
+      mw_reduce_q<NW>(a, cc, (int64_t)floor(fu));
+      const int D = cc->D, w = cc->w;
+      for (int d = 0; d < D; ++d) {
+        const int bit = d * w;
+        // digit words (up to 3 for w <= 190)
+        uint64_t dw[3];
+#pragma unroll
+        for (int mword = 0; mword < 3; ++mword) {
+          const int b0 = bit + 64 * mword;
+          const int wi = b0 >> 6, bo = b0 & 63;
+          uint64_t lo = mw_word<NW>(a, wi) >> bo;
+          if (bo) lo |= mw_word<NW>(a, wi + 1) << (64 - bo);
+          const int rem = w - 64 * mword;  // bits of the digit at or above this word
+          if (rem <= 0) lo = 0;
+          else if (rem < 64) lo &= (1ull << rem) - 1;
+          dw[mword] = lo;
+        }
+#pragma unroll
+        for (int l = 0; l < KQ; ++l) {
+          if (l < k) {
+            const LimbConst& c = lcs[l];
+            uint64_t val;
+            if (cc->direct) {
+              val = dw[0];
+            } else {
+              val = csub(shoup_lazy(dw[0], 1, c.one_s, c.q), c.q);
+              if (cc->dwords > 1) val += csub(shoup_lazy(dw[1], cc->dpw[l][1], cc->dpw_s[l][1], c.q), c.q);
+              if (cc->dwords > 2) val += csub(shoup_lazy(dw[2], cc->dpw[l][2], cc->dpw_s[l][2], c.q), c.q);
+              val = csub(csub(val, c.q2), c.q);
+            }
+            DG[((ct * D + d) * k + l) * n + coef] = val;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Key switching MAC in the NTT domain (fv.py:533-537):
+// acc0 = sum_d g_d * D_d, acc1 = sum_d a_d * D_d.
+__global__ void keymac_kernel(const uint64_t* __restrict__ DG, const uint64_t* __restrict__ kg,
+                              const uint64_t* __restrict__ ka, uint64_t* __restrict__ ACC, int64_t C, int D, int k,
+                              int logn, const LimbConst* __restrict__ lcs) {
+  const int n = 1 << logn;
+  const int64_t total = (C * k) << logn;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rowi = e >> logn;
+    const int coef = (int)(e & (n - 1));
+    const int64_t ct = rowi / k;
+    const int l = (int)(rowi % k);
+    const LimbConst c = lcs[l];
+    uint64_t gh = 0, gl = 0, ah = 0, al = 0;
+    for (int d = 0; d < D; ++d) {
+      const uint64_t x = DG[((ct * D + d) * k + l) * n + coef];
+      const int64_t ki = ((int64_t)d * k + l) * n + coef;
+      const uint64_t g = kg[ki], a = ka[ki];
+      add128(gh, gl, __umul64hi(x, g), x * g);
+      add128(ah, al, __umul64hi(x, a), x * a);
+      if ((d & 7) == 7) {
+        gl = reduce128(gh, gl, c);
+        gh = 0;
+        al = reduce128(ah, al, c);
+        ah = 0;
+      }
+    }
+    ACC[((ct * 2 + 0) * k + l) * n + coef] = reduce128(gh, gl, c);
+    ACC[((ct * 2 + 1) * k + l) * n + coef] = reduce128(ah, al, c);
+  }
+}
+
+__global__ void add_rows_kernel(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, uint64_t* __restrict__ out,
+                                int64_t total, int logn, int k, const LimbConst* __restrict__ lcs) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int limb = (int)((e >> logn) % k);
+    out[e] = addmod(a[e], b[e], lcs[limb].q);
+  }
+}
+
+// Decrypt rounding m = floor((w t + (q-1)/2)/q) mod t  (fv.py:344-349).
+template <int KQ, int NW>
+__global__ void decrypt_round_kernel(const uint64_t* __restrict__ W, uint64_t* __restrict__ M, int64_t count, int logn,
+                                     const MulCtConst* __restrict__ cc, const LimbConst* __restrict__ lcs,
+                                     unsigned long long* __restrict__ fallbacks) {
+  const int n = 1 << logn;
+  const int k = cc->k;
+  const uint64_t t = cc->t;
+  const int64_t total = count << logn;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ct = e >> logn;
+    const int coef = (int)(e & (n - 1));
+    uint64_t r[KQ];
+    unsigned __int128 quo = 0;
+    double G = cc->hq;
+#pragma unroll
+    for (int i = 0; i < KQ; ++i) {
+      r[i] = 0;
+      if (i < k) {
+        const LimbConst& c = lcs[i];
+        const uint64_t y = shoup(W[(ct * k + i) * n + coef], cc->qinv[i], cc->qinv_s[i], c.q);
+        uint64_t h;
+        r[i] = shoup_divmod(y, cc->tr[i], cc->tr_s[i], c.q, &h);
+        quo += (unsigned __int128)h + (unsigned __int128)y * cc->tq[i];
+        G += (double)r[i] * cc->rq[i];
+      }
+    }
+    int64_t g = (int64_t)floor(G);
+    const double fr = G - (double)g;
+    if (fr < kEps || fr > 1.0 - kEps) {
+      g = exact_frac_floor<NW>(r, k, cc, g);
+      atomicAdd(fallbacks, 1ull);
+    }
+    quo += (unsigned __int128)g;
+    M[e] = (uint64_t)(quo % t);
+  }
+}
+
+// ------------------------------------------------------ host constants
+
+static Big big_prod(const std::vector<uint64_t>& v, int skip = -1) {
+  Big r(1);
+  for (int i = 0; i < (int)v.size(); ++i)
+    if (i != skip) r = r.mul_small(v[i]);
+  return r;
+}
+
+static void store_words(const Big& b, uint64_t* dst, int cap) {
+  for (int i = 0; i < cap; ++i) dst[i] = b.word(i);
+}
+
+static int build_mulct_const(const fcn_ctx* x, uint64_t t, MulCtConst* mc) {
+  memset(mc, 0, sizeof(*mc));
+  const int k = x->k, m = x->m, K = k + m;
+  mc->k = k;
+  mc->m = m;
+  mc->K = K;
+  mc->D = x->ell + 1;
+  mc->w = x->log2_beta;
+  mc->t = t;
+  std::vector<uint64_t> ext = x->primes;
+  ext.insert(ext.end(), x->aux.begin(), x->aux.end());
+  const Big q = big_prod(x->primes);
+  const Big P = big_prod(x->aux);
+  mc->qwords = (int)q.w.size();
+  store_words(q, mc->qw, MW_LIM);
+  store_words(q.shr1(), mc->hw, MW_LIM);
+  const double qd = q.to_double();
+  mc->hq = 0.5 - 0.5 / qd;
+  // lift
+  for (int i = 0; i < k; ++i) {
+    const uint64_t qi = x->primes[i];
+    const Big Qi = big_prod(x->primes, i);
+    store_words(Qi, mc->Qw[i], MW_LIM);
+    const uint64_t qm = Qi.mod_small(qi);
+    mc->qinv[i] = h_powmod(qm, qi - 2, qi);
+    mc->qinv_s[i] = h_shoup(mc->qinv[i], qi);
+    mc->rq[i] = 1.0 / (double)qi;
+  }
+  for (int j = 0; j < m; ++j) {
+    const uint64_t p = x->aux[j];
+    for (int i = 0; i < k; ++i) {
+      const uint64_t c = big_prod(x->primes, i).mod_small(p);
+      mc->lc[j][i] = c;
+      mc->lc_s[j][i] = h_shoup(c, p);
+    }
+    const uint64_t qp = q.mod_small(p);
+    for (int v = 0; v <= k + 1; ++v) mc->lvq[j][v] = (p - h_mulmod(qp, (uint64_t)v, p)) % p;
+  }
+  // rescale
+  const Big B = q.mul(P);
+  const Big tP = P.mul_small(t);
+  for (int j = 0; j < K; ++j) {
+    const uint64_t b = ext[j];
+    const uint64_t bm = big_prod(ext, j).mod_small(b);
+    mc->binv[j] = h_powmod(bm, b - 2, b);
+    mc->binv_s[j] = h_shoup(mc->binv[j], b);
+    mc->rb[j] = 1.0 / (double)b;
+  }
+  (void)B;
+  std::vector<Big> alpha(k);
+  for (int j = 0; j < k; ++j) {
+    uint64_t rem;
+    alpha[j] = tP.div_small(x->primes[j], &rem);
+    mc->beta[j] = rem;
+    mc->beta_s[j] = h_shoup(rem, x->primes[j]);
+  }
+  std::vector<Big> tPp(m);
+  for (int j = 0; j < m; ++j) {
+    uint64_t rem;
+    tPp[j] = tP.div_small(x->aux[j], &rem);
+    if (rem) return set_error(FCN_ERR_PARAM, "internal: aux prime does not divide tP");
+  }
+  for (int i = 0; i < k; ++i) {
+    const uint64_t qi = x->primes[i];
+    for (int j = 0; j < K; ++j) {
+      const uint64_t c = j < k ? alpha[j].mod_small(qi) : tPp[j - k].mod_small(qi);
+      mc->rc[i][j] = c;
+      mc->rc_s[i][j] = h_shoup(c, qi);
+    }
+    const uint64_t tpm = tP.mod_small(qi);
+    for (int v = 0; v <= K + 1; ++v) mc->rvt[i][v] = (qi - h_mulmod(tpm, (uint64_t)v, qi)) % qi;
+    // decrypt
+    mc->tr[i] = t % qi;
+    mc->tq[i] = t / qi;
+    mc->tr_s[i] = h_shoup(mc->tr[i], qi);
+    // digits: 2^(64 m) mod q_i
+    for (int mm = 0; mm < 4; ++mm) {
+      uint64_t pw = 1 % qi;
+      for (int s = 0; s < mm; ++s) pw = (uint64_t)(((unsigned __int128)pw << 64) % qi);
+      mc->dpw[i][mm] = pw;
+      mc->dpw_s[i][mm] = h_shoup(pw, qi);
+    }
+    // add_pt
+    uint64_t dr;
+    const Big delta = q.div_small(t, &dr);
+    mc->delta[i] = delta.mod_small(qi);
+    mc->delta_s[i] = h_shoup(mc->delta[i], qi);
+  }
+  uint64_t qmin = ~0ull;
+  for (uint64_t qi : x->primes) qmin = qi < qmin ? qi : qmin;
+  mc->direct = (mc->w < 64 && ((1ull << mc->w) <= qmin)) ? 1 : 0;
+  mc->dwords = (mc->w + 63) / 64;
+  if (mc->dwords > 3) return set_error(FCN_ERR_PARAM, "log2(beta) = %d exceeds the supported 192 bits", mc->w);
+  return FCN_OK;
+}
+
+// kernel variant dispatch: (max q limbs, max aux limbs)
+enum Variant { V4_5 = 0, V8_8, V16_16 };
+static Variant pick_variant(int k, int m) {
+  if (k <= 4 && m <= 5) return V4_5;
+  if (k <= 8 && m <= 8) return V8_8;
+  return V16_16;
+}
+
+}  // namespace fcn
+
+using namespace fcn;
+
+// ----------------------------------------------------------------- C ABI
+
+extern "C" int fcn_ctx_create(int device, int n, int k, const uint64_t* primes, int n_lanes, const uint64_t* t_lanes,
+                              int log2_beta, fcn_ctx** out) {
+  if (!out || !primes || !t_lanes || k <= 0 || n_lanes <= 0) return set_error(FCN_ERR_ARG, "bad context arguments");
+  if (k > KQ_LIM) return set_error(FCN_ERR_PARAM, "at most %d ciphertext limbs are supported", KQ_LIM);
+  if (n_lanes > LANE_LIM) return set_error(FCN_ERR_PARAM, "at most %d plaintext lanes", LANE_LIM);
+  if (log2_beta < 1 || log2_beta > 190) return set_error(FCN_ERR_PARAM, "log2(beta) must be in [1, 190]");
+  fcn_ctx* x = new fcn_ctx();
+  x->device = device;
+  x->n = n;
+  x->k = k;
+  x->log2_beta = log2_beta;
+  x->n_lanes = n_lanes;
+  x->primes.assign(primes, primes + k);
+  x->lanes.assign(t_lanes, t_lanes + n_lanes);
+  for (int i = 0; i < k; ++i)
+    for (int j = i + 1; j < k; ++j)
+      if (primes[i] == primes[j]) {
+        delete x;
+        return set_error(FCN_ERR_PARAM, "duplicate limb prime");
+      }
+  const Big q = big_prod(x->primes);
+  for (uint64_t t : x->lanes) {
+    if (t < 2) {
+      delete x;
+      return set_error(FCN_ERR_PARAM, "plaintext modulus must be >= 2");
+    }
+    uint64_t r;
+    const Big d = q.div_small(t, &r);
+    if (d.bits() <= 16) {
+      delete x;
+      return set_error(FCN_ERR_PARAM, "ciphertext modulus too small for lane t=%llu", (unsigned long long)t);
+    }
+  }
+  // ell = max e with beta^e <= q  (fv.py:78-85)
+  x->ell = (q.bits() - 1) / log2_beta;
+  // auxiliary base (fv.py:99-107): find_ntt_primes(n, need//54 + 1, bits=55, exclude=q)
+  int nb = 0;
+  while ((1 << nb) <= n) ++nb;
+  const int need = nb + q.bits() + 1;
+  const int count = need / 54 + 1;
+  const uint64_t step = 2ull * (uint64_t)n;
+  uint64_t p = ((1ull << 55) / step) * step + 1;
+  while ((int)x->aux.size() < count) {
+    p += step;
+    bool skip = false;
+    for (uint64_t qq : x->primes) skip |= qq == p;
+    if (!skip && h_is_prime(p)) x->aux.push_back(p);
+  }
+  x->m = count;
+  if (k + count > KE_LIM) {
+    delete x;
+    return set_error(FCN_ERR_PARAM, "extended base of %d limbs exceeds %d", k + count, KE_LIM);
+  }
+  std::vector<uint64_t> ext = x->primes;
+  ext.insert(ext.end(), x->aux.begin(), x->aux.end());
+  int rc = fcn_ring_create(device, n, (int)ext.size(), ext.data(), &x->ext);
+  if (rc) {
+    delete x;
+    return rc;
+  }
+  x->logn = x->ext->logn;
+  std::vector<MulCtConst> host(n_lanes);
+  for (int l = 0; l < n_lanes; ++l) {
+    rc = build_mulct_const(x, x->lanes[l], &host[l]);
+    if (rc) {
+      fcn_ctx_destroy(x);
+      return rc;
+    }
+  }
+  DeviceGuard g(device);
+  cudaError_t e = cudaMalloc(&x->d_mc, sizeof(MulCtConst) * n_lanes);
+  if (e == cudaSuccess) e = cudaMemcpy(x->d_mc, host.data(), sizeof(MulCtConst) * n_lanes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&x->d_fallbacks, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(x->d_fallbacks, 0, sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    fcn_ctx_destroy(x);
+    return check_cuda(e, "fcn_ctx_create upload");
+  }
+  *out = x;
+  return FCN_OK;
+}
+
+extern "C" int fcn_ctx_destroy(fcn_ctx* x) {
+  if (!x) return FCN_OK;
+  {
+    DeviceGuard g(x->device);
+    cudaFree(x->d_mc);
+    cudaFree(x->d_fallbacks);
+  }
+  fcn_ring_destroy(x->ext);
+  delete x;
+  return FCN_OK;
+}
+
+extern "C" int fcn_ctx_ring(const fcn_ctx* x, const fcn_ring** out) {
+  if (!x || !out) return set_error(FCN_ERR_ARG, "null argument");
+  *out = x->ext;
+  return FCN_OK;
+}
+
+extern "C" int fcn_ctx_query(const fcn_ctx* x, int what, int64_t* value) {
+  if (!x || !value) return set_error(FCN_ERR_ARG, "null argument");
+  switch (what) {
+    case 0: *value = x->n; break;
+    case 1: *value = x->k; break;
+    case 2: *value = x->m; break;
+    case 3: *value = x->ell; break;
+    case 4: *value = x->n_lanes; break;
+    case 5: *value = x->log2_beta; break;
+    default: return set_error(FCN_ERR_ARG, "unknown query %d", what);
+  }
+  return FCN_OK;
+}
+
+extern "C" int fcn_ctx_aux_primes(const fcn_ctx* x, uint64_t* out_m) {
+  if (!x || !out_m) return set_error(FCN_ERR_ARG, "null argument");
+  for (int j = 0; j < x->m; ++j) out_m[j] = x->aux[j];
+  return FCN_OK;
+}
+
+extern "C" int fcn_ctx_fallback_count(const fcn_ctx* x, int64_t* value) {
+  if (!x || !value) return set_error(FCN_ERR_ARG, "null argument");
+  DeviceGuard g(x->device);
+  unsigned long long v = 0;
+  FCN_CUDA(cudaMemcpy(&v, x->d_fallbacks, sizeof(v), cudaMemcpyDeviceToHost));
+  *value = (int64_t)v;
+  return FCN_OK;
+}
+
+extern "C" int fcn_keys_create(const fcn_ctx* x, const uint64_t* a, const uint64_t* g, fcn_keys** out) {
+  if (!x || !a || !g || !out) return set_error(FCN_ERR_ARG, "null argument");
+  fcn_keys* kk = new fcn_keys();
+  kk->device = x->device;
+  kk->D = x->ell + 1;
+  kk->k = x->k;
+  kk->n = x->n;
+  const size_t words = (size_t)kk->D * kk->k * kk->n;
+  DeviceGuard gd(x->device);
+  cudaError_t e = cudaMalloc(&kk->d_g, words * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&kk->d_a, words * 8);
+  if (e == cudaSuccess) e = cudaMemcpy(kk->d_g, g, words * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(kk->d_a, a, words * 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    fcn_keys_destroy(kk);
+    return check_cuda(e, "fcn_keys_create upload");
+  }
+  int rc = launch_ntt(x->ext, kk->d_g, (int64_t)kk->D * kk->k, kk->k, 0, true, 0);
+  if (!rc) rc = launch_ntt(x->ext, kk->d_a, (int64_t)kk->D * kk->k, kk->k, 0, true, 0);
+  if (!rc) {
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) rc = check_cuda(e, "fcn_keys_create ntt");
+  }
+  if (rc) {
+    fcn_keys_destroy(kk);
+    return rc;
+  }
+  *out = kk;
+  return FCN_OK;
+}
+
+extern "C" int fcn_keys_destroy(fcn_keys* kk) {
+  if (!kk) return FCN_OK;
+  {
+    DeviceGuard g(kk->device);
+    cudaFree(kk->d_g);
+    cudaFree(kk->d_a);
+  }
+  delete kk;
+  return FCN_OK;
+}
+
+extern "C" int fcn_add_plain_terms(const fcn_ctx* x, int lane, uint64_t* d_cts, int64_t n_terms, const int32_t* d_ct_index,
+                                   const int32_t* d_pos, const int64_t* d_coef, void* stream) {
+  if (!x || lane < 0 || lane >= x->n_lanes) return set_error(FCN_ERR_ARG, "bad context or lane");
+  if (n_terms <= 0) return FCN_OK;
+  if (!d_cts || !d_ct_index || !d_pos || !d_coef) return set_error(FCN_ERR_ARG, "null argument");
+  DeviceGuard g(x->device);
+  const int64_t total = n_terms * x->k;
+  add_plain_kernel<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(d_cts, n_terms, d_ct_index, d_pos, d_coef, x->k,
+                                                                          x->logn, x->d_mc + lane, x->ext->d_lc);
+  FCN_LAUNCH_CHECK("add_plain_kernel");
+  return FCN_OK;
+}
+
+extern "C" int fcn_linear_mac(const fcn_ctx* x, const uint64_t* d_in0, int64_t n_in0, const uint64_t* d_in1, int64_t n_in1,
+                              const int32_t* d_rowptr, const int32_t* d_col, const int32_t* d_rot, const int64_t* d_coef,
+                              uint64_t* d_out, int64_t n_out, void* stream) {
+  if (!x) return set_error(FCN_ERR_ARG, "null context");
+  if (n_out <= 0) return FCN_OK;
+  if (!d_out || !d_rowptr || (n_in0 > 0 && !d_in0) || (n_in1 > 0 && !d_in1))
+    return set_error(FCN_ERR_ARG, "null argument");
+  if (n_out > 65535) return set_error(FCN_ERR_ARG, "at most 65535 outputs per launch");
+  DeviceGuard g(x->device);
+  const int threads = 256;
+  const int per_cta = threads * 2;
+  dim3 grid((x->n + per_cta - 1) / per_cta, (unsigned)n_out, 2 * x->k);
+  mac_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_rot, d_coef, d_out, x->logn,
+                                                         x->k, x->ext->d_lc);
+  FCN_LAUNCH_CHECK("mac_kernel");
+  return FCN_OK;
+}
+
+// workspace per ciphertext in words
+static int64_t mulct_words_per_ct(const fcn_ctx* x) {
+  const int64_t K = x->k + x->m, k = x->k, D = x->ell + 1;
+  return (2 * K + 2 * K + 3 * K + 2 * k + D * k + 2 * k) * (int64_t)x->n;
+}
+
+extern "C" size_t fcn_mul_ct_workspace_bytes(const fcn_ctx* x, int64_t chunk) {
+  if (!x || chunk <= 0) return 0;
+  return (size_t)(mulct_words_per_ct(x) * chunk * 8);
+}
+
+template <int KQ, int KA>
+static void launch_lift(const uint64_t* in, uint64_t* ext, int64_t npoly, const fcn_ctx* x, const MulCtConst* mc,
+                        cudaStream_t st) {
+  const int64_t total = npoly << x->logn;
+  lift_kernel<KQ, KA, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, ext, npoly, x->logn, mc, x->ext->d_lc,
+                                                                     x->d_fallbacks);
+}
+
+template <int KQ, int KE>
+static void launch_rescale(const uint64_t* T, uint64_t* R01, uint64_t* DG, int64_t C, const fcn_ctx* x,
+                           const MulCtConst* mc, cudaStream_t st) {
+  const int64_t total = (C * 3) << x->logn;
+  rescale_kernel<KQ, KE, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(T, R01, DG, C, x->logn, mc, x->ext->d_lc,
+                                                                        x->d_fallbacks);
+}
+
+extern "C" int fcn_mul_ct(const fcn_ctx* x, const fcn_keys* keys, int lane, const uint64_t* d_a, const uint64_t* d_b,
+                          uint64_t* d_out, int64_t count, void* d_workspace, size_t workspace_bytes, void* stream) {
+  if (!x || !keys) return set_error(FCN_ERR_ARG, "null context or keys");
+  if (lane < 0 || lane >= x->n_lanes) return set_error(FCN_ERR_ARG, "lane %d out of range", lane);
+  if (count <= 0) return FCN_OK;
+  if (!d_a || !d_out || !d_workspace) return set_error(FCN_ERR_ARG, "null buffer");
+  if (keys->k != x->k || keys->n != x->n || keys->D != x->ell + 1) return set_error(FCN_ERR_ARG, "keys do not match context");
+  const int64_t per = mulct_words_per_ct(x);
+  const int64_t chunk_max = (int64_t)(workspace_bytes / 8) / per;
+  if (chunk_max < 1) return set_error(FCN_ERR_STATE, "workspace too small (%zu bytes; need %lld per ciphertext)", workspace_bytes, (long long)(per * 8));
+  DeviceGuard gd(x->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int k = x->k, K = x->k + x->m, D = x->ell + 1, n = x->n, logn = x->logn;
+  const MulCtConst* mc = x->d_mc + lane;
+  const Variant var = pick_variant(k, x->m);
+  const int64_t ct_words = 2LL * k * n;
+  for (int64_t off = 0; off < count; off += chunk_max) {
+    const int64_t C = (count - off) < chunk_max ? (count - off) : chunk_max;
+    uint64_t* ws = (uint64_t*)d_workspace;
+    uint64_t* EA = ws;
+    uint64_t* EB = EA + C * 2 * K * n;
+    uint64_t* T = EB + C * 2 * K * n;
+    uint64_t* R01 = T + C * 3 * K * n;
+    uint64_t* DG = R01 + C * 2 * k * n;
+    uint64_t* ACC = DG + C * D * k * n;
+    const uint64_t* a = d_a + off * ct_words;
+    const uint64_t* b = d_b ? d_b + off * ct_words : nullptr;
+    // (i) lift + forward NTT over the extended base
+    for (int which = 0; which < (b ? 2 : 1); ++which) {
+      const uint64_t* src = which ? b : a;
+      uint64_t* dst = which ? EB : EA;
+      switch (var) {
+        case V4_5: launch_lift<4, 5>(src, dst, C * 2, x, mc, st); break;
+        case V8_8: launch_lift<8, 8>(src, dst, C * 2, x, mc, st); break;
+        default: launch_lift<16, 16>(src, dst, C * 2, x, mc, st); break;
+      }
+      FCN_LAUNCH_CHECK("lift_kernel");
+      int rc = launch_ntt(x->ext, dst, C * 2 * K, K, 0, true, st);
+      if (rc) return rc;
+    }
+    // (ii) tensor, (iii) inverse NTT
+    tensor_kernel<<<grid_for((C * K) << logn, 256), 256, 0, st>>>(EA, b ? EB : nullptr, T, C, K, logn, x->ext->d_lc);
+    FCN_LAUNCH_CHECK("tensor_kernel");
+    int rc = launch_ntt(x->ext, T, C * 3 * K, K, 0, false, st);
+    if (rc) return rc;
+    // (iv) exact rescale + digit decomposition
+    switch (var) {
+      case V4_5: launch_rescale<4, 9>(T, R01, DG, C, x, mc, st); break;
+      case V8_8: launch_rescale<8, 16>(T, R01, DG, C, x, mc, st); break;
+      default: launch_rescale<16, 32>(T, R01, DG, C, x, mc, st); break;
+    }
+    FCN_LAUNCH_CHECK("rescale_kernel");
+    // (v) digits to NTT, key MAC, (vi) inverse NTT + add
+    rc = launch_ntt(x->ext, DG, C * D * k, k, 0, true, st);
+    if (rc) return rc;
+    keymac_kernel<<<grid_for((C * k) << logn, 256), 256, 0, st>>>(DG, keys->d_g, keys->d_a, ACC, C, D, k, logn, x->ext->d_lc);
+    FCN_LAUNCH_CHECK("keymac_kernel");
+    rc = launch_ntt(x->ext, ACC, C * 2 * k, k, 0, false, st);
+    if (rc) return rc;
+    const int64_t tot = (C * 2 * k) << logn;
+    add_rows_kernel<<<grid_for(tot, 256), 256, 0, st>>>(R01, ACC, d_out + off * ct_words, tot, logn, k, x->ext->d_lc);
+    FCN_LAUNCH_CHECK("add_rows_kernel");
+  }
+  return FCN_OK;
+}
+
+extern "C" int fcn_decrypt_round(const fcn_ctx* x, int lane, const uint64_t* d_w, uint64_t* d_m, int64_t count, void* stream) {
+  if (!x || lane < 0 || lane >= x->n_lanes) return set_error(FCN_ERR_ARG, "bad context or lane");
+  if (count <= 0) return FCN_OK;
+  if (!d_w || !d_m) return set_error(FCN_ERR_ARG, "null buffer");
+  DeviceGuard g(x->device);
+  const int64_t total = count << x->logn;
+  cudaStream_t st = (cudaStream_t)stream;
+  const MulCtConst* mc = x->d_mc + lane;
+  if (x->k <= 4)
+    decrypt_round_kernel<4, 6><<<grid_for(total, 256), 256, 0, st>>>(d_w, d_m, count, x->logn, mc, x->ext->d_lc, x->d_fallbacks);
+  else if (x->k <= 8)
+    decrypt_round_kernel<8, 10><<<grid_for(total, 256), 256, 0, st>>>(d_w, d_m, count, x->logn, mc, x->ext->d_lc, x->d_fallbacks);
+  else
+    decrypt_round_kernel<16, 18><<<grid_for(total, 256), 256, 0, st>>>(d_w, d_m, count, x->logn, mc, x->ext->d_lc, x->d_fallbacks);
+  FCN_LAUNCH_CHECK("decrypt_round_kernel");
+  return FCN_OK;
+}

@@ -1,0 +1,510 @@
+"""Encrypted evaluation of a compiled network on B200 (mirrors reference engine.py).
+
+`eval_encrypted(net, tensor, ek, cfg, workers=1)` keeps the reference
+signature and semantics (engine.py:651-774): it compiles the same integer
+plan (`netplan.compile_network`), tallies the same HOP counters, carries the
+same scale / factor / depth metadata, and produces ciphertexts that are
+bit-identical to the reference evaluator's.  Instead of one `fv.*` call per
+HOP it issues one fused kernel per layer:
+
+  * linear layer / pool:  `fcn_linear_mac` -- every (tap x encoded-term)
+    becomes a signed monomial term c * x^r applied to an input ciphertext
+    and accumulated exactly (mul_pt + add_ct chain, engine.py:698-743),
+    then `fcn_add_plain_terms` for the bias (add_pt, engine.py:713-715);
+  * activation: `fcn_mul_ct` on all nodes (square + relinearisation), then
+    one `fcn_linear_mac` over [sq ; x] for a2*sq + a1*x, then add_pt(a0)
+    (engine.py:747-768).
+
+Plaintext constants are encoded as in the reference (`encoding="integer"`:
+base-2 encoder, a +-1 term per set bit at x^bit) or, for the SIMD-batched
+configurations, as constant polynomials (`encoding="batched"`: one term
+c = centered(z mod t) at x^0).  A CipherTensor holds one [B][2][k][n]
+device buffer -- byte-identical to the serialized ciphertext bodies.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from . import device as dev
+from . import fv
+from .encode import FixedPointConfig, decode_fixed, encode_integer, integer_bits, round_half_away
+from .fv import Ciphertext, EncryptionParams, EvalKeys, FVError, PublicKey, SecretKey
+from .netplan import (  # noqa: F401  (re-exported: reference engine API surface)
+    ActPlan,
+    BatchNormAffine,
+    CompiledNet,
+    Conv2d,
+    Dense,
+    EngineError,
+    HopCounter,
+    LayerCounts,
+    LinearOut,
+    LinearPlan,
+    NetworkSpec,
+    PolyActivation,
+    PolyApprox,
+    PoolPlan,
+    ScaledAvgPool,
+    TapPlan,
+    compile_network,
+    fold_batchnorm,
+    int_is_monomial,
+    plan_hops,
+    project_hops,
+    square_activation,
+)
+
+ENCODINGS = ("integer", "batched")
+
+
+# ----------------------------------------------------------------- tensors
+
+
+class CipherTensor:
+    """Grid of ciphertexts sharing lane and scale (engine.py:592-607).
+
+    `buf` is a [count][2][k][n] device buffer; `depths` the per-element
+    multiplicative depth (host int array)."""
+
+    def __init__(self, shape, cts=None, scale_exponent: int = 0, scale_factor: int = 1, *, buf=None, params=None,
+                 lane: int = 0, depths=None):
+        self.shape = tuple(int(d) for d in shape)
+        count = int(np.prod(self.shape))
+        if cts is not None:
+            cts = list(cts)
+            if len(cts) != count:
+                raise EngineError("ciphertext count does not match tensor shape")
+            import torch
+
+            params = cts[0].params
+            lane = cts[0].lane
+            buf = torch.stack([torch.stack([c.c0.data, c.c1.data]) for c in cts]).contiguous()
+            depths = np.array([c.mul_depth for c in cts], dtype=np.int64)
+        if buf is None or params is None:
+            raise EngineError("CipherTensor needs ciphertexts or a device buffer with params")
+        if buf.shape[0] != count:
+            raise EngineError("ciphertext count does not match tensor shape")
+        self.buf = buf
+        self.params = params
+        self.lane = int(lane)
+        self.scale_exponent = int(scale_exponent)
+        self.scale_factor = int(scale_factor)
+        self.depths = np.zeros(count, dtype=np.int64) if depths is None else np.asarray(depths, dtype=np.int64)
+
+    @property
+    def cts(self) -> list:
+        return [
+            fv.ciphertext_from_buffer(self.params, self.buf[i], self.lane, self.scale_exponent, int(self.depths[i]))
+            for i in range(self.buf.shape[0])
+        ]
+
+    def __len__(self):
+        return self.buf.shape[0]
+
+    def host_bodies(self) -> np.ndarray:
+        """[count][2][k][n] uint64 host copy (the serialized bodies)."""
+        return dev.to_host(self.buf)
+
+
+def encrypt_tensor(pk: PublicKey, params: EncryptionParams, values, cfg: FixedPointConfig, lane: int = 0, rng=None) -> CipherTensor:
+    """One ciphertext per scalar, base-2 integer encoding (engine.py:610-627).
+
+    Byte-identical to the reference for the same rng (same draw order)."""
+    values = np.asarray(values, dtype=np.float64)
+    rng = rng if isinstance(rng, np.random.Generator) else np.random.default_rng(rng)
+    t = int(params.t_lanes[lane])
+    zs = [round_half_away(float(v) * (1 << cfg.precision_bits)) for v in values.ravel()]
+    width = max([1] + [abs(z).bit_length() for z in zs])
+    if width > params.n:
+        raise FVError("plaintext degree exceeds ring degree")
+    cen = np.zeros((len(zs), width), dtype=np.int64)
+    for i, z in enumerate(zs):
+        if z:
+            cen[i, integer_bits(z)] = 1 if z > 0 else -1
+    buf = fv.encrypt_batch(pk, params, cen, lane, rng)
+    return CipherTensor(tuple(values.shape), scale_exponent=cfg.precision_bits, buf=buf, params=params, lane=lane)
+
+
+# ------------------------------------------------------------- slot encoder
+
+
+def _t_ring(params: EncryptionParams, lane: int):
+    from .ring import RingContext
+
+    return RingContext.create(params.n, (int(params.t_lanes[lane]),))
+
+
+def slot_encode(params: EncryptionParams, slots: np.ndarray, lane: int = 0) -> np.ndarray:
+    """(count, <=n) slot integers -> (count, n) centered plaintext coefficients.
+
+    Plaintext = inverse negacyclic NTT over Z_t of the slot vector (SURVEY
+    sec. 0.5); runs in libfcn over the t-ring."""
+    t = int(params.t_lanes[lane])
+    s = np.asarray(slots, dtype=np.int64)
+    count = s.shape[0]
+    full = np.zeros((count, params.n), dtype=np.int64)
+    full[:, : s.shape[1]] = np.mod(s, t)
+    tr = _t_ring(params, lane)
+    d = dev.to_device(full)
+    _lib.check(_lib.lib().fcn_ntt_inverse(tr.handle().ptr, d.data_ptr(), count, 1, 0, dev.stream_ptr()), FVError)
+    coeffs = dev.to_host(d).astype(np.int64)
+    return np.where(coeffs > t // 2, coeffs - t, coeffs)
+
+
+def slot_decode(params: EncryptionParams, plain: np.ndarray, lane: int = 0) -> np.ndarray:
+    """(count, n) plaintext coefficients mod t -> (count, n) slot values in [0, t)."""
+    t = int(params.t_lanes[lane])
+    d = dev.to_device(np.mod(np.asarray(plain, dtype=np.int64), t))
+    tr = _t_ring(params, lane)
+    _lib.check(_lib.lib().fcn_ntt_forward(tr.handle().ptr, d.data_ptr(), d.shape[0], 1, 0, dev.stream_ptr()), FVError)
+    return dev.to_host(d).astype(np.int64)
+
+
+def encrypt_tensor_batched(pk: PublicKey, params: EncryptionParams, values, cfg: FixedPointConfig, lane: int = 0, rng=None) -> CipherTensor:
+    """SIMD batch: values (*shape, slots); element e's ciphertext packs
+    round_half_away(v * 2^prec) mod t of every slot (engine.py:623 rule)."""
+    values = np.asarray(values)
+    shape = values.shape[:-1]
+    flat = values.reshape(-1, values.shape[-1])
+    if np.issubdtype(flat.dtype, np.integer):
+        z = flat.astype(np.int64) << cfg.precision_bits
+    else:
+        v = flat.astype(np.float64) * float(1 << cfg.precision_bits)
+        mag = np.floor(np.abs(v) + 0.5)
+        z = np.where(v >= 0, mag, -mag).astype(np.int64)
+    cen = slot_encode(params, z, lane)
+    rng = rng if isinstance(rng, np.random.Generator) else np.random.default_rng(rng)
+    buf = fv.encrypt_batch(pk, params, cen, lane, rng)
+    return CipherTensor(shape, scale_exponent=cfg.precision_bits, buf=buf, params=params, lane=lane)
+
+
+def decrypt_tensor(sk: SecretKey, tensor: CipherTensor) -> list:
+    """Per-element PlainPoly (engine.py:630-631)."""
+    t = int(tensor.params.t_lanes[tensor.lane])
+    ms = fv.decrypt_batch(sk, tensor.params, tensor.buf, tensor.lane)
+    return [fv.PlainPoly(t, m) for m in ms]
+
+
+def decrypt_tensor_slots(sk: SecretKey, tensor: CipherTensor) -> np.ndarray:
+    """Batched mode: (count, n) decrypted slot values in [0, t)."""
+    ms = fv.decrypt_batch(sk, tensor.params, tensor.buf, tensor.lane)
+    return slot_decode(tensor.params, ms.astype(np.int64), tensor.lane)
+
+
+def decode_lane_outputs(lane_plaintexts, tensor_shape, scale_exponent, scale_factor, cfg) -> np.ndarray:
+    """Per-lane decrypted grids -> real-valued tensor (engine.py:634-648)."""
+    count = int(np.prod(tensor_shape))
+    out = np.zeros(count)
+    for i in range(count):
+        out[i] = decode_fixed([lane[i] for lane in lane_plaintexts], scale_exponent, cfg, scale_factor)
+    return out.reshape(tensor_shape)
+
+
+# ------------------------------------------------------------ plan lowering
+
+
+def const_terms(z: int, t: int, n: int, encoding: str) -> list:
+    """Signed monomial terms (rot, coef) of the plaintext encoding integer z.
+
+    integer: encode_integer(z) (encode.py:64-78) -> +-1 at each set bit;
+    batched: PlainPoly(t, [z mod t]) -> centered(z mod t) at x^0."""
+    z = int(z)
+    if encoding == "batched":
+        c = z % t
+        if c == 0:
+            raise FVError("zero plaintext multiplier: elide the operation instead")
+        return [(0, c - t if c > t // 2 else c)]
+    if z == 0:
+        raise FVError("zero plaintext multiplier: elide the operation instead")
+    bits = integer_bits(z)
+    if bits[-1] >= n:
+        raise FVError("plaintext degree exceeds ring degree")
+    s = 1 if z > 0 else -1
+    return [(b, s) for b in bits]
+
+
+def plain_terms(z: int, t: int, n: int, encoding: str) -> list:
+    """(pos, coef) of the plaintext added by add_pt(encode(z)); [] when zero."""
+    z = int(z)
+    if encoding == "batched":
+        c = z % t
+        return [] if c == 0 else [(0, c - t if c > t // 2 else c)]
+    if z == 0:
+        return []
+    bits = integer_bits(z)
+    if bits[-1] >= n:
+        raise FVError("plaintext degree exceeds ring degree")
+    s = 1 if z > 0 else -1
+    return [(b, s) for b in bits]
+
+
+@dataclass
+class _Mac:
+    rowptr: object
+    col: object
+    rot: object
+    coef: object
+    n_out: int
+    n_terms: int
+
+
+@dataclass
+class _Bias:
+    ct_index: object
+    pos: object
+    coef: object
+    n_terms: int
+
+
+def _upload_mac(rowptr, col, rot, coef) -> _Mac:
+    import torch
+
+    d = "cuda"
+    return _Mac(
+        torch.as_tensor(np.asarray(rowptr, dtype=np.int32), device=d),
+        torch.as_tensor(np.asarray(col, dtype=np.int32) if len(col) else np.zeros(1, np.int32), device=d),
+        torch.as_tensor(np.asarray(rot, dtype=np.int32) if len(rot) else np.zeros(1, np.int32), device=d),
+        torch.as_tensor(np.asarray(coef, dtype=np.int64) if len(coef) else np.zeros(1, np.int64), device=d),
+        len(rowptr) - 1,
+        len(col),
+    )
+
+
+def _upload_bias(idx, pos, coef) -> _Bias | None:
+    import torch
+
+    if not idx:
+        return None
+    d = "cuda"
+    return _Bias(
+        torch.as_tensor(np.asarray(idx, dtype=np.int32), device=d),
+        torch.as_tensor(np.asarray(pos, dtype=np.int32), device=d),
+        torch.as_tensor(np.asarray(coef, dtype=np.int64), device=d),
+        len(idx),
+    )
+
+
+def _lower_linear(plan: LinearPlan, t: int, n: int, encoding: str):
+    """CSR of monomial terms for a LinearPlan (vectorised for big layers)."""
+    outs = plan.outputs
+    counts = np.array([len(o.taps) for o in outs], dtype=np.int64)
+    cols = np.fromiter((tp.in_index for o in outs for tp in o.taps), dtype=np.int64, count=int(counts.sum()))
+    wts = [tp.weight_int for o in outs for tp in o.taps]
+    small = all(abs(w) < (1 << 62) for w in wts)
+    if encoding == "batched" and small:
+        w = np.asarray(wts, dtype=np.int64)
+        c = np.mod(w, t)
+        if np.any(c == 0):
+            raise FVError("zero plaintext multiplier: elide the operation instead")
+        coef = np.where(c > t // 2, c - t, c)
+        rowptr = np.concatenate([[0], np.cumsum(counts)])
+        mac = (rowptr, cols, np.zeros_like(cols), coef)
+    else:
+        rowptr = [0]
+        col, rot, coef = [], [], []
+        k = 0
+        for o in outs:
+            for tp in o.taps:
+                for r, c in const_terms(tp.weight_int, t, n, encoding):
+                    col.append(tp.in_index)
+                    rot.append(r)
+                    coef.append(c)
+                k += 0
+            rowptr.append(len(col))
+        mac = (rowptr, col, rot, coef)
+    bidx, bpos, bcoef = [], [], []
+    for o_i, o in enumerate(outs):
+        if o.bias_int is not None:
+            for p, c in plain_terms(o.bias_int, t, n, encoding):
+                bidx.append(o_i)
+                bpos.append(p)
+                bcoef.append(c)
+    return _upload_mac(*mac), _upload_bias(bidx, bpos, bcoef)
+
+
+def _lower_pool(plan: PoolPlan, t: int, n: int, encoding: str):
+    rterms = [(0, 1)] if plan.reciprocal_int is None else const_terms(plan.reciprocal_int, t, n, encoding)
+    rowptr, col, rot, coef = [0], [], [], []
+    for idxs in plan.outputs:
+        for i in idxs:
+            for r, c in rterms:
+                col.append(i)
+                rot.append(r)
+                coef.append(c)
+        rowptr.append(len(col))
+    return _upload_mac(rowptr, col, rot, coef), None
+
+
+def _lower_act(plan: ActPlan, t: int, n: int, encoding: str):
+    """MAC over [sq ; x]: a2 * sq[o] + a1 * x[o]; bias terms for a0."""
+    a2 = [(0, 1)] if plan.a2_int is None else const_terms(plan.a2_int, t, n, encoding)
+    a1 = [] if plan.a1_mult_int is None else const_terms(plan.a1_mult_int, t, n, encoding)
+    N = plan.nodes
+    per = len(a2) + len(a1)
+    o = np.arange(N, dtype=np.int64)
+    col = np.concatenate([np.repeat(o[:, None], len(a2), 1), np.repeat(o[:, None] + N, len(a1), 1)], axis=1).ravel()
+    rot = np.tile(np.array([r for r, _ in a2] + [r for r, _ in a1], dtype=np.int64), N)
+    coef = np.tile(np.array([c for _, c in a2] + [c for _, c in a1], dtype=np.int64), N)
+    rowptr = np.arange(N + 1, dtype=np.int64) * per
+    bidx, bpos, bcoef = [], [], []
+    if plan.a0_add_int is not None:
+        pt = plain_terms(plan.a0_add_int, t, n, encoding)
+        for i in range(N):
+            for p, c in pt:
+                bidx.append(i)
+                bpos.append(p)
+                bcoef.append(c)
+    identity = plan.a2_int is None and plan.a1_mult_int is None
+    return _upload_mac(rowptr, col, rot, coef), _upload_bias(bidx, bpos, bcoef), identity
+
+
+_lower_cache: dict = {}
+
+
+def _lowered(compiled: CompiledNet, t: int, n: int, encoding: str):
+    key = (id(compiled), t, n, encoding, dev.current_device())
+    hit = _lower_cache.get(key)
+    if hit is not None and hit[0] is compiled:
+        return hit[1]
+    low = []
+    for plan in compiled.plans:
+        if isinstance(plan, LinearPlan):
+            low.append(("linear",) + _lower_linear(plan, t, n, encoding))
+        elif isinstance(plan, PoolPlan):
+            low.append(("pool",) + _lower_pool(plan, t, n, encoding))
+        elif isinstance(plan, ActPlan):
+            low.append(("act",) + _lower_act(plan, t, n, encoding))
+        else:
+            raise EngineError(f"unknown plan {type(plan).__name__}")
+    _lower_cache[key] = (compiled, low)
+    return low
+
+
+# ------------------------------------------------------------------ kernels
+
+
+def _run_mac(params, in0, in1, mac: _Mac, out):
+    h = params.native()
+    n_in0 = in0.shape[0]
+    n_in1 = in1.shape[0] if in1 is not None else 0
+    _lib.check(
+        _lib.lib().fcn_linear_mac(
+            h.ptr, in0.data_ptr(), n_in0, in1.data_ptr() if in1 is not None else None, n_in1, mac.rowptr.data_ptr(),
+            mac.col.data_ptr(), mac.rot.data_ptr(), mac.coef.data_ptr(), out.data_ptr(), mac.n_out, dev.stream_ptr(),
+        ),
+        FVError,
+    )
+
+
+def _run_bias(params, lane, buf, bias: _Bias | None):
+    if bias is None:
+        return
+    _lib.check(
+        _lib.lib().fcn_add_plain_terms(
+            params.native().ptr, lane, buf.data_ptr(), bias.n_terms, bias.ct_index.data_ptr(), bias.pos.data_ptr(),
+            bias.coef.data_ptr(), dev.stream_ptr(),
+        ),
+        FVError,
+    )
+
+
+def _mac_out(params, mac: _Mac, in0, in1):
+    out = dev.empty((mac.n_out, 2, len(params.limb_primes), params.n))
+    for lo in range(0, mac.n_out, 65535):
+        hi = min(mac.n_out, lo + 65535)
+        if lo == 0 and hi == mac.n_out:
+            _run_mac(params, in0, in1, mac, out)
+        else:  # split launches over output rows (grid.y limit)
+            sub = _Mac(mac.rowptr[lo : hi + 1], mac.col, mac.rot, mac.coef, hi - lo, mac.n_terms)
+            _run_mac(params, in0, in1, sub, out[lo:hi])
+    return out
+
+
+# --------------------------------------------------------------- evaluator
+
+
+def _depths_linear(plan_outputs, depths):
+    out = np.zeros(len(plan_outputs), dtype=np.int64)
+    for i, o in enumerate(plan_outputs):
+        idx = [tp.in_index for tp in o.taps] if hasattr(o, "taps") else list(o)
+        out[i] = depths[idx].max() if idx else 0
+    return out
+
+
+def eval_encrypted(net, tensor: CipherTensor, ek: EvalKeys, cfg: FixedPointConfig, workers: int = 1,
+                   encoding: str = "integer", mul_chunk: int | None = None):
+    """Execute the compiled plan over a ciphertext tensor, tallying every HOP.
+
+    Same contract as reference engine.eval_encrypted (engine.py:651-774);
+    `workers` is accepted for API compatibility (the GPU parallelises
+    every layer's outputs).  `encoding` selects the plaintext encoding of
+    the integer constants ("integer" = the reference's base-2 encoder;
+    "batched" = constant polynomials for SIMD-packed slots)."""
+    if encoding not in ENCODINGS:
+        raise EngineError(f"encoding must be one of {ENCODINGS}")
+    if not isinstance(tensor, CipherTensor):
+        raise EngineError("tensor must be a CipherTensor")
+    import torch
+
+    params = tensor.params
+    lane = tensor.lane
+    t = int(params.t_lanes[lane])
+    if int(cfg.t_lanes[lane]) != t:
+        raise EngineError("fixed-point lane configuration disagrees with ciphertexts")
+    acts = sum(type(l).__name__ == "PolyActivation" for l in net.layers)
+    if acts > params.mul_depth_budget:
+        raise EngineError(f"{acts} activations exceed the parameter depth budget {params.mul_depth_budget}")
+    compiled = compile_network(net, cfg) if not isinstance(net, CompiledNet) else net
+    counter = plan_hops(compiled, encoding, t)
+    low = _lowered(compiled, t, params.n, encoding)
+    prec = cfg.precision_bits
+    cur = tensor.buf
+    depths = tensor.depths.copy()
+    scale = tensor.scale_exponent
+    factor = tensor.scale_factor
+    events = []
+    for plan, lw in zip(compiled.plans, low):
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        kind = lw[0]
+        if kind == "linear":
+            _, mac, bias = lw
+            nxt = _mac_out(params, mac, cur, None)
+            _run_bias(params, lane, nxt, bias)
+            depths = _depths_linear(plan.outputs, depths)
+            scale += prec
+        elif kind == "pool":
+            _, mac, _ = lw
+            nxt = _mac_out(params, mac, cur, None)
+            depths = _depths_linear(plan.outputs, depths)
+            if plan.reciprocal_int is not None:
+                scale += prec
+            else:
+                scale += plan.pow2_shift
+                factor *= plan.factor_mult
+        else:
+            _, mac, bias, identity = lw
+            sq = fv.mul_ct_batch(params, ek, lane, cur, None, chunk=mul_chunk)
+            if identity:
+                nxt = sq
+            else:
+                nxt = _mac_out(params, mac, sq, cur)
+            _run_bias(params, lane, nxt, bias)
+            depths = depths + 1
+            scale = 2 * scale + plan.scale_bump
+            factor = factor * factor
+        ev1.record()
+        events.append((ev0, ev1))
+        cur = nxt
+    torch.cuda.current_stream().synchronize()
+    for c, (a, b) in zip(counter.layer_counts, events):
+        c.wall_ms = a.elapsed_time(b)
+    out = CipherTensor(compiled.out_shape, scale_exponent=scale, scale_factor=factor, buf=cur, params=params, lane=lane,
+                       depths=depths)
+    return out, counter

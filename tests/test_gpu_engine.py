@@ -1,0 +1,202 @@
+"""GPU parity of the drop-in evaluator `engine.eval_encrypted` (both
+encodings) against the reference golden run and the CPU oracle drivers."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import bfv as ob  # noqa: E402
+from oracle import drivers as od  # noqa: E402
+from oracle import rns as orn  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def E():
+    import torch
+
+    from paper_1811_09953_b200 import engine
+
+    assert torch.cuda.is_available()
+    return engine
+
+
+def _tiny_net(E, meta):
+    conv = E.Conv2d(np.array(meta["conv_w"]), np.array(meta["conv_b"]), 1, 0)
+    c0, c1, c2 = meta["act"]
+    act = E.PolyActivation(E.PolyApprox(2, (c0, c1, c2)))
+    pool = E.ScaledAvgPool(2, stride=1, padding=1)
+    dense = E.Dense(np.array(meta["dense_w"]), np.array(meta["dense_b"]))
+    return E.NetworkSpec((1, 4, 4), [conv, act, pool, dense])
+
+
+def test_integer_mode_matches_reference_run(E, golden_meta, golden_npz):
+    """The reference's own eval_encrypted on the tiny params (integer encoder,
+    non-monomial weights, pooling with single-element windows, an empty
+    dense row with bias) -- output ciphertexts byte-identical."""
+    from paper_1811_09953_b200 import device as dev
+    from paper_1811_09953_b200 import fv
+    from paper_1811_09953_b200.encode import FixedPointConfig
+
+    d = golden_npz("engine_tiny")
+    em = golden_meta["engine_tiny"]
+    m = golden_meta["fv"]["tiny"]
+    P = fv.EncryptionParams(m["n"], tuple(m["primes"]), tuple(m["t_lanes"]), m["beta"])
+    sk, pk, ek = fv.keygen(P, 42)
+    cfg = FixedPointConfig(tuple(m["t_lanes"]), em["prec"])
+    net = _tiny_net(E, em)
+    # encryption path is byte-identical too
+    tensor = E.encrypt_tensor(pk, P, d["x"], cfg, 0, np.random.default_rng(22))
+    assert np.array_equal(tensor.host_bodies(), d["in_cts"])
+    out, counter = E.eval_encrypted(net, tensor, ek, cfg)
+    assert np.array_equal(out.host_bodies(), d["out_cts"])
+    assert out.scale_exponent == em["out_scale"] and out.scale_factor == em["out_factor"]
+    meta = np.array([[out.lane, out.scale_exponent, int(dd)] for dd in out.depths])
+    assert np.array_equal(meta, d["out_meta"])
+    assert [list(r[:5]) + [r[6]] for r in counter.rows()] == em["hops"]
+    assert counter.same_ops(E.project_hops(net, cfg))
+    plains = E.decrypt_tensor(sk, out)
+    dec = E.decode_lane_outputs([plains], out.shape, out.scale_exponent, out.scale_factor, cfg)
+    assert np.allclose(dec, d["decoded"], rtol=0, atol=0)
+    # reference-style list API round trip
+    again = E.CipherTensor(out.shape, out.cts, out.scale_exponent, out.scale_factor)
+    assert np.array_equal(again.host_bodies(), d["out_cts"])
+
+
+def _small_batched_setup(E, fv):
+    n = 1024
+    from oracle import nt
+
+    primes = tuple(nt.ntt_primes(n, 3, bits=36))
+    P = fv.EncryptionParams(n, primes, (65537,))
+    OP = ob.Params(n, primes, (65537,), P.beta)
+    L = E
+    rng = np.random.default_rng(4)
+    conv_w = rng.choice([0.0, 0.25, -0.5, 1.0, -0.125], size=(2, 1, 3, 3), p=[0.5, 0.15, 0.15, 0.1, 0.1])
+    dense_w = rng.choice([0.0, 0.5, -0.25, 1.0], size=(3, 8), p=[0.4, 0.2, 0.2, 0.2])
+    dense_w[2] = 0.0  # an empty row with a bias
+    net = L.NetworkSpec(
+        (1, 4, 4),
+        [
+            L.Conv2d(conv_w, np.array([0.5, -0.25]), 1, 0),
+            L.PolyActivation(L.PolyApprox(2, (0.0625, 0.5, 0.125))),
+            L.ScaledAvgPool(2, stride=1, padding=0),
+            L.Dense(dense_w, np.array([0.25, -1.0, 0.5])),
+            L.PolyActivation(L.square_activation()),
+        ],
+    )
+    return P, OP, net
+
+
+def test_batched_mode_matches_oracle_and_plain_model(E):
+    from paper_1811_09953_b200 import device as dev
+    from paper_1811_09953_b200 import fv
+    from paper_1811_09953_b200.encode import FixedPointConfig
+
+    P, OP, net = _small_batched_setup(E, fv)
+    cfg = FixedPointConfig((65537,), 4)
+    sk, pk, ek = fv.keygen(P, 2)
+    K = ob.Keys(sk.s.host(), pk.p0.host(), pk.p1.host(), [x.host() for x in ek.a], [x.host() for x in ek.g])
+    x = np.random.default_rng(0).integers(0, 16, (16, P.n))
+    tensor = E.encrypt_tensor_batched(pk, P, x.reshape(1, 4, 4, P.n), cfg, 0, 3)
+    out, counter = E.eval_encrypted(net, tensor, ek, cfg, encoding="batched")
+    comp = E.compile_network(net, cfg)
+    bodies = tensor.host_bodies()
+    cts = [ob.Ct(b[0], b[1], 0, cfg.precision_bits, 0) for b in bodies]
+    want, scale, factor = od.run_plan(OP, comp, cts, K, cfg.precision_bits, "batched")
+    assert np.array_equal(out.host_bodies(), np.stack([np.stack([c.c0, c.c1]) for c in want]))
+    assert list(out.depths) == [c.depth for c in want]
+    assert out.scale_exponent == scale and out.scale_factor == factor
+    slots = E.decrypt_tensor_slots(sk, out)
+    model = od.plain_model_batched(comp, x << cfg.precision_bits, 65537)
+    assert np.array_equal(slots, model)
+    tot = counter.totals
+    assert tot.fast_path_hits == tot.pt_ct_mul
+
+
+def test_cfg1_full_network(E):
+    """cfg1 (BASELINE configs[0], the reference's CPU-runnable case) in full:
+    784 inputs x 4096 slots, dense 784->100 + x^2.  Ciphertexts bit-exact vs
+    the oracle evaluator on 8 sampled outputs; all 100 decrypted outputs
+    equal the slot-wise mod-t integer model."""
+    from paper_1811_09953_b200 import configs
+    from paper_1811_09953_b200 import fv
+
+    W = configs.WORKLOADS["cfg1"]
+    P = fv.EncryptionParams(W.n, W.primes, (W.t,), W.beta)
+    OP = ob.Params(W.n, W.primes, (W.t,), W.beta)
+    cfg = W.fixed_point()
+    net = configs.build_network("cfg1")
+    sk, pk, ek = fv.keygen(P, configs.SEED_KEYS)
+    x = configs.build_inputs("cfg1")
+    tensor = E.encrypt_tensor_batched(pk, P, x, cfg, 0, configs.SEED_ENC)
+    out, counter = E.eval_encrypted(net, tensor, ek, cfg, encoding="batched")
+    comp = E.compile_network(net, cfg)
+    slots = E.decrypt_tensor_slots(sk, out)
+    assert np.array_equal(slots, od.plain_model_batched(comp, x << cfg.precision_bits, W.t))
+    K = ob.Keys(sk.s.host(), pk.p0.host(), pk.p1.host(), [a.host() for a in ek.a], [g.host() for g in ek.g])
+    bodies = tensor.host_bodies()
+    lin = comp.plans[0]
+    got = out.host_bodies()
+    for o in np.random.default_rng(1).choice(100, 8, replace=False):
+        acc = None
+        for tp in lin.outputs[o].taps:
+            term = ob.mul_pt(OP, ob.Ct(bodies[tp.in_index, 0], bodies[tp.in_index, 1], 0, 6), [tp.weight_int % W.t], 6)
+            acc = term if acc is None else ob.add_ct(OP, acc, term)
+        want = ob.mul_ct(OP, acc, acc, K)
+        assert np.array_equal(got[o], np.stack([want.c0, want.c1]))
+
+
+def test_mac_sweep_shape_vs_oracle_and_linearity(E):
+    """cfg5's sparse pow2 MAC (n=16384, 8 limbs): exact vs oracle on a
+    slice, and linearity MAC(a+b) = MAC(a) + MAC(b) at a larger size."""
+    import torch
+
+    from paper_1811_09953_b200 import configs
+    from paper_1811_09953_b200 import device as dev
+    from paper_1811_09953_b200 import fv
+
+    W = configs.WORKLOADS["cfg5"]
+    P = fv.EncryptionParams(W.n, W.primes, (W.t,), W.beta)
+    OP = ob.Params(W.n, W.primes, (W.t,), W.beta)
+    plan = configs.mac_sweep_plan(n_out=6, n_in=64, terms=16, seed=5)
+    rng = np.random.default_rng(2)
+    x = np.stack([np.stack([orn.random_uniform(W.primes, W.n, rng) for _ in range(2)]) for _ in range(64)])
+    xd = dev.to_device(x)
+    mac, _ = E._lower_linear(plan, W.t, W.n, "batched")
+    out = dev.to_host(E._mac_out(P, mac, xd, None))
+    for o in (0, 5):
+        acc = None
+        for tp in plan.outputs[o].taps:
+            term = ob.mul_pt(OP, ob.Ct(x[tp.in_index, 0], x[tp.in_index, 1]), [tp.weight_int % W.t])
+            acc = term if acc is None else ob.add_ct(OP, acc, term)
+        assert np.array_equal(out[o], np.stack([acc.c0, acc.c1]))
+    big = configs.mac_sweep_plan(n_out=64, n_in=512, terms=128, seed=6)
+    mac, _ = E._lower_linear(big, W.t, W.n, "batched")
+    g = torch.Generator(device="cuda").manual_seed(0)
+    a = torch.randint(0, 1 << 50, (512, 2, 8, W.n), device="cuda", generator=g, dtype=torch.int64)
+    b = torch.randint(0, 1 << 50, (512, 2, 8, W.n), device="cuda", generator=g, dtype=torch.int64)
+    ring_ptr = P.native().ring_ptr
+    from paper_1811_09953_b200 import _lib
+
+    s = dev.empty(a.shape)
+    _lib.check(_lib.lib().fcn_poly_binary(ring_ptr, 0, a.data_ptr(), b.data_ptr(), a.numel() // W.n, s.data_ptr(), a.numel() // W.n, 8, 0, dev.stream_ptr()))
+    ma, mb, ms = (E._mac_out(P, mac, v, None) for v in (a, b, s))
+    mab = dev.empty(ma.shape)
+    _lib.check(_lib.lib().fcn_poly_binary(ring_ptr, 0, ma.data_ptr(), mb.data_ptr(), ma.numel() // W.n, mab.data_ptr(), ma.numel() // W.n, 8, 0, dev.stream_ptr()))
+    assert torch.equal(mab, ms)
+
+
+def test_eval_errors(E):
+    from paper_1811_09953_b200 import fv
+    from paper_1811_09953_b200.encode import FixedPointConfig
+
+    P = fv.EncryptionParams(1024, (36028797018972161, 36028797018990593), (1099511922689,))
+    sk, pk, ek = fv.keygen(P, 1)
+    cfg = FixedPointConfig((1099511922689,), 4)
+    tensor = E.encrypt_tensor(pk, P, np.zeros(4), cfg, 0, 1)
+    net = E.NetworkSpec((4,), [E.Dense(np.ones((1, 4)), None)])
+    with pytest.raises(E.EngineError):
+        E.eval_encrypted(net, tensor, ek, FixedPointConfig((65537,), 4))
+    with pytest.raises(E.EngineError):
+        E.eval_encrypted(net, tensor, ek, cfg, encoding="nope")

@@ -1,0 +1,272 @@
+"""GPU parity of the FV layer: keys, encryption, evaluation ops and the exact
+mul_ct against reference golden vectors and the CPU oracle.  Bit-exact."""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import bfv as ob  # noqa: E402
+from oracle import drivers as od  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def F():
+    import torch
+
+    from paper_1811_09953_b200 import fv
+
+    assert torch.cuda.is_available()
+    return fv
+
+
+def _params(F, m):
+    return F.EncryptionParams(m["n"], tuple(m["primes"]), tuple(m["t_lanes"]), m["beta"])
+
+
+def _arr(ct):
+    return np.stack([ct.c0.host(), ct.c1.host()])
+
+
+def _keys_equal(F, P, prefix, d, seed):
+    sk, pk, ek = F.keygen(P, seed)
+    assert np.array_equal(sk.s.host(), d[f"{prefix}_s"])
+    assert np.array_equal(pk.p0.host(), d[f"{prefix}_p0"])
+    assert np.array_equal(pk.p1.host(), d[f"{prefix}_p1"])
+    assert np.array_equal(np.stack([x.host() for x in ek.a]), d[f"{prefix}_a"])
+    assert np.array_equal(np.stack([x.host() for x in ek.g]), d[f"{prefix}_g"])
+    return sk, pk, ek
+
+
+def test_params_derivations(F, golden_meta):
+    for key in ("tiny", "bat", "b70", "cfg1"):
+        m = golden_meta["fv"][key]
+        P = _params(F, m)
+        assert list(P.aux_primes) == m["aux"]
+        assert P.ell == m["ell"]
+        assert str(P.delta(0)) == m["delta0"]
+
+
+def test_tiny_scheme_matches_reference(F, golden_meta, golden_npz):
+    from paper_1811_09953_b200 import encode
+
+    d = golden_npz("fv")
+    m = golden_meta["fv"]["tiny"]
+    P = _params(F, m)
+    sk, pk, ek = _keys_equal(F, P, "tiny", d, 42)
+    t = P.t_lanes[0]
+    rng = np.random.default_rng(99)
+    cts = [F.encrypt(pk, P, encode.encode_integer(v, t), 0, 12, rng) for v in m["vals"]]
+    assert np.array_equal(np.stack([_arr(c) for c in cts]), d["tiny_cts"])
+    a, b = cts[0], cts[1]
+    assert np.array_equal(_arr(F.add_ct(a, b)), d["tiny_add"])
+    assert np.array_equal(_arr(F.sub_ct(a, b)), d["tiny_sub"])
+    assert np.array_equal(_arr(F.add_pt(a, encode.encode_integer(-13, t))), d["tiny_addpt"])
+    assert np.array_equal(_arr(F.mul_pt(a, encode.encode_integer(-8, t), 3)), d["tiny_mulpt_mono"])
+    assert np.array_equal(_arr(F.mul_pt(a, encode.encode_integer(11, t), 3)), d["tiny_mulpt_gen"])
+    sq = F.mul_ct(a, a, ek)
+    assert np.array_equal(_arr(sq), d["tiny_sq"])
+    assert [sq.lane, sq.scale_exponent, sq.mul_depth] == m["sq_meta"]
+    ab = F.mul_ct(cts[2], cts[3], ek)
+    assert np.array_equal(_arr(ab), d["tiny_ab"])
+    assert F.ciphertext_to_bytes(sq) == d["tiny_ser"].tobytes()
+    back = F.ciphertext_from_bytes(d["tiny_ser"].tobytes(), P)
+    assert np.array_equal(_arr(back), d["tiny_sq"])
+    assert encode.decode_integer(F.decrypt(sk, sq)) == m["dec"]["sq"]
+    assert encode.decode_integer(F.decrypt(sk, ab)) == m["dec"]["ab"]
+    assert encode.decode_integer(F.decrypt(sk, a)) == m["dec"]["a"]
+    assert abs(F.noise_budget(sk, a) - m["budget_fresh"]) < 1e-9
+    assert abs(F.noise_budget(sk, sq) - m["budget_sq"]) < 1e-9
+
+
+def test_batched_product_matches_reference(F, golden_meta, golden_npz):
+    from paper_1811_09953_b200 import engine
+
+    d = golden_npz("fv")
+    P = _params(F, golden_meta["fv"]["bat"])
+    sk, pk, ek = _keys_equal(F, P, "bat", d, 2)
+    slots = d["bat_slots"]
+    cen = engine.slot_encode(P, slots.astype(np.int64))
+    want_cen = [od.slot_encode(s, 65537, P.n) for s in slots]
+    want_cen = np.array([[c - 65537 if c > 32768 else c for c in row] for row in want_cen])
+    assert np.array_equal(cen, want_cen)
+    # rng state: the golden draws slots first, then encrypts
+    rng = np.random.default_rng(5)
+    rng.integers(0, 65537, (2, P.n), dtype=np.uint64)
+    buf = F.encrypt_batch(pk, P, cen, 0, rng)
+    from paper_1811_09953_b200 import device as dev
+
+    assert np.array_equal(dev.to_host(buf), d["bat_cts"])
+    prod = F.mul_ct_batch(P, ek, 0, buf[0:1], buf[1:2])
+    assert np.array_equal(dev.to_host(prod)[0], d["bat_prod"])
+    slots_out = engine.slot_decode(P, F.decrypt_batch(sk, P, prod).astype(np.int64))
+    assert np.array_equal(slots_out[0].astype(np.uint64), d["bat_prod_slots"])
+
+
+def test_multiword_digits_beta70(F, golden_meta, golden_npz):
+    from paper_1811_09953_b200 import device as dev
+
+    d = golden_npz("fv")
+    P = _params(F, golden_meta["fv"]["b70"])
+    sk, pk, ek = _keys_equal(F, P, "b70", d, 3)
+    out = F.mul_ct_batch(P, ek, 0, dev.to_device(d["b70_in"][None]))
+    assert np.array_equal(dev.to_host(out)[0], d["b70_sq"])
+
+
+def test_cfg1_uniform_square(F, golden_meta, golden_npz):
+    from paper_1811_09953_b200 import device as dev
+
+    d = golden_npz("fv")
+    P = _params(F, golden_meta["fv"]["cfg1"])
+    sk, pk, ek = _keys_equal(F, P, "cfg1", d, 2)
+    out = F.mul_ct_batch(P, ek, 0, dev.to_device(d["cfg1_u"][None]))
+    assert np.array_equal(dev.to_host(out)[0], d["cfg1_usq"])
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3", "cfg5"])
+def test_config_shape_square_vs_oracle(F, cfg):
+    """mul_ct on random uniform ciphertexts at the full config ring shapes."""
+    from paper_1811_09953_b200 import configs
+    from paper_1811_09953_b200 import device as dev
+
+    W = configs.WORKLOADS[cfg]
+    P = F.EncryptionParams(W.n, W.primes, (W.t,), W.beta)
+    OP = ob.Params(W.n, W.primes, (W.t,), W.beta)
+    sk, pk, ek = F.keygen(P, 2)
+    K = ob.Keys(sk.s.host(), pk.p0.host(), pk.p1.host(), [x.host() for x in ek.a], [x.host() for x in ek.g])
+    rng = np.random.default_rng(0)
+    from oracle import rns as orn
+
+    B = 3
+    x = np.stack([np.stack([orn.random_uniform(W.primes, W.n, rng) for _ in range(2)]) for _ in range(B)])
+    out = dev.to_host(F.mul_ct_batch(P, ek, 0, dev.to_device(x)))
+    for b in (0, B - 1):
+        c = ob.Ct(x[b, 0], x[b, 1])
+        want = ob.mul_ct(OP, c, c, K)
+        assert np.array_equal(out[b], np.stack([want.c0, want.c1]))
+
+
+def test_general_product_and_batch_chunking(F, golden_meta, golden_npz):
+    """a*b with distinct operands, across several workspace chunks."""
+    from oracle import rns as orn
+    from paper_1811_09953_b200 import device as dev
+
+    d = golden_npz("fv")
+    m = golden_meta["fv"]["tiny"]
+    P = _params(F, m)
+    OP = ob.Params(P.n, P.limb_primes, P.t_lanes, P.beta)
+    sk, pk, ek = F.keygen(P, 42)
+    K = ob.keygen(OP, 42)
+    rng = np.random.default_rng(17)
+    B = 5
+    xa = np.stack([np.stack([orn.random_uniform(P.limb_primes, P.n, rng) for _ in range(2)]) for _ in range(B)])
+    xb = np.stack([np.stack([orn.random_uniform(P.limb_primes, P.n, rng) for _ in range(2)]) for _ in range(B)])
+    ws = F.mul_ct_workspace(P, 2)  # forces 3 chunks
+    out = dev.to_host(F.mul_ct_batch(P, ek, 0, dev.to_device(xa), dev.to_device(xb), workspace=ws))
+    for b in range(B):
+        want = ob.mul_ct(OP, ob.Ct(xa[b, 0], xa[b, 1]), ob.Ct(xb[b, 0], xb[b, 1]), K)
+        assert np.array_equal(out[b], np.stack([want.c0, want.c1]))
+
+
+def _sqrt_mod_p(a, p):
+    """Tonelli-Shanks; None if a is a non-residue."""
+    a %= p
+    if a == 0:
+        return 0
+    if pow(a, (p - 1) // 2, p) != 1:
+        return None
+    q, s = p - 1, 0
+    while q % 2 == 0:
+        q //= 2
+        s += 1
+    z = 2
+    while pow(z, (p - 1) // 2, p) != p - 1:
+        z += 1
+    m, c, t, r = s, pow(z, q, p), pow(a, q, p), pow(a, (q + 1) // 2, p)
+    while t != 1:
+        i, tt = 0, t
+        while tt != 1:
+            tt = tt * tt % p
+            i += 1
+        b = pow(c, 1 << (m - i - 1), p)
+        m, c, t, r = i, b * b % p, t * b * b % p, r * b % p
+    return r
+
+
+def test_exact_fallback_paths(F):
+    """Inputs placed on the float64 ambiguity bands must take the exact
+    multiword path and still match the oracle bit-for-bit."""
+    from paper_1811_09953_b200 import device as dev
+
+    n = 1024
+    primes = (36028797018972161, 36028797018990593)
+    P = F.EncryptionParams(n, primes, (1099511922689,))
+    OP = ob.Params(n, primes, P.t_lanes, P.beta)
+    sk, pk, ek = F.keygen(P, 42)
+    K = ob.keygen(OP, 42)
+    q, t = P.q, P.t_lanes[0]
+    h = q >> 1
+    cases = []
+    # (1) lift: coefficient exactly at the centered-lift boundary (q-1)/2 and (q+1)/2
+    for v in (h, h + 1):
+        c0 = np.zeros((2, n), dtype=np.uint64)
+        c0[:, 0] = [v % p for p in primes]
+        c0[:, 5] = [(q - 3) % p for p in primes]
+        cases.append((c0, np.zeros((2, n), dtype=np.uint64)))
+    # (2) rescale: c0 = x (constant), c1 = 0 with t*x^2 = -h (mod q) -> (t x^2 + h)/q is an integer
+    for delta in range(0, 200):
+        target = (delta - h) * pow(t, -1, q) % q
+        roots = [_sqrt_mod_p(target % p, p) for p in primes]
+        if all(r is not None for r in roots):
+            break
+    assert all(r is not None for r in roots)
+    if True:
+        x = 0
+        for r, p in zip(roots, primes):
+            mp = q // p
+            x += r * mp * pow(mp, -1, p)
+        x %= q
+        c0 = np.zeros((2, n), dtype=np.uint64)
+        c0[:, 0] = [x % p for p in primes]
+        cases.append((c0, np.zeros((2, n), dtype=np.uint64)))
+    before = P.native().fallbacks()
+    bufs = np.stack([np.stack([a, b]) for a, b in cases])
+    out = dev.to_host(F.mul_ct_batch(P, ek, 0, dev.to_device(bufs)))
+    for i, (a, b) in enumerate(cases):
+        want = ob.mul_ct(OP, ob.Ct(a, b), ob.Ct(a, b), K)
+        assert np.array_equal(out[i], np.stack([want.c0, want.c1])), i
+    assert P.native().fallbacks() > before
+    # (3) decrypt rounding: w on the exact rounding boundary of floor((w t + h)/q)
+    from paper_1811_09953_b200 import _lib
+
+    ws = []
+    for j in (1, 7, 123456789):
+        # smallest w with w t + h >= j q, and its predecessor
+        w = (j * q - h + t - 1) // t
+        ws += [w, w - 1]
+    W = np.zeros((1, 2, n), dtype=np.uint64)
+    for i, w in enumerate(ws):
+        W[0, :, i] = [w % p for p in primes]
+    Wd = dev.to_device(W)
+    M = dev.empty((1, n))
+    _lib.check(_lib.lib().fcn_decrypt_round(P.native().ptr, 0, Wd.data_ptr(), M.data_ptr(), 1, dev.stream_ptr()))
+    got = dev.to_host(M)[0]
+    for i, w in enumerate(ws):
+        assert int(got[i]) == ((w * t + h) // q) % t
+
+
+def test_errors(F):
+    from paper_1811_09953_b200 import encode
+
+    P = F.EncryptionParams(1024, (36028797018972161, 36028797018990593), (1099511922689,))
+    sk, pk, ek = F.keygen(P, 1)
+    ct = F.encrypt(pk, P, encode.encode_integer(3, P.t_lanes[0]), 0, 4, 1)
+    with pytest.raises(F.FVError):
+        F.mul_pt(ct, F.PlainPoly.zero(P.t_lanes[0]))
+    with pytest.raises(F.FVError):
+        F.add_ct(ct, F.Ciphertext(ct.c0, ct.c1, P, 0, 5, 0))
+    with pytest.raises(F.FVError):
+        F.EncryptionParams(1000, (17,), (2,))
+    assert F.add_pt(ct, F.PlainPoly.zero(P.t_lanes[0])) is ct
