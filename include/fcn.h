@@ -43,6 +43,8 @@ typedef struct fcn_keys fcn_keys; /* device-resident relinearization keys   */
 
 const char* fcn_last_error(void);
 int fcn_version(void);
+/* Number of kernels this library has launched in the process (bench evidence). */
+long long fcn_launch_count(void);
 
 /* ---------------------------------------------------------------- rings */
 

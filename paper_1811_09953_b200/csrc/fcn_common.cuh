@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <string>
@@ -22,10 +23,12 @@ int check_cuda(cudaError_t e, const char* what);
     cudaError_t _e = (call);                            \
     if (_e != cudaSuccess) return check_cuda(_e, #call); \
   } while (0)
+extern std::atomic<long long> g_launches;  // kernels launched by this library
 #define FCN_LAUNCH_CHECK(what)                                 \
   do {                                                         \
     cudaError_t _e = cudaGetLastError();                       \
     if (_e != cudaSuccess) return check_cuda(_e, what);        \
+    ::fcn::g_launches.fetch_add(1, std::memory_order_relaxed); \
   } while (0)
 
 struct DeviceGuard {

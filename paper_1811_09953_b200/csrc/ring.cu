@@ -25,6 +25,7 @@
 namespace fcn {
 
 static thread_local std::string g_last_error;
+std::atomic<long long> g_launches{0};
 
 int set_error(int code, const char* fmt, ...) {
   char buf[1024];
@@ -478,6 +479,7 @@ using namespace fcn;
 
 extern "C" const char* fcn_last_error(void) { return g_last_error.c_str(); }
 extern "C" int fcn_version(void) { return 1; }
+extern "C" long long fcn_launch_count(void) { return g_launches.load(); }
 
 extern "C" int fcn_ring_create(int device, int n, int count, const uint64_t* primes, fcn_ring** out) {
   if (!out || !primes || count <= 0 || count > 64) return set_error(FCN_ERR_ARG, "bad ring arguments");

@@ -72,7 +72,7 @@ class CipherTensor:
     multiplicative depth (host int array)."""
 
     def __init__(self, shape, cts=None, scale_exponent: int = 0, scale_factor: int = 1, *, buf=None, params=None,
-                 lane: int = 0, depths=None):
+                 lane: int = 0, depths=None, scales=None):
         self.shape = tuple(int(d) for d in shape)
         count = int(np.prod(self.shape))
         if cts is not None:
@@ -85,6 +85,7 @@ class CipherTensor:
             lane = cts[0].lane
             buf = torch.stack([torch.stack([c.c0.data, c.c1.data]) for c in cts]).contiguous()
             depths = np.array([c.mul_depth for c in cts], dtype=np.int64)
+            scales = np.array([c.scale_exponent for c in cts], dtype=np.int64)
         if buf is None or params is None:
             raise EngineError("CipherTensor needs ciphertexts or a device buffer with params")
         if buf.shape[0] != count:
@@ -95,11 +96,16 @@ class CipherTensor:
         self.scale_exponent = int(scale_exponent)
         self.scale_factor = int(scale_factor)
         self.depths = np.zeros(count, dtype=np.int64) if depths is None else np.asarray(depths, dtype=np.int64)
+        # per-ciphertext scale_exponent (serialized in each header, fv.py:555-571);
+        # it can differ from the tensor-level exponent after pooling (engine.py:711-743)
+        self.scales = (
+            np.full(count, self.scale_exponent, dtype=np.int64) if scales is None else np.asarray(scales, dtype=np.int64)
+        )
 
     @property
     def cts(self) -> list:
         return [
-            fv.ciphertext_from_buffer(self.params, self.buf[i], self.lane, self.scale_exponent, int(self.depths[i]))
+            fv.ciphertext_from_buffer(self.params, self.buf[i], self.lane, int(self.scales[i]), int(self.depths[i]))
             for i in range(self.buf.shape[0])
         ]
 
@@ -324,7 +330,8 @@ def _lower_linear(plan: LinearPlan, t: int, n: int, encoding: str):
                 bidx.append(o_i)
                 bpos.append(p)
                 bcoef.append(c)
-    return _upload_mac(*mac), _upload_bias(bidx, bpos, bcoef)
+    taps = (np.concatenate([[0], np.cumsum(counts)]), cols)
+    return _upload_mac(*mac), _upload_bias(bidx, bpos, bcoef), taps
 
 
 def _lower_pool(plan: PoolPlan, t: int, n: int, encoding: str):
@@ -337,7 +344,9 @@ def _lower_pool(plan: PoolPlan, t: int, n: int, encoding: str):
                 rot.append(r)
                 coef.append(c)
         rowptr.append(len(col))
-    return _upload_mac(rowptr, col, rot, coef), None
+    counts = np.array([len(w) for w in plan.outputs], dtype=np.int64)
+    taps = (np.concatenate([[0], np.cumsum(counts)]), np.fromiter((i for w in plan.outputs for i in w), dtype=np.int64))
+    return _upload_mac(rowptr, col, rot, coef), None, taps
 
 
 def _lower_act(plan: ActPlan, t: int, n: int, encoding: str):
@@ -428,12 +437,27 @@ def _mac_out(params, mac: _Mac, in0, in1):
 # --------------------------------------------------------------- evaluator
 
 
-def _depths_linear(plan_outputs, depths):
-    out = np.zeros(len(plan_outputs), dtype=np.int64)
-    for i, o in enumerate(plan_outputs):
-        idx = [tp.in_index for tp in o.taps] if hasattr(o, "taps") else list(o)
-        out[i] = depths[idx].max() if idx else 0
-    return out
+def _gather_meta(taps, depths, scales, empty_scale):
+    """Per-output (depth, scale) of an add_ct chain over the taps' inputs.
+
+    depth = max over inputs (add_ct, fv.py:394-403), 0 for an empty row
+    (Ciphertext.zero); every input of a chain must share its scale
+    exponent, exactly as the reference's add_ct demands (fv.py:383-391)."""
+    rowptr, cols = taps
+    n_out = len(rowptr) - 1
+    d = np.zeros(n_out, dtype=np.int64)
+    sc = np.full(n_out, empty_scale, dtype=np.int64)
+    nonempty = np.diff(rowptr) > 0
+    if cols.size:
+        starts = rowptr[:-1][nonempty]
+        d[nonempty] = np.maximum.reduceat(depths[cols], starts)
+        smin = np.minimum.reduceat(scales[cols], starts)
+        smax = np.maximum.reduceat(scales[cols], starts)
+        if np.any(smin != smax):
+            bad = int(np.nonzero(smin != smax)[0][0])
+            raise FVError(f"scale mismatch: 2^{int(smin[bad])} vs 2^{int(smax[bad])}")
+        sc[nonempty] = smin
+    return d, sc, nonempty
 
 
 def eval_encrypted(net, tensor: CipherTensor, ek: EvalKeys, cfg: FixedPointConfig, workers: int = 1,
@@ -465,6 +489,7 @@ def eval_encrypted(net, tensor: CipherTensor, ek: EvalKeys, cfg: FixedPointConfi
     prec = cfg.precision_bits
     cur = tensor.buf
     depths = tensor.depths.copy()
+    scales = tensor.scales.copy()
     scale = tensor.scale_exponent
     factor = tensor.scale_factor
     events = []
@@ -474,16 +499,18 @@ def eval_encrypted(net, tensor: CipherTensor, ek: EvalKeys, cfg: FixedPointConfi
         ev0.record()
         kind = lw[0]
         if kind == "linear":
-            _, mac, bias = lw
+            _, mac, bias, taps = lw
+            depths, scales, nonempty = _gather_meta(taps, depths, scales, scale + prec)
+            scales = np.where(nonempty, scales + prec, scales)
             nxt = _mac_out(params, mac, cur, None)
             _run_bias(params, lane, nxt, bias)
-            depths = _depths_linear(plan.outputs, depths)
             scale += prec
         elif kind == "pool":
-            _, mac, _ = lw
+            _, mac, _, taps = lw
+            depths, scales, _ = _gather_meta(taps, depths, scales, scale)
             nxt = _mac_out(params, mac, cur, None)
-            depths = _depths_linear(plan.outputs, depths)
             if plan.reciprocal_int is not None:
+                scales = scales + prec
                 scale += prec
             else:
                 scale += plan.pow2_shift
@@ -497,6 +524,7 @@ def eval_encrypted(net, tensor: CipherTensor, ek: EvalKeys, cfg: FixedPointConfi
                 nxt = _mac_out(params, mac, sq, cur)
             _run_bias(params, lane, nxt, bias)
             depths = depths + 1
+            scales = 2 * scales + (prec if plan.a2_int is not None else 0)
             scale = 2 * scale + plan.scale_bump
             factor = factor * factor
         ev1.record()
@@ -506,5 +534,5 @@ def eval_encrypted(net, tensor: CipherTensor, ek: EvalKeys, cfg: FixedPointConfi
     for c, (a, b) in zip(counter.layer_counts, events):
         c.wall_ms = a.elapsed_time(b)
     out = CipherTensor(compiled.out_shape, scale_exponent=scale, scale_factor=factor, buf=cur, params=params, lane=lane,
-                       depths=depths)
+                       depths=depths, scales=scales)
     return out, counter

@@ -51,7 +51,7 @@ def test_integer_mode_matches_reference_run(E, golden_meta, golden_npz):
     out, counter = E.eval_encrypted(net, tensor, ek, cfg)
     assert np.array_equal(out.host_bodies(), d["out_cts"])
     assert out.scale_exponent == em["out_scale"] and out.scale_factor == em["out_factor"]
-    meta = np.array([[out.lane, out.scale_exponent, int(dd)] for dd in out.depths])
+    meta = np.array([[out.lane, int(sc), int(dd)] for sc, dd in zip(out.scales, out.depths)])
     assert np.array_equal(meta, d["out_meta"])
     assert [list(r[:5]) + [r[6]] for r in counter.rows()] == em["hops"]
     assert counter.same_ops(E.project_hops(net, cfg))
@@ -73,14 +73,14 @@ def _small_batched_setup(E, fv):
     L = E
     rng = np.random.default_rng(4)
     conv_w = rng.choice([0.0, 0.25, -0.5, 1.0, -0.125], size=(2, 1, 3, 3), p=[0.5, 0.15, 0.15, 0.1, 0.1])
-    dense_w = rng.choice([0.0, 0.5, -0.25, 1.0], size=(3, 8), p=[0.4, 0.2, 0.2, 0.2])
+    dense_w = rng.choice([0.0, 0.5, -0.25, 1.0], size=(3, 18), p=[0.4, 0.2, 0.2, 0.2])
     dense_w[2] = 0.0  # an empty row with a bias
     net = L.NetworkSpec(
         (1, 4, 4),
         [
             L.Conv2d(conv_w, np.array([0.5, -0.25]), 1, 0),
             L.PolyActivation(L.PolyApprox(2, (0.0625, 0.5, 0.125))),
-            L.ScaledAvgPool(2, stride=1, padding=0),
+            L.ScaledAvgPool(2, stride=1, padding=1),
             L.Dense(dense_w, np.array([0.25, -1.0, 0.5])),
             L.PolyActivation(L.square_activation()),
         ],
@@ -106,6 +106,7 @@ def test_batched_mode_matches_oracle_and_plain_model(E):
     want, scale, factor = od.run_plan(OP, comp, cts, K, cfg.precision_bits, "batched")
     assert np.array_equal(out.host_bodies(), np.stack([np.stack([c.c0, c.c1]) for c in want]))
     assert list(out.depths) == [c.depth for c in want]
+    assert list(out.scales) == [c.scale for c in want]
     assert out.scale_exponent == scale and out.scale_factor == factor
     slots = E.decrypt_tensor_slots(sk, out)
     model = od.plain_model_batched(comp, x << cfg.precision_bits, 65537)
@@ -163,7 +164,7 @@ def test_mac_sweep_shape_vs_oracle_and_linearity(E):
     rng = np.random.default_rng(2)
     x = np.stack([np.stack([orn.random_uniform(W.primes, W.n, rng) for _ in range(2)]) for _ in range(64)])
     xd = dev.to_device(x)
-    mac, _ = E._lower_linear(plan, W.t, W.n, "batched")
+    mac, _, _ = E._lower_linear(plan, W.t, W.n, "batched")
     out = dev.to_host(E._mac_out(P, mac, xd, None))
     for o in (0, 5):
         acc = None
@@ -172,7 +173,7 @@ def test_mac_sweep_shape_vs_oracle_and_linearity(E):
             acc = term if acc is None else ob.add_ct(OP, acc, term)
         assert np.array_equal(out[o], np.stack([acc.c0, acc.c1]))
     big = configs.mac_sweep_plan(n_out=64, n_in=512, terms=128, seed=6)
-    mac, _ = E._lower_linear(big, W.t, W.n, "batched")
+    mac, _, _ = E._lower_linear(big, W.t, W.n, "batched")
     g = torch.Generator(device="cuda").manual_seed(0)
     a = torch.randint(0, 1 << 50, (512, 2, 8, W.n), device="cuda", generator=g, dtype=torch.int64)
     b = torch.randint(0, 1 << 50, (512, 2, 8, W.n), device="cuda", generator=g, dtype=torch.int64)
