@@ -160,6 +160,7 @@ inline uint64_t h_shoup(uint64_t w, uint64_t q) { return (uint64_t)(((unsigned _
 bool h_is_prime(uint64_t v);
 int bitlen64(uint64_t v);
 LimbConst make_limb_const(uint64_t q, int n, uint64_t ipsi1);
+int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st);
 
 inline int grid_for(int64_t work, int block, int max_blocks = 148 * 16) {
   int64_t g = (work + block - 1) / block;

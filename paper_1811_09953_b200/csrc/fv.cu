@@ -23,7 +23,6 @@
 
 namespace fcn {
 
-int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st);
 
 constexpr int KQ_LIM = 16;  // max ciphertext limbs
 constexpr int KE_LIM = 32;  // max extended-base limbs

@@ -1,0 +1,584 @@
+// libfcn: batched negacyclic NTT on B200 (replaces reference ring.py:199-255).
+//
+// Two kernel families produce bit-identical outputs (canonical residues,
+// forward output in the reference's bit-reversed order):
+//
+//  * ntt_v2 (n = 1024 .. 16384, q < 2^61): one persistent CTA per row slot,
+//    n/32 threads each owning 32 residues in registers.  A transform is
+//    three register passes -- 5 stages, LOGN-10 stages, 5 stages -- with two
+//    shared-memory exchanges (row padded by one word per 32 so every access
+//    pattern is conflict-free).  The forward transform loads pass-1 operands
+//    straight from HBM (coalesced: thread t holds t + j n/32) and prefetches
+//    the next row into registers while the finished row is copied out; the
+//    inverse streams the next row into shared memory with cp.async while the
+//    last pass computes and stores coalesced from registers.  Butterflies
+//    use a Shoup product whose quotient drops the low 32x32 partial product
+//    (3 IMAD instead of 5; remainder in [0,4q)) with Harvey lazy ranges
+//    [0,8q) forward / [0,4q) inverse, one canonicalisation at the end, and
+//    the inverse's n^-1 scaling merged into its last stage.
+//
+//  * ntt_v1 (any other n, or q >= 2^61): the generic shared-memory kernel
+//    with exact Shoup products.
+
+#include <mutex>
+
+#include "fcn_common.cuh"
+
+namespace fcn {
+
+__device__ __forceinline__ int phys(int i) { return i + (i >> 5); }
+
+// ============================================================ v1 (generic)
+
+template <int R>
+__device__ __forceinline__ void v1_fwd_pass(uint64_t* sm, int logs, int ls0, int sbase, int part,
+                                            const Twiddle* __restrict__ tw, uint64_t q, uint64_t q2, bool last) {
+  constexpr int G = 1 << R;
+  const int lt = logs - ls0 - R;
+  const int tend = 1 << lt;
+  const int groups = 1 << (logs - R);
+  for (int g = threadIdx.x; g < groups; g += blockDim.x) {
+    const int b = g >> lt, o = g & (tend - 1);
+    const int base = (b << (lt + R)) + o;
+    uint64_t x[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) x[j] = sm[phys(base + (j << lt))];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int s = sbase + ls0 + u;
+      const int tbase = (1 << s) + (part << (ls0 + u)) + (b << u);
+      const int h = G >> (u + 1);
+#pragma unroll
+      for (int blk = 0; blk < (1 << u); ++blk) {
+        const Twiddle w = tw[tbase + blk];
+#pragma unroll
+        for (int jj = 0; jj < h; ++jj) {
+          const int j = blk * 2 * h + jj;
+          uint64_t X = csub(x[j], q2);
+          uint64_t T = shoup_lazy(x[j + h], w.w, w.s, q);
+          x[j] = X + T;
+          x[j + h] = X - T + q2;
+        }
+      }
+    }
+    if (last) {
+#pragma unroll
+      for (int j = 0; j < G; ++j) x[j] = csub(csub(x[j], q2), q);
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) sm[phys(base + (j << lt))] = x[j];
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void v1_inv_pass(uint64_t* sm, int logs, int ls0, int logn, int part,
+                                            const Twiddle* __restrict__ tw, const LimbConst& c, bool final_scale,
+                                            bool canon) {
+  constexpr int G = 1 << R;
+  const uint64_t q = c.q, q2 = c.q2;
+  const int lt = ls0;
+  const int tstart = 1 << lt;
+  const int groups = 1 << (logs - R);
+  for (int g = threadIdx.x; g < groups; g += blockDim.x) {
+    const int b = g >> lt, o = g & (tstart - 1);
+    const int base = (b << (lt + R)) + o;
+    uint64_t x[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) x[j] = sm[phys(base + (j << lt))];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int s = ls0 + u;
+      const int hd = 1 << u;
+      const bool is_final = final_scale && (s == logn - 1);
+      const int tbase = (1 << (logn - s - 1)) + (part << (logs - s - 1)) + (b << (R - 1 - u));
+#pragma unroll
+      for (int blk = 0; blk < (G >> (u + 1)); ++blk) {
+        const Twiddle w = tw[tbase + blk];
+#pragma unroll
+        for (int jj = 0; jj < hd; ++jj) {
+          const int j = blk * 2 * hd + jj;
+          uint64_t X = x[j], Y = x[j + hd];
+          uint64_t T = X - Y + q2;
+          if (is_final) {
+            x[j] = shoup(X + Y, c.ninv, c.ninv_s, q);
+            x[j + hd] = shoup(T, c.wlast, c.wlast_s, q);
+          } else {
+            x[j] = csub(X + Y, q2);
+            x[j + hd] = shoup_lazy(T, w.w, w.s, q);
+          }
+        }
+      }
+    }
+    if (canon && !final_scale) {
+#pragma unroll
+      for (int j = 0; j < G; ++j) x[j] = csub(x[j], q);
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) sm[phys(base + (j << lt))] = x[j];
+  }
+}
+
+__device__ __forceinline__ int v1_pass_count(int logs) {
+  int rem = logs - (logs < 5 ? logs : 5);
+  return 1 + (rem + 4) / 5;
+}
+__device__ __forceinline__ int v1_pass_size(int logs, int p, int np) {
+  int last = logs < 5 ? logs : 5;
+  if (p == np - 1) return last;
+  int rem = logs - last, k = np - 1;
+  int base = rem / k, extra = rem % k;
+  return base + (p < extra ? 1 : 0);
+}
+
+template <bool FWD>
+__global__ void __launch_bounds__(512) ntt_v1_kernel(uint64_t* __restrict__ data, int64_t n_segs, int logs, int logn,
+                                                     int period, int offset, const LimbConst* __restrict__ lcs,
+                                                     const Twiddle* __restrict__ tws) {
+  extern __shared__ uint64_t sm[];
+  const int S = 1 << logs;
+  const int nseg = 1 << (logn - logs);
+  const int n = 1 << logn;
+  for (int64_t seg = blockIdx.x; seg < n_segs; seg += gridDim.x) {
+    const int64_t row = seg >> (logn - logs);
+    const int part = (int)(seg & (nseg - 1));
+    const int limb = offset + (int)(row % period);
+    const LimbConst c = lcs[limb];
+    const Twiddle* tw = tws + (int64_t)limb * n;
+    uint64_t* p = data + row * (int64_t)n + (int64_t)part * S;
+    for (int i = threadIdx.x; i < S / 2; i += blockDim.x) {
+      ulonglong2 v = reinterpret_cast<const ulonglong2*>(p)[i];
+      sm[phys(2 * i)] = v.x;
+      sm[phys(2 * i + 1)] = v.y;
+    }
+    __syncthreads();
+    const int np = v1_pass_count(logs);
+    int ls = 0;
+    if (FWD) {
+      for (int pi = 0; pi < np; ++pi) {
+        const int R = v1_pass_size(logs, pi, np);
+        const bool last = pi == np - 1;
+        switch (R) {
+          case 1: v1_fwd_pass<1>(sm, logs, ls, logn - logs, part, tw, c.q, c.q2, last); break;
+          case 2: v1_fwd_pass<2>(sm, logs, ls, logn - logs, part, tw, c.q, c.q2, last); break;
+          case 3: v1_fwd_pass<3>(sm, logs, ls, logn - logs, part, tw, c.q, c.q2, last); break;
+          case 4: v1_fwd_pass<4>(sm, logs, ls, logn - logs, part, tw, c.q, c.q2, last); break;
+          default: v1_fwd_pass<5>(sm, logs, ls, logn - logs, part, tw, c.q, c.q2, last); break;
+        }
+        ls += R;
+        __syncthreads();
+      }
+    } else {
+      const bool final_scale = logs == logn;
+      for (int pi = np - 1; pi >= 0; --pi) {
+        const int R = v1_pass_size(logs, pi, np);
+        const bool canon = pi == 0;
+        switch (R) {
+          case 1: v1_inv_pass<1>(sm, logs, ls, logn, part, tw, c, final_scale, canon); break;
+          case 2: v1_inv_pass<2>(sm, logs, ls, logn, part, tw, c, final_scale, canon); break;
+          case 3: v1_inv_pass<3>(sm, logs, ls, logn, part, tw, c, final_scale, canon); break;
+          case 4: v1_inv_pass<4>(sm, logs, ls, logn, part, tw, c, final_scale, canon); break;
+          default: v1_inv_pass<5>(sm, logs, ls, logn, part, tw, c, final_scale, canon); break;
+        }
+        ls += R;
+        __syncthreads();
+      }
+    }
+    for (int i = threadIdx.x; i < S / 2; i += blockDim.x) {
+      ulonglong2 v;
+      v.x = sm[phys(2 * i)];
+      v.y = sm[phys(2 * i + 1)];
+      reinterpret_cast<ulonglong2*>(p)[i] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// forward stage 0 / inverse last stage of n > 16384 rows, in global memory
+__global__ void ntt_v1_fwd_stage0(uint64_t* __restrict__ data, int64_t n_rows, int logn, int period, int offset,
+                                  const LimbConst* __restrict__ lcs, const Twiddle* __restrict__ tws) {
+  const int n = 1 << logn, h = n >> 1;
+  const int64_t total = n_rows * h;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / h;
+    const int j = (int)(e % h);
+    const int limb = offset + (int)(row % period);
+    const LimbConst c = lcs[limb];
+    const Twiddle w = tws[(int64_t)limb * n + 1];
+    uint64_t* p = data + row * n;
+    uint64_t X = p[j];
+    uint64_t T = shoup_lazy(p[j + h], w.w, w.s, c.q);
+    p[j] = X + T;
+    p[j + h] = X - T + c.q2;
+  }
+}
+
+__global__ void ntt_v1_inv_last(uint64_t* __restrict__ data, int64_t n_rows, int logn, int period, int offset,
+                                const LimbConst* __restrict__ lcs) {
+  const int n = 1 << logn, h = n >> 1;
+  const int64_t total = n_rows * h;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / h;
+    const int j = (int)(e % h);
+    const LimbConst c = lcs[offset + (int)(row % period)];
+    uint64_t* p = data + row * n;
+    uint64_t X = p[j], Y = p[j + h];
+    p[j] = shoup(X + Y, c.ninv, c.ninv_s, c.q);
+    p[j + h] = shoup(X - Y + c.q2, c.wlast, c.wlast_s, c.q);
+  }
+}
+
+// ================================================================= v2
+
+// a*w mod q in [0, 4q) for constant w < q, ws = floor(w 2^64/q), q < 2^61:
+// the quotient estimate omits the a0*ws0 partial product and the low
+// halves of the cross products, so it undershoots floor(a ws / 2^64) by <= 2.
+__device__ __forceinline__ uint64_t mulw(uint64_t a, uint64_t w, uint64_t ws, uint64_t q) {
+  const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32);
+  const uint32_t s0 = (uint32_t)ws, s1 = (uint32_t)(ws >> 32);
+  const uint64_t h = (uint64_t)a1 * s1 + __umulhi(a1, s0) + __umulhi(a0, s1);
+  return a * w - h * q;
+}
+
+__device__ __forceinline__ Twiddle ld_tw(const Twiddle* p) {
+  const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
+  return Twiddle{v.x, v.y};
+}
+
+// forward CT butterfly on [0, 8q): X' = X + wY, Y' = X - wY (+4q)
+__device__ __forceinline__ void bfly_f(uint64_t& X, uint64_t& Y, const Twiddle& w, uint64_t q, uint64_t q4) {
+  const uint64_t x = csub(X, q4);
+  const uint64_t t = mulw(Y, w.w, w.s, q);
+  X = x + t;
+  Y = x - t + q4;
+}
+
+// inverse GS butterfly on [0, 4q): X' = X + Y, Y' = w (X - Y)
+__device__ __forceinline__ void bfly_i(uint64_t& X, uint64_t& Y, const Twiddle& w, uint64_t q, uint64_t q4) {
+  const uint64_t s = csub(X + Y, q4);
+  const uint64_t d = X - Y + q4;
+  X = s;
+  Y = mulw(d, w.w, w.s, q);
+}
+
+// R forward stages on G = 2^R registers; twiddle of block blk at local stage u
+// is tw[base_u + blk] with base_u = (1 << (s0 + u)) + (b << u).
+template <int R, int OFF>
+__device__ __forceinline__ void fwd_stages(uint64_t* x, int s0, int b, const Twiddle* __restrict__ tw, uint64_t q,
+                                           uint64_t q4) {
+  constexpr int G = 1 << R;
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    const int tb = (1 << (s0 + u)) + (b << u);
+    const int h = G >> (u + 1);  // butterfly span in registers
+    Twiddle w;
+#pragma unroll
+    for (int bi = 0; bi < G / 2; ++bi) {  // flattened (block, offset) loop: always fully unrolled
+      const int blk = bi / h, jj = bi % h;
+      if (jj == 0) w = ld_tw(tw + tb + blk);
+      const int j = blk * 2 * h + jj;
+      bfly_f(x[OFF + j], x[OFF + j + h], w, q, q4);
+    }
+  }
+}
+
+// R inverse stages on G = 2^R registers starting at global inverse stage s0;
+// twiddle index (n >> (s+1)) + (b << (R-1-u)) + blk.  When LASTSCALE, the
+// final stage (s0 + R - 1 == logn - 1) is merged with n^-1 and canonicalised.
+template <int R, int OFF, bool LASTSCALE>
+__device__ __forceinline__ void inv_stages(uint64_t* x, int s0, int logn, int b, const Twiddle* __restrict__ tw,
+                                           const LimbConst& c) {
+  constexpr int G = 1 << R;
+  const uint64_t q = c.q, q4 = 4 * c.q;
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    const int s = s0 + u;
+    const int hd = 1 << u;
+    const int tb = (1 << (logn - s - 1)) + (b << (R - 1 - u));
+    if (LASTSCALE && u == R - 1) {
+#pragma unroll
+      for (int jj = 0; jj < G / 2; ++jj) {
+        const uint64_t X = x[OFF + jj], Y = x[OFF + jj + G / 2];
+        const uint64_t a = mulw(X + Y, c.ninv, c.ninv_s, q);
+        const uint64_t d = mulw(X - Y + q4, c.wlast, c.wlast_s, q);
+        x[OFF + jj] = csub(csub(a, 2 * q), q);
+        x[OFF + jj + G / 2] = csub(csub(d, 2 * q), q);
+      }
+    } else {
+      Twiddle w;
+#pragma unroll
+      for (int bi = 0; bi < G / 2; ++bi) {
+        const int blk = bi / hd, jj = bi % hd;
+        if (jj == 0) w = ld_tw(tw + tb + blk);
+        const int j = blk * 2 * hd + jj;
+        bfly_i(x[OFF + j], x[OFF + j + hd], w, q, q4);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_async8(uint64_t* smem_dst, const uint64_t* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+template <int LOGN>
+__global__ void __launch_bounds__((1 << LOGN) / 32, 16384 / (1 << LOGN)) ntt_v2_fwd(uint64_t* __restrict__ data, int64_t n_rows, int period,
+                                                               int offset, const LimbConst* __restrict__ lcs,
+                                                               const Twiddle* __restrict__ tws) {
+  constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
+  extern __shared__ uint64_t sm[];
+  const int tid = threadIdx.x;
+  int64_t row = blockIdx.x;
+  if (row >= n_rows) return;
+  uint64_t x[32];
+  {
+    const uint64_t* p = data + row * N;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = p[tid + j * T];
+  }
+  for (; row < n_rows; row += gridDim.x) {
+    const int limb = offset + (int)(row % period);
+    const uint64_t q = lcs[limb].q, q4 = 4 * q;
+    const Twiddle* tw = tws + (int64_t)limb * N;
+    // pass 1: stages 0..4 on t + j*T (twiddles uniform across the CTA)
+    fwd_stages<5, 0>(x, 0, 0, tw, q, q4);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) sm[phys(tid + j * T)] = x[j];
+    __syncthreads();
+    // pass 2: stages 5 .. 4+RM on groups of GM elements 32 apart
+    if (RM > 0) {
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) {
+        const int g = tid + i * T;
+        const int b = g >> 5, o = g & 31;
+        const int base = (b << (5 + RM)) + o;
+#pragma unroll
+        for (int j = 0; j < GM; ++j) x[i * GM + j] = sm[phys(base + j * 32)];
+      }
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) {
+        const int b = (tid + i * T) >> 5;
+        fwd_stages<(RM > 0 ? RM : 1), 0>(x + i * GM, 5, b, tw, q, q4);
+      }
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) {
+        const int g = tid + i * T;
+        const int b = g >> 5, o = g & 31;
+        const int base = (b << (5 + RM)) + o;
+#pragma unroll
+        for (int j = 0; j < GM; ++j) sm[phys(base + j * 32)] = x[i * GM + j];
+      }
+      __syncthreads();
+    }
+    // pass 3: the last 5 stages on 32 contiguous residues, canonical out
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = sm[tid * 33 + j];
+    fwd_stages<5, 0>(x, LOGN - 5, tid, tw, q, q4);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) sm[tid * 33 + j] = csub(csub(csub(x[j], q4), 2 * q), q);
+    __syncthreads();
+    // prefetch the next row's pass-1 operands, then copy this row out (coalesced)
+    const int64_t nxt = row + gridDim.x;
+    if (nxt < n_rows) {
+      const uint64_t* p = data + nxt * N;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] = p[tid + j * T];
+    }
+    ulonglong2* o2 = reinterpret_cast<ulonglong2*>(data + row * N);
+#pragma unroll 4
+    for (int i = tid; i < N / 2; i += T) {
+      ulonglong2 v;
+      v.x = sm[phys(2 * i)];
+      v.y = sm[phys(2 * i + 1)];
+      o2[i] = v;
+    }
+    __syncthreads();
+  }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__((1 << LOGN) / 32, 16384 / (1 << LOGN)) ntt_v2_inv(uint64_t* __restrict__ data, int64_t n_rows, int period,
+                                                               int offset, const LimbConst* __restrict__ lcs,
+                                                               const Twiddle* __restrict__ tws) {
+  constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
+  extern __shared__ uint64_t sm[];
+  const int tid = threadIdx.x;
+  int64_t row = blockIdx.x;
+  if (row >= n_rows) return;
+  {
+    const uint64_t* p = data + row * N;
+    for (int i = tid; i < N; i += T) cp_async8(&sm[phys(i)], p + i);
+    cp_async_commit();
+  }
+  uint64_t x[32];
+  for (; row < n_rows; row += gridDim.x) {
+    const int limb = offset + (int)(row % period);
+    const LimbConst c = lcs[limb];
+    const Twiddle* tw = tws + (int64_t)limb * N;
+    cp_async_wait_all();
+    __syncthreads();
+    // pass 1: inverse stages 0..4 on 32 contiguous residues
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = sm[tid * 33 + j];
+    inv_stages<5, 0, false>(x, 0, LOGN, tid, tw, c);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) sm[tid * 33 + j] = x[j];
+    __syncthreads();
+    // pass 2: stages 5 .. 4+RM on groups of GM elements 32 apart
+    if (RM > 0) {
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) {
+        const int g = tid + i * T;
+        const int b = g >> 5, o = g & 31;
+        const int base = (b << (5 + RM)) + o;
+#pragma unroll
+        for (int j = 0; j < GM; ++j) x[i * GM + j] = sm[phys(base + j * 32)];
+      }
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) {
+        const int b = (tid + i * T) >> 5;
+        inv_stages<(RM > 0 ? RM : 1), 0, false>(x + i * GM, 5, LOGN, b, tw, c);
+      }
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) {
+        const int g = tid + i * T;
+        const int b = g >> 5, o = g & 31;
+        const int base = (b << (5 + RM)) + o;
+#pragma unroll
+        for (int j = 0; j < GM; ++j) sm[phys(base + j * 32)] = x[i * GM + j];
+      }
+      __syncthreads();
+    }
+    // pass 3: last 5 stages on t + j*T; stream the next row in meanwhile
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = sm[phys(tid + j * T)];
+    __syncthreads();
+    const int64_t nxt = row + gridDim.x;
+    if (nxt < n_rows) {
+      const uint64_t* p = data + nxt * N;
+      for (int i = tid; i < N; i += T) cp_async8(&sm[phys(i)], p + i);
+      cp_async_commit();
+    }
+    inv_stages<5, 0, true>(x, LOGN - 5, LOGN, 0, tw, c);
+    uint64_t* p = data + row * N;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) p[tid + j * T] = x[j];
+  }
+  cp_async_wait_all();
+}
+
+// ============================================================== dispatch
+
+static size_t v1_smem(int logs) { return (size_t)((1 << logs) + (1 << logs) / 32 + 2) * sizeof(uint64_t); }
+static size_t v2_smem(int logn) { return (size_t)((1 << logn) + (1 << logn) / 32 + 2) * sizeof(uint64_t); }
+
+struct V2Entry {
+  const void* fn;
+  int ctas_per_sm;
+};
+
+template <int LOGN, bool FWD>
+static const void* v2_ptr() {
+  return FWD ? (const void*)ntt_v2_fwd<LOGN> : (const void*)ntt_v2_inv<LOGN>;
+}
+
+static int g_sms = 0;
+static V2Entry g_v2[2][15];
+static std::once_flag g_init;
+static cudaError_t g_init_err = cudaSuccess;
+
+static void init_tables() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+  const void* fns[2][15] = {};
+  fns[1][10] = v2_ptr<10, true>();
+  fns[1][11] = v2_ptr<11, true>();
+  fns[1][12] = v2_ptr<12, true>();
+  fns[1][13] = v2_ptr<13, true>();
+  fns[1][14] = v2_ptr<14, true>();
+  fns[0][10] = v2_ptr<10, false>();
+  fns[0][11] = v2_ptr<11, false>();
+  fns[0][12] = v2_ptr<12, false>();
+  fns[0][13] = v2_ptr<13, false>();
+  fns[0][14] = v2_ptr<14, false>();
+  for (int f = 0; f < 2; ++f) {
+    for (int lg = 10; lg <= 14; ++lg) {
+      const size_t sm = v2_smem(lg);
+      cudaError_t e = cudaFuncSetAttribute(fns[f][lg], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      int occ = 0;
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fns[f][lg], (1 << lg) / 32, sm);
+      if (e != cudaSuccess) g_init_err = e;
+      g_v2[f][lg] = {fns[f][lg], occ > 0 ? occ : 1};
+    }
+  }
+  const size_t mx = v1_smem(14);
+  cudaError_t e1 = cudaFuncSetAttribute(ntt_v1_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+  cudaError_t e2 = cudaFuncSetAttribute(ntt_v1_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+  if (e1 != cudaSuccess) g_init_err = e1;
+  if (e2 != cudaSuccess) g_init_err = e2;
+}
+
+static int launch_v1(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st) {
+  const int logn = r->logn;
+  const int logs = logn < 14 ? logn : 14;
+  const int64_t segs = n_rows << (logn - logs);
+  int threads = (1 << logs) / 32;
+  threads = threads < 32 ? 32 : (threads > 512 ? 512 : threads);
+  const size_t smem = v1_smem(logs);
+  int64_t grid = segs;
+  const int64_t cap = (int64_t)(g_sms ? g_sms : 148) * 64;
+  if (grid > cap) grid = cap;
+  if (fwd) {
+    if (logs < logn) {
+      ntt_v1_fwd_stage0<<<grid_for(n_rows << (logn - 1), 256), 256, 0, st>>>(d, n_rows, logn, period, offset, r->d_lc, r->d_fwd);
+      FCN_LAUNCH_CHECK("ntt_v1_fwd_stage0");
+    }
+    ntt_v1_kernel<true><<<(int)grid, threads, smem, st>>>(d, segs, logs, logn, period, offset, r->d_lc, r->d_fwd);
+    FCN_LAUNCH_CHECK("ntt_v1_kernel<fwd>");
+  } else {
+    ntt_v1_kernel<false><<<(int)grid, threads, smem, st>>>(d, segs, logs, logn, period, offset, r->d_lc, r->d_inv);
+    FCN_LAUNCH_CHECK("ntt_v1_kernel<inv>");
+    if (logs < logn) {
+      ntt_v1_inv_last<<<grid_for(n_rows << (logn - 1), 256), 256, 0, st>>>(d, n_rows, logn, period, offset, r->d_lc);
+      FCN_LAUNCH_CHECK("ntt_v1_inv_last");
+    }
+  }
+  return FCN_OK;
+}
+
+template <int LOGN>
+static void launch_v2_t(bool fwd, int grid, uint64_t* d, int64_t n_rows, int period, int offset, const fcn_ring* r,
+                        cudaStream_t st) {
+  const size_t sm = v2_smem(LOGN);
+  if (fwd)
+    ntt_v2_fwd<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fwd);
+  else
+    ntt_v2_inv<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_inv);
+}
+
+int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st) {
+  if (n_rows <= 0) return FCN_OK;
+  std::call_once(g_init, init_tables);
+  if (g_init_err != cudaSuccess) return check_cuda(g_init_err, "ntt init");
+  const int logn = r->logn;
+  bool v2 = logn >= 10 && logn <= 14;
+  for (int l = 0; v2 && l < period; ++l) v2 = r->primes[offset + l] < (1ull << 61);
+  if (!v2) return launch_v1(r, d, n_rows, period, offset, fwd, st);
+  const V2Entry& e = g_v2[fwd ? 1 : 0][logn];
+  int64_t grid = (int64_t)g_sms * e.ctas_per_sm;
+  if (grid > n_rows) grid = n_rows;
+  switch (logn) {
+    case 10: launch_v2_t<10>(fwd, (int)grid, d, n_rows, period, offset, r, st); break;
+    case 11: launch_v2_t<11>(fwd, (int)grid, d, n_rows, period, offset, r, st); break;
+    case 12: launch_v2_t<12>(fwd, (int)grid, d, n_rows, period, offset, r, st); break;
+    case 13: launch_v2_t<13>(fwd, (int)grid, d, n_rows, period, offset, r, st); break;
+    default: launch_v2_t<14>(fwd, (int)grid, d, n_rows, period, offset, r, st); break;
+  }
+  FCN_LAUNCH_CHECK(fwd ? "ntt_v2_fwd" : "ntt_v2_inv");
+  return FCN_OK;
+}
+
+}  // namespace fcn

@@ -111,291 +111,6 @@ static uint32_t bitrev(uint32_t x, int bits) {
   return r;
 }
 
-// ------------------------------------------------------------ NTT kernels
-
-__device__ __forceinline__ int phys(int i) { return i + (i >> 5); }
-
-// Forward CT pass over R stages (local stages ls0 .. ls0+R-1 of a segment of
-// size S = 2^logs that starts at global stage sbase; `part` = segment index).
-template <int R>
-__device__ __forceinline__ void fwd_pass(uint64_t* sm, int logs, int ls0, int sbase, int part,
-                                         const Twiddle* __restrict__ tw, uint64_t q, uint64_t q2,
-                                         bool last) {
-  constexpr int G = 1 << R;
-  const int lt = logs - ls0 - R;  // log2 of the element distance inside a group
-  const int tend = 1 << lt;
-  const int groups = 1 << (logs - R);
-  for (int g = threadIdx.x; g < groups; g += blockDim.x) {
-    const int b = g >> lt, o = g & (tend - 1);
-    const int base = (b << (lt + R)) + o;
-    uint64_t x[G];
-#pragma unroll
-    for (int j = 0; j < G; ++j) x[j] = sm[phys(base + (j << lt))];
-#pragma unroll
-    for (int u = 0; u < R; ++u) {
-      const int s = sbase + ls0 + u;
-      const int tbase = (1 << s) + (part << (ls0 + u)) + (b << u);
-      constexpr int dummy = 0;
-      (void)dummy;
-      const int h = G >> (u + 1);
-#pragma unroll
-      for (int blk = 0; blk < (1 << u); ++blk) {
-        const Twiddle w = tw[tbase + blk];
-#pragma unroll
-        for (int jj = 0; jj < h; ++jj) {
-          const int j = blk * 2 * h + jj;
-          uint64_t X = csub(x[j], q2);
-          uint64_t T = shoup_lazy(x[j + h], w.w, w.s, q);
-          x[j] = X + T;
-          x[j + h] = X - T + q2;
-        }
-      }
-    }
-    if (last) {
-#pragma unroll
-      for (int j = 0; j < G; ++j) x[j] = csub(csub(x[j], q2), q);
-    }
-#pragma unroll
-    for (int j = 0; j < G; ++j) sm[phys(base + (j << lt))] = x[j];
-  }
-}
-
-// Inverse GS pass over R stages (local stages ls0 .. ls0+R-1; element
-// distance 2^ls0).  `final_scale`: the pass holds the last global stage,
-// which is merged with the n^-1 scaling and canonicalisation.
-template <int R>
-__device__ __forceinline__ void inv_pass(uint64_t* sm, int logs, int ls0, int logn, int part,
-                                         const Twiddle* __restrict__ tw, const LimbConst& c,
-                                         bool final_scale, bool canon) {
-  constexpr int G = 1 << R;
-  const uint64_t q = c.q, q2 = c.q2;
-  const int lt = ls0;
-  const int tstart = 1 << lt;
-  const int groups = 1 << (logs - R);
-  for (int g = threadIdx.x; g < groups; g += blockDim.x) {
-    const int b = g >> lt, o = g & (tstart - 1);
-    const int base = (b << (lt + R)) + o;
-    uint64_t x[G];
-#pragma unroll
-    for (int j = 0; j < G; ++j) x[j] = sm[phys(base + (j << lt))];
-#pragma unroll
-    for (int u = 0; u < R; ++u) {
-      const int s = ls0 + u;  // global inverse stage (segments start at stage 0)
-      const int hd = 1 << u;
-      const bool is_final = final_scale && (s == logn - 1);
-      const int tbase = (1 << (logn - s - 1)) + (part << (logs - s - 1)) + (b << (R - 1 - u));
-#pragma unroll
-      for (int blk = 0; blk < (G >> (u + 1)); ++blk) {
-        const Twiddle w = tw[tbase + blk];
-#pragma unroll
-        for (int jj = 0; jj < hd; ++jj) {
-          const int j = blk * 2 * hd + jj;
-          uint64_t X = x[j], Y = x[j + hd];
-          uint64_t T = X - Y + q2;
-          if (is_final) {
-            x[j] = shoup(X + Y, c.ninv, c.ninv_s, q);
-            x[j + hd] = shoup(T, c.wlast, c.wlast_s, q);
-          } else {
-            x[j] = csub(X + Y, q2);
-            x[j + hd] = shoup_lazy(T, w.w, w.s, q);
-          }
-        }
-      }
-    }
-    if (canon && !final_scale) {
-#pragma unroll
-      for (int j = 0; j < G; ++j) x[j] = csub(x[j], q);
-    }
-#pragma unroll
-    for (int j = 0; j < G; ++j) sm[phys(base + (j << lt))] = x[j];
-  }
-}
-
-// Pass plan: last pass takes min(5, logs) stages, the rest split evenly.
-__device__ __forceinline__ int pass_count(int logs) {
-  int rem = logs - (logs < 5 ? logs : 5);
-  return 1 + (rem + 4) / 5;
-}
-__device__ __forceinline__ int pass_size(int logs, int p, int np) {
-  int last = logs < 5 ? logs : 5;
-  if (p == np - 1) return last;
-  int rem = logs - last, k = np - 1;
-  int base = rem / k, extra = rem % k;
-  return base + (p < extra ? 1 : 0);
-}
-
-template <bool FWD>
-__global__ void __launch_bounds__(512) ntt_smem_kernel(uint64_t* __restrict__ data, int64_t n_segs,
-                                                       int logs, int logn, int period, int offset,
-                                                       const LimbConst* __restrict__ lcs,
-                                                       const Twiddle* __restrict__ tws) {
-  extern __shared__ uint64_t sm[];
-  const int S = 1 << logs;
-  const int nseg = 1 << (logn - logs);
-  const int n = 1 << logn;
-  for (int64_t seg = blockIdx.x; seg < n_segs; seg += gridDim.x) {
-    const int64_t row = seg >> (logn - logs);
-    const int part = (int)(seg & (nseg - 1));
-    const int limb = offset + (int)(row % period);
-    const LimbConst c = lcs[limb];
-    const Twiddle* tw = tws + (int64_t)limb * n;
-    uint64_t* p = data + row * (int64_t)n + (int64_t)part * S;
-    if (S >= 2) {
-      const ulonglong2* p2 = reinterpret_cast<const ulonglong2*>(p);
-      for (int i = threadIdx.x; i < S / 2; i += blockDim.x) {
-        ulonglong2 v = p2[i];
-        sm[phys(2 * i)] = v.x;
-        sm[phys(2 * i + 1)] = v.y;
-      }
-    }
-    __syncthreads();
-    const int np = pass_count(logs);
-    if (FWD) {
-      int ls = 0;
-      for (int pi = 0; pi < np; ++pi) {
-        const int R = pass_size(logs, pi, np);
-        const bool last = pi == np - 1;
-        switch (R) {
-          case 1: fwd_pass<1>(sm, logs, ls, logn - logs, part, tw, c.q, c.q2, last); break;
-          case 2: fwd_pass<2>(sm, logs, ls, logn - logs, part, tw, c.q, c.q2, last); break;
-          case 3: fwd_pass<3>(sm, logs, ls, logn - logs, part, tw, c.q, c.q2, last); break;
-          case 4: fwd_pass<4>(sm, logs, ls, logn - logs, part, tw, c.q, c.q2, last); break;
-          default: fwd_pass<5>(sm, logs, ls, logn - logs, part, tw, c.q, c.q2, last); break;
-        }
-        ls += R;
-        __syncthreads();
-      }
-    } else {
-      // inverse: small distances first -> run the plan mirrored
-      int ls = 0;
-      const bool final_scale = logs == logn;
-      for (int pi = np - 1; pi >= 0; --pi) {
-        const int R = pass_size(logs, pi, np);
-        const bool canon = pi == 0;
-        switch (R) {
-          case 1: inv_pass<1>(sm, logs, ls, logn, part, tw, c, final_scale, canon); break;
-          case 2: inv_pass<2>(sm, logs, ls, logn, part, tw, c, final_scale, canon); break;
-          case 3: inv_pass<3>(sm, logs, ls, logn, part, tw, c, final_scale, canon); break;
-          case 4: inv_pass<4>(sm, logs, ls, logn, part, tw, c, final_scale, canon); break;
-          default: inv_pass<5>(sm, logs, ls, logn, part, tw, c, final_scale, canon); break;
-        }
-        ls += R;
-        __syncthreads();
-      }
-    }
-    ulonglong2* o2 = reinterpret_cast<ulonglong2*>(p);
-    for (int i = threadIdx.x; i < S / 2; i += blockDim.x) {
-      ulonglong2 v;
-      v.x = sm[phys(2 * i)];
-      v.y = sm[phys(2 * i + 1)];
-      o2[i] = v;
-    }
-    __syncthreads();
-  }
-}
-
-// Forward stage 0 of an n > 16384 row in global memory: (a_j, a_{j+n/2}) with psi[1].
-__global__ void ntt_fwd_stage0(uint64_t* __restrict__ data, int64_t n_rows, int logn, int period,
-                               int offset, const LimbConst* __restrict__ lcs,
-                               const Twiddle* __restrict__ tws) {
-  const int n = 1 << logn, h = n >> 1;
-  const int64_t total = n_rows * h;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = e / h;
-    const int j = (int)(e % h);
-    const int limb = offset + (int)(row % period);
-    const LimbConst c = lcs[limb];
-    const Twiddle w = tws[(int64_t)limb * n + 1];
-    uint64_t* p = data + row * n;
-    uint64_t X = p[j];
-    uint64_t T = shoup_lazy(p[j + h], w.w, w.s, c.q);
-    p[j] = X + T;
-    p[j + h] = X - T + c.q2;
-  }
-}
-
-// Inverse last stage of an n > 16384 row: merged with n^-1, canonical out.
-__global__ void ntt_inv_last(uint64_t* __restrict__ data, int64_t n_rows, int logn, int period,
-                             int offset, const LimbConst* __restrict__ lcs) {
-  const int n = 1 << logn, h = n >> 1;
-  const int64_t total = n_rows * h;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = e / h;
-    const int j = (int)(e % h);
-    const LimbConst c = lcs[offset + (int)(row % period)];
-    uint64_t* p = data + row * n;
-    uint64_t X = p[j], Y = p[j + h];
-    p[j] = shoup(X + Y, c.ninv, c.ninv_s, c.q);
-    p[j + h] = shoup(X - Y + c.q2, c.wlast, c.wlast_s, c.q);
-  }
-}
-
-static int ntt_threads(int logs) {
-  int S = 1 << logs;
-  int t = S / 32;
-  if (t < 32) t = 32;
-  if (t > 512) t = 512;
-  return t;
-}
-
-static size_t ntt_smem_bytes(int logs) {
-  int S = 1 << logs;
-  return (size_t)(S + S / 32 + 2) * sizeof(uint64_t);
-}
-
-static const int kMaxLogS = 14;
-
-static int set_smem_attr() {
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [] {
-    size_t mx = ntt_smem_bytes(kMaxLogS);
-    cudaError_t e1 = cudaFuncSetAttribute(ntt_smem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
-    cudaError_t e2 = cudaFuncSetAttribute(ntt_smem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
-    err = e1 != cudaSuccess ? e1 : e2;
-  });
-  if (err != cudaSuccess) return check_cuda(err, "cudaFuncSetAttribute(ntt)");
-  return FCN_OK;
-}
-
-int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd,
-               cudaStream_t st) {
-  if (n_rows <= 0) return FCN_OK;
-  int rc = set_smem_attr();
-  if (rc) return rc;
-  const int logn = r->logn;
-  const int logs = logn < kMaxLogS ? logn : kMaxLogS;
-  const int64_t segs = n_rows << (logn - logs);
-  const int threads = ntt_threads(logs);
-  const size_t smem = ntt_smem_bytes(logs);
-  int dev_sms = 148;
-  int64_t grid = segs;
-  const int64_t cap = (int64_t)dev_sms * 64;
-  if (grid > cap) grid = cap;
-  if (fwd) {
-    if (logs < logn) {
-      ntt_fwd_stage0<<<grid_for(n_rows << (logn - 1), 256), 256, 0, st>>>(d, n_rows, logn, period, offset,
-                                                                           r->d_lc, r->d_fwd);
-      FCN_LAUNCH_CHECK("ntt_fwd_stage0");
-    }
-    ntt_smem_kernel<true><<<(int)grid, threads, smem, st>>>(d, segs, logs, logn, period, offset, r->d_lc,
-                                                            r->d_fwd);
-    FCN_LAUNCH_CHECK("ntt_smem_kernel<fwd>");
-  } else {
-    ntt_smem_kernel<false><<<(int)grid, threads, smem, st>>>(d, segs, logs, logn, period, offset, r->d_lc,
-                                                             r->d_inv);
-    FCN_LAUNCH_CHECK("ntt_smem_kernel<inv>");
-    if (logs < logn) {
-      ntt_inv_last<<<grid_for(n_rows << (logn - 1), 256), 256, 0, st>>>(d, n_rows, logn, period, offset,
-                                                                         r->d_lc);
-      FCN_LAUNCH_CHECK("ntt_inv_last");
-    }
-  }
-  return FCN_OK;
-}
-
 // ------------------------------------------------------- elementwise ops
 
 template <int OP>

@@ -373,6 +373,65 @@ def _lower_act(plan: ActPlan, t: int, n: int, encoding: str):
 
 
 _lower_cache: dict = {}
+_compile_cache: dict = {}
+
+
+def _net_fingerprint(net) -> bytes:
+    """Content hash of everything compile_network reads (weights, masks,
+    biases, geometry, activation coefficients)."""
+    import hashlib
+
+    h = hashlib.blake2b(digest_size=16)
+    h.update(repr(tuple(net.input_shape)).encode())
+    for layer in net.layers:
+        h.update(type(layer).__name__.encode())
+        for attr in ("weights", "mask", "bias", "scale", "shift"):
+            v = getattr(layer, attr, None)
+            if v is not None:
+                a = np.ascontiguousarray(v, dtype=np.float64)
+                h.update(repr(a.shape).encode())
+                h.update(a.tobytes())
+        for attr in ("stride", "padding", "window", "reciprocal"):
+            if hasattr(layer, attr):
+                h.update(repr(getattr(layer, attr)).encode())
+        poly = getattr(layer, "poly", None)
+        if poly is not None:
+            h.update(repr(tuple(float(c) for c in poly.coeffs)).encode())
+    return h.digest()
+
+
+_hops_cache: dict = {}
+
+
+def _hops(compiled: CompiledNet, encoding: str, t: int) -> HopCounter:
+    """Fresh HopCounter with the plan's static tally (cached per plan)."""
+    key = (id(compiled), encoding, t)
+    hit = _hops_cache.get(key)
+    if hit is None or hit[0] is not compiled:
+        hit = (compiled, plan_hops(compiled, encoding, t))
+        _hops_cache[key] = hit
+    tmpl = hit[1]
+    out = HopCounter()
+    for name, c in zip(tmpl.layer_names, tmpl.layer_counts):
+        lc = out.layer(name)
+        lc.add(c)
+        lc.wall_ms = 0.0
+    return out
+
+
+def _compiled(net, cfg) -> CompiledNet:
+    """compile_network with a content-addressed cache (the plan is public,
+    deterministic host data; recompiling per call would dominate a step)."""
+    if isinstance(net, CompiledNet):
+        return net
+    key = (_net_fingerprint(net), tuple(int(t) for t in cfg.t_lanes), cfg.precision_bits)
+    hit = _compile_cache.get(key)
+    if hit is None:
+        hit = compile_network(net, cfg)
+        if len(_compile_cache) > 64:
+            _compile_cache.clear()
+        _compile_cache[key] = hit
+    return hit
 
 
 def _lowered(compiled: CompiledNet, t: int, n: int, encoding: str):
@@ -483,8 +542,8 @@ def eval_encrypted(net, tensor: CipherTensor, ek: EvalKeys, cfg: FixedPointConfi
     acts = sum(type(l).__name__ == "PolyActivation" for l in net.layers)
     if acts > params.mul_depth_budget:
         raise EngineError(f"{acts} activations exceed the parameter depth budget {params.mul_depth_budget}")
-    compiled = compile_network(net, cfg) if not isinstance(net, CompiledNet) else net
-    counter = plan_hops(compiled, encoding, t)
+    compiled = _compiled(net, cfg)
+    counter = _hops(compiled, encoding, t)
     low = _lowered(compiled, t, params.n, encoding)
     prec = cfg.precision_bits
     cur = tensor.buf
