@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfcn.so")
+LIB_PATH = os.environ.get("FCN_LIB_PATH") or os.path.join(HERE, "libfcn.so")
 
 FCN_OK = 0
 FCN_ERR_ARG = -1

@@ -60,6 +60,9 @@ struct LimbConst {
   uint64_t one_s;   // floor(2^64 / q): Shoup quotient of the constant 1
   uint64_t r64;     // 2^64 mod q
   uint64_t r64_s;
+  uint64_t nq;      // 2^64 - q
+  uint32_t m32;     // floor(2^64 / q) when q > 2^32, else 0
+  uint32_t pad2;
 };
 
 struct __align__(16) Twiddle {
@@ -80,6 +83,8 @@ struct fcn_ring {
   fcn::LimbConst* d_lc = nullptr;  // [L]
   fcn::Twiddle* d_fwd = nullptr;   // [L][n]
   fcn::Twiddle* d_inv = nullptr;   // [L][n]
+  fcn::Twiddle* d_ict = nullptr;   // [L][n] DIT inverse twiddles: [2^s + k] = psi^-(k n / 2^s)
+  fcn::Twiddle* d_twist = nullptr; // [L][n] n^-1 psi^-j
 };
 
 namespace fcn {

@@ -3,7 +3,7 @@
 // Two kernel families produce bit-identical outputs (canonical residues,
 // forward output in the reference's bit-reversed order):
 //
-//  * ntt_v2 (n = 1024 .. 16384, q < 2^61): one persistent CTA per row slot,
+//  * ntt_v2 (n = 1024 .. 16384, 2^34 <= q < 2^56): one persistent CTA per row slot,
 //    n/32 threads each owning 32 residues in registers.  A transform is
 //    three register passes -- 5 stages, LOGN-10 stages, 5 stages -- with two
 //    shared-memory exchanges (row padded by one word per 32 so every access
@@ -23,6 +23,11 @@
 #include <mutex>
 
 #include "fcn_common.cuh"
+
+// min resident CTAs per SM for the v2 kernels (register budget = 64K / (T * minb))
+#ifndef FCN_NTT_MINB
+#define FCN_NTT_MINB(LOGN) (16384 / (1 << (LOGN)))
+#endif
 
 namespace fcn {
 
@@ -229,88 +234,111 @@ __global__ void ntt_v1_inv_last(uint64_t* __restrict__ data, int64_t n_rows, int
 
 // ================================================================= v2
 
-// a*w mod q in [0, 4q) for constant w < q, ws = floor(w 2^64/q), q < 2^61:
-// the quotient estimate omits the a0*ws0 partial product and the low
-// halves of the cross products, so it undershoots floor(a ws / 2^64) by <= 2.
-__device__ __forceinline__ uint64_t mulw(uint64_t a, uint64_t w, uint64_t ws, uint64_t q) {
-  const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32);
-  const uint32_t s0 = (uint32_t)ws, s1 = (uint32_t)(ws >> 32);
-  const uint64_t h = (uint64_t)a1 * s1 + __umulhi(a1, s0) + __umulhi(a0, s1);
-  return a * w - h * q;
-}
-
 __device__ __forceinline__ Twiddle ld_tw(const Twiddle* p) {
+#ifdef FCN_EXP_NO_TW
+  const uint64_t a = (uint64_t)p;
+  return Twiddle{a >> 9, a * 0x9E3779B97F4A7C15ull};
+#else
   const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
   return Twiddle{v.x, v.y};
+#endif
 }
 
-// forward CT butterfly on [0, 8q): X' = X + wY, Y' = X - wY (+4q)
-__device__ __forceinline__ void bfly_f(uint64_t& X, uint64_t& Y, const Twiddle& w, uint64_t q, uint64_t q4) {
-  const uint64_t x = csub(X, q4);
-  const uint64_t t = mulw(Y, w.w, w.s, q);
+// a*w mod q in [0, 4q) for any a < 2^64, constant w < q with ws = floor(w 2^64/q),
+// nq = 2^64 - q.  The quotient estimate h = a1 s1 + hi(a1 s0) + hi(a0 s1) omits
+// a0*s0 and the low halves of the cross products, so it undershoots
+// floor(a ws / 2^64) by at most 2 (remainder < 2q + 2q).  9 IMAD-pipe ops.
+__device__ __forceinline__ uint64_t mulw(uint64_t a, uint64_t w, uint64_t ws, uint64_t nq) {
+#ifdef FCN_EXP_NO_MUL
+  return (a ^ w) + ws;
+#endif
+  uint64_t r;
+  asm("{\n\t"
+      ".reg .u32 a0, a1, w0, w1, s0, s1, n0, n1, hl, hh, rl, rh;\n\t"
+      ".reg .u64 H, R;\n\t"
+      "mov.b64 {a0, a1}, %1;\n\t"
+      "mov.b64 {w0, w1}, %2;\n\t"
+      "mov.b64 {s0, s1}, %3;\n\t"
+      "mov.b64 {n0, n1}, %4;\n\t"
+      "mul.wide.u32 H, a1, s1;\n\t"
+      "mov.b64 {hl, hh}, H;\n\t"
+      "mad.hi.cc.u32 hl, a1, s0, hl;\n\t"
+      "addc.u32 hh, hh, 0;\n\t"
+      "mad.hi.cc.u32 hl, a0, s1, hl;\n\t"
+      "addc.u32 hh, hh, 0;\n\t"
+      "mul.wide.u32 R, a0, w0;\n\t"
+      "mad.wide.u32 R, hl, n0, R;\n\t"
+      "mov.b64 {rl, rh}, R;\n\t"
+      "mad.lo.u32 rh, a0, w1, rh;\n\t"
+      "mad.lo.u32 rh, a1, w0, rh;\n\t"
+      "mad.lo.u32 rh, hl, n1, rh;\n\t"
+      "mad.lo.u32 rh, hh, n0, rh;\n\t"
+      "mov.b64 %0, {rl, rh};\n\t"
+      "}"
+      : "=l"(r)
+      : "l"(a), "l"(w), "l"(ws), "l"(nq));
+  return r;
+}
+
+// Cooley-Tukey butterfly without reduction: X' = X + wY, Y' = X - wY + 4q.
+// Bounds grow by 4q per stage (inputs < q): after <= 14 stages every value
+// is < 57q < 2^62 for q < 2^56.
+__device__ __forceinline__ void bfly(uint64_t& X, uint64_t& Y, const Twiddle& w, uint64_t nq, uint64_t q4) {
+  const uint64_t t = mulw(Y, w.w, w.s, nq);
+  const uint64_t x = X;
   X = x + t;
-  Y = x - t + q4;
+  Y = x + q4 - t;
 }
 
-// inverse GS butterfly on [0, 4q): X' = X + Y, Y' = w (X - Y)
-__device__ __forceinline__ void bfly_i(uint64_t& X, uint64_t& Y, const Twiddle& w, uint64_t q, uint64_t q4) {
-  const uint64_t s = csub(X + Y, q4);
-  const uint64_t d = X - Y + q4;
-  X = s;
-  Y = mulw(d, w.w, w.s, q);
+// x mod q for x < 2^62, 2^34 <= q < 2^56: quotient from the high word
+// (m32 = floor(2^64/q)) undershoots by at most 1.
+__device__ __forceinline__ uint64_t reduce_small(uint64_t x, uint32_t m32, uint64_t q) {
+  const uint32_t qe = __umulhi((uint32_t)(x >> 32), m32);
+  const uint64_t r = x - (uint64_t)qe * q;
+  return r >= q ? r - q : r;
 }
 
-// R forward stages on G = 2^R registers; twiddle of block blk at local stage u
-// is tw[base_u + blk] with base_u = (1 << (s0 + u)) + (b << u).
-template <int R, int OFF>
-__device__ __forceinline__ void fwd_stages(uint64_t* x, int s0, int b, const Twiddle* __restrict__ tw, uint64_t q,
-                                           uint64_t q4) {
+// Forward (natural in, bit-reversed out; reference ring.py:199-217): R
+// stages starting at global stage s0 on G = 2^R registers whose elements lie
+// in block b of size n/2^s0; pair twiddle psi[2^s + b 2^u + blk].
+template <int R>
+__device__ __forceinline__ void fwd_ct(uint64_t* x, int s0, int b, const Twiddle* __restrict__ tw, uint64_t nq,
+                                       uint64_t q4) {
   constexpr int G = 1 << R;
 #pragma unroll
   for (int u = 0; u < R; ++u) {
     const int tb = (1 << (s0 + u)) + (b << u);
-    const int h = G >> (u + 1);  // butterfly span in registers
-    Twiddle w;
+    const int h = G >> (u + 1);
 #pragma unroll
-    for (int bi = 0; bi < G / 2; ++bi) {  // flattened (block, offset) loop: always fully unrolled
-      const int blk = bi / h, jj = bi % h;
-      if (jj == 0) w = ld_tw(tw + tb + blk);
-      const int j = blk * 2 * h + jj;
-      bfly_f(x[OFF + j], x[OFF + j + h], w, q, q4);
+    for (int blk = 0; blk < (1 << u); ++blk) {
+      const Twiddle w = ld_tw(tw + tb + blk);
+#pragma unroll
+      for (int jj = 0; jj < h; ++jj) {
+        const int j = blk * 2 * h + jj;
+        bfly(x[j], x[j + h], w, nq, q4);
+      }
     }
   }
 }
 
-// R inverse stages on G = 2^R registers starting at global inverse stage s0;
-// twiddle index (n >> (s+1)) + (b << (R-1-u)) + blk.  When LASTSCALE, the
-// final stage (s0 + R - 1 == logn - 1) is merged with n^-1 and canonicalised.
-template <int R, int OFF, bool LASTSCALE>
-__device__ __forceinline__ void inv_stages(uint64_t* x, int s0, int logn, int b, const Twiddle* __restrict__ tw,
-                                           const LimbConst& c) {
+// Inverse as a decimation-in-time transform on the bit-reversed input:
+// stage s pairs elements 2^s apart with twiddle ict[2^s + (idx mod 2^s)].
+// Registers hold elements base + (j << s0) with base = (block) + o, o < 2^s0.
+template <int R>
+__device__ __forceinline__ void inv_ct(uint64_t* x, int s0, int o, const Twiddle* __restrict__ tw, uint64_t nq,
+                                       uint64_t q4) {
   constexpr int G = 1 << R;
-  const uint64_t q = c.q, q4 = 4 * c.q;
 #pragma unroll
   for (int u = 0; u < R; ++u) {
-    const int s = s0 + u;
     const int hd = 1 << u;
-    const int tb = (1 << (logn - s - 1)) + (b << (R - 1 - u));
-    if (LASTSCALE && u == R - 1) {
+    const int tb = (1 << (s0 + u)) + o;
 #pragma unroll
-      for (int jj = 0; jj < G / 2; ++jj) {
-        const uint64_t X = x[OFF + jj], Y = x[OFF + jj + G / 2];
-        const uint64_t a = mulw(X + Y, c.ninv, c.ninv_s, q);
-        const uint64_t d = mulw(X - Y + q4, c.wlast, c.wlast_s, q);
-        x[OFF + jj] = csub(csub(a, 2 * q), q);
-        x[OFF + jj + G / 2] = csub(csub(d, 2 * q), q);
-      }
-    } else {
-      Twiddle w;
+    for (int jj = 0; jj < hd; ++jj) {
+      const Twiddle w = ld_tw(tw + tb + (jj << s0));
 #pragma unroll
-      for (int bi = 0; bi < G / 2; ++bi) {
-        const int blk = bi / hd, jj = bi % hd;
-        if (jj == 0) w = ld_tw(tw + tb + blk);
+      for (int blk = 0; blk < (G >> (u + 1)); ++blk) {
         const int j = blk * 2 * hd + jj;
-        bfly_i(x[OFF + j], x[OFF + j + hd], w, q, q4);
+        bfly(x[j], x[j + hd], w, nq, q4);
       }
     }
   }
@@ -324,9 +352,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 template <int LOGN>
-__global__ void __launch_bounds__((1 << LOGN) / 32, 16384 / (1 << LOGN)) ntt_v2_fwd(uint64_t* __restrict__ data, int64_t n_rows, int period,
-                                                               int offset, const LimbConst* __restrict__ lcs,
-                                                               const Twiddle* __restrict__ tws) {
+__global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
+    ntt_v2_fwd(uint64_t* __restrict__ data, int64_t n_rows, int period, int offset, const LimbConst* __restrict__ lcs,
+               const Twiddle* __restrict__ tws) {
   constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
   extern __shared__ uint64_t sm[];
   const int tid = threadIdx.x;
@@ -340,10 +368,12 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, 16384 / (1 << LOGN)) ntt_v2_
   }
   for (; row < n_rows; row += gridDim.x) {
     const int limb = offset + (int)(row % period);
-    const uint64_t q = lcs[limb].q, q4 = 4 * q;
+    const LimbConst& c = lcs[limb];
+    const uint64_t q = c.q, nq = c.nq, q4 = 4 * q;
+    const uint32_t m32 = c.m32;
     const Twiddle* tw = tws + (int64_t)limb * N;
     // pass 1: stages 0..4 on t + j*T (twiddles uniform across the CTA)
-    fwd_stages<5, 0>(x, 0, 0, tw, q, q4);
+    fwd_ct<5>(x, 0, 0, tw, nq, q4);
 #pragma unroll
     for (int j = 0; j < 32; ++j) sm[phys(tid + j * T)] = x[j];
     __syncthreads();
@@ -352,21 +382,16 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, 16384 / (1 << LOGN)) ntt_v2_
 #pragma unroll
       for (int i = 0; i < 32 / GM; ++i) {
         const int g = tid + i * T;
-        const int b = g >> 5, o = g & 31;
-        const int base = (b << (5 + RM)) + o;
+        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
 #pragma unroll
         for (int j = 0; j < GM; ++j) x[i * GM + j] = sm[phys(base + j * 32)];
       }
 #pragma unroll
-      for (int i = 0; i < 32 / GM; ++i) {
-        const int b = (tid + i * T) >> 5;
-        fwd_stages<(RM > 0 ? RM : 1), 0>(x + i * GM, 5, b, tw, q, q4);
-      }
+      for (int i = 0; i < 32 / GM; ++i) fwd_ct<(RM > 0 ? RM : 1)>(x + i * GM, 5, (tid + i * T) >> 5, tw, nq, q4);
 #pragma unroll
       for (int i = 0; i < 32 / GM; ++i) {
         const int g = tid + i * T;
-        const int b = g >> 5, o = g & 31;
-        const int base = (b << (5 + RM)) + o;
+        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
 #pragma unroll
         for (int j = 0; j < GM; ++j) sm[phys(base + j * 32)] = x[i * GM + j];
       }
@@ -375,9 +400,9 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, 16384 / (1 << LOGN)) ntt_v2_
     // pass 3: the last 5 stages on 32 contiguous residues, canonical out
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = sm[tid * 33 + j];
-    fwd_stages<5, 0>(x, LOGN - 5, tid, tw, q, q4);
+    fwd_ct<5>(x, LOGN - 5, tid, tw, nq, q4);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) sm[tid * 33 + j] = csub(csub(csub(x[j], q4), 2 * q), q);
+    for (int j = 0; j < 32; ++j) sm[tid * 33 + j] = reduce_small(x[j], m32, q);
     __syncthreads();
     // prefetch the next row's pass-1 operands, then copy this row out (coalesced)
     const int64_t nxt = row + gridDim.x;
@@ -399,9 +424,9 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, 16384 / (1 << LOGN)) ntt_v2_
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__((1 << LOGN) / 32, 16384 / (1 << LOGN)) ntt_v2_inv(uint64_t* __restrict__ data, int64_t n_rows, int period,
-                                                               int offset, const LimbConst* __restrict__ lcs,
-                                                               const Twiddle* __restrict__ tws) {
+__global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
+    ntt_v2_inv(uint64_t* __restrict__ data, int64_t n_rows, int period, int offset, const LimbConst* __restrict__ lcs,
+               const Twiddle* __restrict__ tws, const Twiddle* __restrict__ twists) {
   constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
   extern __shared__ uint64_t sm[];
   const int tid = threadIdx.x;
@@ -415,14 +440,16 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, 16384 / (1 << LOGN)) ntt_v2_
   uint64_t x[32];
   for (; row < n_rows; row += gridDim.x) {
     const int limb = offset + (int)(row % period);
-    const LimbConst c = lcs[limb];
+    const LimbConst& c = lcs[limb];
+    const uint64_t q = c.q, nq = c.nq, q4 = 4 * q;
     const Twiddle* tw = tws + (int64_t)limb * N;
+    const Twiddle* twist = twists + (int64_t)limb * N;
     cp_async_wait_all();
     __syncthreads();
-    // pass 1: inverse stages 0..4 on 32 contiguous residues
+    // pass 1: stages 0..4 on 32 contiguous residues (twiddles uniform)
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = sm[tid * 33 + j];
-    inv_stages<5, 0, false>(x, 0, LOGN, tid, tw, c);
+    inv_ct<5>(x, 0, 0, tw, nq, q4);
 #pragma unroll
     for (int j = 0; j < 32; ++j) sm[tid * 33 + j] = x[j];
     __syncthreads();
@@ -431,21 +458,16 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, 16384 / (1 << LOGN)) ntt_v2_
 #pragma unroll
       for (int i = 0; i < 32 / GM; ++i) {
         const int g = tid + i * T;
-        const int b = g >> 5, o = g & 31;
-        const int base = (b << (5 + RM)) + o;
+        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
 #pragma unroll
         for (int j = 0; j < GM; ++j) x[i * GM + j] = sm[phys(base + j * 32)];
       }
 #pragma unroll
-      for (int i = 0; i < 32 / GM; ++i) {
-        const int b = (tid + i * T) >> 5;
-        inv_stages<(RM > 0 ? RM : 1), 0, false>(x + i * GM, 5, LOGN, b, tw, c);
-      }
+      for (int i = 0; i < 32 / GM; ++i) inv_ct<(RM > 0 ? RM : 1)>(x + i * GM, 5, (tid + i * T) & 31, tw, nq, q4);
 #pragma unroll
       for (int i = 0; i < 32 / GM; ++i) {
         const int g = tid + i * T;
-        const int b = g >> 5, o = g & 31;
-        const int base = (b << (5 + RM)) + o;
+        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
 #pragma unroll
         for (int j = 0; j < GM; ++j) sm[phys(base + j * 32)] = x[i * GM + j];
       }
@@ -461,10 +483,16 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, 16384 / (1 << LOGN)) ntt_v2_
       for (int i = tid; i < N; i += T) cp_async8(&sm[phys(i)], p + i);
       cp_async_commit();
     }
-    inv_stages<5, 0, true>(x, LOGN - 5, LOGN, 0, tw, c);
+    inv_ct<5>(x, LOGN - 5, tid, tw, nq, q4);
+    // twist by n^-1 psi^-j, canonicalise, store coalesced
     uint64_t* p = data + row * N;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) p[tid + j * T] = x[j];
+    for (int j = 0; j < 32; ++j) {
+      const Twiddle w = ld_tw(twist + tid + j * T);
+      uint64_t v = mulw(x[j], w.w, w.s, nq);
+      v = csub(v, 2 * q);
+      p[tid + j * T] = csub(v, q);
+    }
   }
   cp_async_wait_all();
 }
@@ -556,7 +584,7 @@ static void launch_v2_t(bool fwd, int grid, uint64_t* d, int64_t n_rows, int per
   if (fwd)
     ntt_v2_fwd<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fwd);
   else
-    ntt_v2_inv<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_inv);
+    ntt_v2_inv<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_ict, r->d_twist);
 }
 
 int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st) {
@@ -565,7 +593,10 @@ int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int o
   if (g_init_err != cudaSuccess) return check_cuda(g_init_err, "ntt init");
   const int logn = r->logn;
   bool v2 = logn >= 10 && logn <= 14;
-  for (int l = 0; v2 && l < period; ++l) v2 = r->primes[offset + l] < (1ull << 61);
+  for (int l = 0; v2 && l < period; ++l) {
+    const uint64_t q = r->primes[offset + l];
+    v2 = q >= (1ull << 34) && q < (1ull << 56);
+  }
   if (!v2) return launch_v1(r, d, n_rows, period, offset, fwd, st);
   const V2Entry& e = g_v2[fwd ? 1 : 0][logn];
   int64_t grid = (int64_t)g_sms * e.ctas_per_sm;

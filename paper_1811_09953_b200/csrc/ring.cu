@@ -84,6 +84,9 @@ LimbConst make_limb_const(uint64_t q, int n, uint64_t ipsi1) {
   c.one_s = h_shoup(1, q);
   c.r64 = (uint64_t)(((unsigned __int128)1 << 64) % q);
   c.r64_s = h_shoup(c.r64, q);
+  c.nq = (uint64_t)0 - q;
+  const unsigned __int128 m = (((unsigned __int128)1) << 64) / q;
+  c.m32 = (m >> 32) ? 0u : (uint32_t)m;
   return c;
 }
 
@@ -204,7 +207,7 @@ extern "C" int fcn_ring_create(int device, int n, int count, const uint64_t* pri
   r->n = n;
   r->logn = bitlen64((uint64_t)n) - 1;
   r->L = count;
-  std::vector<Twiddle> fw((size_t)count * n), iv((size_t)count * n);
+  std::vector<Twiddle> fw((size_t)count * n), iv((size_t)count * n), ict((size_t)count * n), tws((size_t)count * n);
   for (int l = 0; l < count; ++l) {
     const uint64_t q = primes[l];
     if (q >= (1ull << 62) || !h_is_prime(q)) {
@@ -232,6 +235,19 @@ extern "C" int fcn_ring_create(int device, int n, int count, const uint64_t* pri
       fw[(size_t)l * n + i] = a;
       iv[(size_t)l * n + i] = b;
     }
+    // DIT inverse: stage s (pairs 2^s apart) uses W_s^k = psi^-(k n / 2^s) at [2^s + k];
+    // the final twist multiplies output j by n^-1 psi^-j.
+    const uint64_t ninv = h_powmod((uint64_t)n % q, q - 2, q);
+    ict[(size_t)l * n] = Twiddle{1, h_shoup(1, q)};
+    for (int sg = 0; (1 << sg) < n; ++sg)
+      for (int k = 0; k < (1 << sg); ++k) {
+        const uint64_t w = ipw[(size_t)k * (n >> sg)];
+        ict[(size_t)l * n + (1 << sg) + k] = Twiddle{w, h_shoup(w, q)};
+      }
+    for (int j = 0; j < n; ++j) {
+      const uint64_t w = h_mulmod(ninv, ipw[j], q);
+      tws[(size_t)l * n + j] = Twiddle{w, h_shoup(w, q)};
+    }
     r->host_lc.push_back(make_limb_const(q, n, iv[(size_t)l * n + 1].w));
   }
   DeviceGuard g(device);
@@ -241,6 +257,10 @@ extern "C" int fcn_ring_create(int device, int n, int count, const uint64_t* pri
   if (e == cudaSuccess) e = cudaMemcpy(r->d_lc, r->host_lc.data(), sizeof(LimbConst) * count, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(r->d_fwd, fw.data(), sizeof(Twiddle) * fw.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(r->d_inv, iv.data(), sizeof(Twiddle) * iv.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&r->d_ict, sizeof(Twiddle) * ict.size());
+  if (e == cudaSuccess) e = cudaMalloc(&r->d_twist, sizeof(Twiddle) * tws.size());
+  if (e == cudaSuccess) e = cudaMemcpy(r->d_ict, ict.data(), sizeof(Twiddle) * ict.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(r->d_twist, tws.data(), sizeof(Twiddle) * tws.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     fcn_ring_destroy(r);
     return check_cuda(e, "fcn_ring_create upload");
@@ -256,6 +276,8 @@ extern "C" int fcn_ring_destroy(fcn_ring* r) {
     cudaFree(r->d_lc);
     cudaFree(r->d_fwd);
     cudaFree(r->d_inv);
+    cudaFree(r->d_ict);
+    cudaFree(r->d_twist);
   }
   delete r;
   return FCN_OK;
