@@ -85,6 +85,10 @@ struct fcn_ring {
   fcn::Twiddle* d_inv = nullptr;   // [L][n]
   fcn::Twiddle* d_ict = nullptr;   // [L][n] DIT inverse twiddles: [2^s + k] = psi^-(k n / 2^s)
   fcn::Twiddle* d_twist = nullptr; // [L][n] n^-1 psi^-j
+  // forward twiddles of the last five stages laid out for coalesced loads in
+  // the register pass that owns 32 contiguous residues per thread:
+  // [L][u][blk][t] = psi[2^(logn-5+u) + t 2^u + blk], t < n/32 (n >= 32)
+  fcn::Twiddle* d_fwd_last = nullptr;
 };
 
 namespace fcn {

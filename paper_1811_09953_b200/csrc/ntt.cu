@@ -321,6 +321,28 @@ __device__ __forceinline__ void fwd_ct(uint64_t* x, int s0, int b, const Twiddle
   }
 }
 
+// The forward's last five stages for a thread owning 32 contiguous residues
+// (group t): twiddles come from the transposed table [u][blk][t] so a warp's
+// loads are 32 consecutive 16-byte entries.
+__device__ __forceinline__ void fwd_ct_last(uint64_t* x, int t, int T, const Twiddle* __restrict__ tl, uint64_t nq,
+                                            uint64_t q4) {
+  int off = 0;
+#pragma unroll
+  for (int u = 0; u < 5; ++u) {
+    const int h = 32 >> (u + 1);
+#pragma unroll
+    for (int blk = 0; blk < (1 << u); ++blk) {
+      const Twiddle w = ld_tw(tl + off + blk * T + t);
+#pragma unroll
+      for (int jj = 0; jj < h; ++jj) {
+        const int j = blk * 2 * h + jj;
+        bfly(x[j], x[j + h], w, nq, q4);
+      }
+    }
+    off += (1 << u) * T;
+  }
+}
+
 // Inverse as a decimation-in-time transform on the bit-reversed input:
 // stage s pairs elements 2^s apart with twiddle ict[2^s + (idx mod 2^s)].
 // Registers hold elements base + (j << s0) with base = (block) + o, o < 2^s0.
@@ -354,7 +376,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <int LOGN>
 __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     ntt_v2_fwd(uint64_t* __restrict__ data, int64_t n_rows, int period, int offset, const LimbConst* __restrict__ lcs,
-               const Twiddle* __restrict__ tws) {
+               const Twiddle* __restrict__ tws, const Twiddle* __restrict__ twl) {
   constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
   extern __shared__ uint64_t sm[];
   const int tid = threadIdx.x;
@@ -400,7 +422,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     // pass 3: the last 5 stages on 32 contiguous residues, canonical out
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = sm[tid * 33 + j];
-    fwd_ct<5>(x, LOGN - 5, tid, tw, nq, q4);
+    fwd_ct_last(x, tid, T, twl + (int64_t)limb * N, nq, q4);
 #pragma unroll
     for (int j = 0; j < 32; ++j) sm[tid * 33 + j] = reduce_small(x[j], m32, q);
     __syncthreads();
@@ -582,7 +604,7 @@ static void launch_v2_t(bool fwd, int grid, uint64_t* d, int64_t n_rows, int per
                         cudaStream_t st) {
   const size_t sm = v2_smem(LOGN);
   if (fwd)
-    ntt_v2_fwd<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fwd);
+    ntt_v2_fwd<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fwd, r->d_fwd_last);
   else
     ntt_v2_inv<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_ict, r->d_twist);
 }

@@ -208,6 +208,7 @@ extern "C" int fcn_ring_create(int device, int n, int count, const uint64_t* pri
   r->logn = bitlen64((uint64_t)n) - 1;
   r->L = count;
   std::vector<Twiddle> fw((size_t)count * n), iv((size_t)count * n), ict((size_t)count * n), tws((size_t)count * n);
+  std::vector<Twiddle> fl((size_t)count * n);
   for (int l = 0; l < count; ++l) {
     const uint64_t q = primes[l];
     if (q >= (1ull << 62) || !h_is_prime(q)) {
@@ -248,6 +249,15 @@ extern "C" int fcn_ring_create(int device, int n, int count, const uint64_t* pri
       const uint64_t w = h_mulmod(ninv, ipw[j], q);
       tws[(size_t)l * n + j] = Twiddle{w, h_shoup(w, q)};
     }
+    if (n >= 32) {
+      const int T = n / 32;
+      size_t o = (size_t)l * n;
+      for (int u = 0; u < 5; ++u) {
+        const int s0 = (r->logn - 5) + u;
+        for (int blk = 0; blk < (1 << u); ++blk)
+          for (int t = 0; t < T; ++t) fl[o++] = fw[(size_t)l * n + (1 << s0) + ((size_t)t << u) + blk];
+      }
+    }
     r->host_lc.push_back(make_limb_const(q, n, iv[(size_t)l * n + 1].w));
   }
   DeviceGuard g(device);
@@ -261,6 +271,8 @@ extern "C" int fcn_ring_create(int device, int n, int count, const uint64_t* pri
   if (e == cudaSuccess) e = cudaMalloc(&r->d_twist, sizeof(Twiddle) * tws.size());
   if (e == cudaSuccess) e = cudaMemcpy(r->d_ict, ict.data(), sizeof(Twiddle) * ict.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(r->d_twist, tws.data(), sizeof(Twiddle) * tws.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&r->d_fwd_last, sizeof(Twiddle) * fl.size());
+  if (e == cudaSuccess) e = cudaMemcpy(r->d_fwd_last, fl.data(), sizeof(Twiddle) * fl.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     fcn_ring_destroy(r);
     return check_cuda(e, "fcn_ring_create upload");
@@ -278,6 +290,7 @@ extern "C" int fcn_ring_destroy(fcn_ring* r) {
     cudaFree(r->d_inv);
     cudaFree(r->d_ict);
     cudaFree(r->d_twist);
+    cudaFree(r->d_fwd_last);
   }
   delete r;
   return FCN_OK;
