@@ -138,6 +138,13 @@ int fcn_add_plain_terms(const fcn_ctx* ctx, int lane, uint64_t* d_cts, int64_t n
 int fcn_linear_mac(const fcn_ctx* ctx, const uint64_t* d_in0, int64_t n_in0, const uint64_t* d_in1,
                    int64_t n_in1, const int32_t* d_rowptr, const int32_t* d_col, const int32_t* d_rot,
                    const int64_t* d_coef, uint64_t* d_out, int64_t n_out, void* stream);
+/* Same, with host-known layer facts enabling the fast path: no_rot != 0
+ * when every rot is 0 (constant plaintexts, the SIMD-batched encoding) and
+ * max_abs_coef = max |coef| (0 = unknown).  Output is identical.          */
+int fcn_linear_mac_ex(const fcn_ctx* ctx, const uint64_t* d_in0, int64_t n_in0, const uint64_t* d_in1,
+                      int64_t n_in1, const int32_t* d_rowptr, const int32_t* d_col, const int32_t* d_rot,
+                      const int64_t* d_coef, uint64_t* d_out, int64_t n_out, int no_rot, uint64_t max_abs_coef,
+                      void* stream);
 
 /* fv.mul_ct (fv.py:498-549): exact tensor in the extended base, exact
  * floor((t*T + q>>1)/q) mod q, base-beta digits of c2', key switching.

@@ -150,6 +150,50 @@ __device__ __forceinline__ void add128(uint64_t& hi, uint64_t& lo, uint64_t ph, 
 __device__ __forceinline__ uint64_t addmod(uint64_t a, uint64_t b, uint64_t q) { return csub(a + b, q); }
 __device__ __forceinline__ uint64_t submod(uint64_t a, uint64_t b, uint64_t q) { return csub(a + q - b, q); }
 
+// a*w mod q in [0, 4q) for any a < 2^64, constant w < q with ws = floor(w 2^64/q),
+// nq = 2^64 - q.  The quotient estimate h = a1 s1 + hi(a1 s0) + hi(a0 s1) omits
+// a0*s0 and the low halves of the cross products, so it undershoots
+// floor(a ws / 2^64) by at most 2 (remainder < 2q + 2q).  9 IMAD-pipe ops.
+__device__ __forceinline__ uint64_t mulw(uint64_t a, uint64_t w, uint64_t ws, uint64_t nq) {
+#ifdef FCN_EXP_NO_MUL
+  return (a ^ w) + ws;
+#endif
+  uint64_t r;
+  asm("{\n\t"
+      ".reg .u32 a0, a1, w0, w1, s0, s1, n0, n1, hl, hh, rl, rh;\n\t"
+      ".reg .u64 H, R;\n\t"
+      "mov.b64 {a0, a1}, %1;\n\t"
+      "mov.b64 {w0, w1}, %2;\n\t"
+      "mov.b64 {s0, s1}, %3;\n\t"
+      "mov.b64 {n0, n1}, %4;\n\t"
+      "mul.wide.u32 H, a1, s1;\n\t"
+      "mov.b64 {hl, hh}, H;\n\t"
+      "mad.hi.cc.u32 hl, a1, s0, hl;\n\t"
+      "addc.u32 hh, hh, 0;\n\t"
+      "mad.hi.cc.u32 hl, a0, s1, hl;\n\t"
+      "addc.u32 hh, hh, 0;\n\t"
+      "mul.wide.u32 R, a0, w0;\n\t"
+      "mad.wide.u32 R, hl, n0, R;\n\t"
+      "mov.b64 {rl, rh}, R;\n\t"
+      "mad.lo.u32 rh, a0, w1, rh;\n\t"
+      "mad.lo.u32 rh, a1, w0, rh;\n\t"
+      "mad.lo.u32 rh, hl, n1, rh;\n\t"
+      "mad.lo.u32 rh, hh, n0, rh;\n\t"
+      "mov.b64 %0, {rl, rh};\n\t"
+      "}"
+      : "=l"(r)
+      : "l"(a), "l"(w), "l"(ws), "l"(nq));
+  return r;
+}
+
+// x mod q for x < 2^62, 2^34 <= q < 2^56: quotient from the high word
+// (m32 = floor(2^64/q)) undershoots by at most 1.
+__device__ __forceinline__ uint64_t reduce_small(uint64_t x, uint32_t m32, uint64_t q) {
+  const uint32_t qe = __umulhi((uint32_t)(x >> 32), m32);
+  const uint64_t r = x - (uint64_t)qe * q;
+  return r >= q ? r - q : r;
+}
+
 // ---------------------------------------------------- host-side helpers
 
 inline uint64_t h_mulmod(uint64_t a, uint64_t b, uint64_t m) {
@@ -169,7 +213,10 @@ inline uint64_t h_shoup(uint64_t w, uint64_t q) { return (uint64_t)(((unsigned _
 bool h_is_prime(uint64_t v);
 int bitlen64(uint64_t v);
 LimbConst make_limb_const(uint64_t q, int n, uint64_t ipsi1);
-int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st);
+// Batched NTT over rows; the forward may read row r's input from
+// src + (r / src_div) * n (broadcast of one source row to several limbs).
+int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st,
+               const uint64_t* src = nullptr, int src_div = 1);
 
 inline int grid_for(int64_t work, int block, int max_blocks = 148 * 16) {
   int64_t g = (work + block - 1) / block;

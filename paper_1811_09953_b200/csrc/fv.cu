@@ -65,6 +65,7 @@ struct fcn_ctx {
   std::vector<uint64_t> primes, aux, lanes;
   fcn_ring* ext = nullptr;
   fcn::MulCtConst* d_mc = nullptr;  // [n_lanes]
+  std::vector<fcn::MulCtConst> host_mc;
   unsigned long long* d_fallbacks = nullptr;
 };
 
@@ -198,6 +199,8 @@ __device__ __noinline__ int64_t exact_frac_floor(const uint64_t* r, int k, const
   return mw_reduce_q<NW>(a, cc, g_est);
 }
 
+__device__ __forceinline__ double cc_hq(const MulCtConst* __restrict__ cc) { return __ldg(&cc->hq); }
+
 // ------------------------------------------------------------ add_pt
 
 __global__ void add_plain_kernel(uint64_t* __restrict__ cts, int64_t n_terms, const int32_t* __restrict__ ct_index,
@@ -291,16 +294,114 @@ __global__ void __launch_bounds__(256) mac_kernel(const uint64_t* __restrict__ i
   *reinterpret_cast<ulonglong2*>(out + (int64_t)o * ct_words + (int64_t)r * n + j0) = res;
 }
 
+// Fast path: all rotations 0 (constant plaintexts) and max|coef| * q small
+// enough that `fold` consecutive products fit one 64-bit accumulator.  Each
+// term is then one IMAD.WIDE + one IMAD per residue (acc += x * |c|),
+// accumulators are folded back below 4q every `fold` terms.  Four residues
+// per thread (two 16-byte loads) amortise the term metadata.
+__global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restrict__ in0, int64_t n_in0,
+                                                       const uint64_t* __restrict__ in1,
+                                                       const int32_t* __restrict__ rowptr,
+                                                       const int32_t* __restrict__ col,
+                                                       const int64_t* __restrict__ coef, uint64_t* __restrict__ out,
+                                                       int logn, int k, const LimbConst* __restrict__ lcs, int fold) {
+  const int n = 1 << logn;
+  const int o = blockIdx.y;
+  const int r = blockIdx.z;
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (j0 >= n) return;
+  const LimbConst& c = lcs[r % k];
+  const uint64_t q = c.q, nq = c.nq, one_s = c.one_s;
+  const int64_t ct_words = (int64_t)2 * k * n;
+  uint64_t pos[4] = {0, 0, 0, 0}, neg[4] = {0, 0, 0, 0};
+  const int e0 = rowptr[o], e1 = rowptr[o + 1];
+  int cnt = 0;
+  for (int e = e0; e < e1; ++e) {
+    const int cl = __ldg(col + e);
+    const int64_t cf = __ldg(coef + e);
+    const uint64_t* src = (cl < n_in0 ? in0 + (int64_t)cl * ct_words : in1 + (int64_t)(cl - n_in0) * ct_words) +
+                          (int64_t)r * n + j0;
+    const ulonglong2 va = *reinterpret_cast<const ulonglong2*>(src);
+    const ulonglong2 vb = *reinterpret_cast<const ulonglong2*>(src + 2);
+    if (cf >= 0) {
+      const uint64_t m = (uint64_t)cf;
+      pos[0] += va.x * m;
+      pos[1] += va.y * m;
+      pos[2] += vb.x * m;
+      pos[3] += vb.y * m;
+    } else {
+      const uint64_t m = (uint64_t)(-cf);
+      neg[0] += va.x * m;
+      neg[1] += va.y * m;
+      neg[2] += vb.x * m;
+      neg[3] += vb.y * m;
+    }
+    if (++cnt == fold) {
+      cnt = 0;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        pos[v] = mulw(pos[v], 1, one_s, nq);
+        neg[v] = mulw(neg[v], 1, one_s, nq);
+      }
+    }
+  }
+  uint64_t res[4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const uint64_t a = csub(csub(mulw(pos[v], 1, one_s, nq), 2 * q), q);
+    const uint64_t b = csub(csub(mulw(neg[v], 1, one_s, nq), 2 * q), q);
+    res[v] = submod(a, b, q);
+  }
+  uint64_t* dst = out + (int64_t)o * ct_words + (int64_t)r * n + j0;
+  *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(res[0], res[1]);
+  *reinterpret_cast<ulonglong2*>(dst + 2) = make_ulonglong2(res[2], res[3]);
+}
+
 // ------------------------------------------------------------- mul_ct
 
-// Centered lift of c0/c1 into the extended base (fv.py:463-470).
+// Kernel-parameter constant blocks (constant bank: uniform operands, no
+// global loads in the per-coefficient loops), sized by the limb counts.
+template <int KQ, int KA>
+struct LiftP {
+  int k, m, K;
+  uint64_t q[KQ], nq[KQ], qinv[KQ], qinv_s[KQ];
+  double rq[KQ];
+  uint64_t p[KA], np[KA], p_one_s[KA];
+  uint64_t lc[KA][KQ], lc_s[KA][KQ];
+  uint64_t nqp[KA], nqp_s[KA];  // p_j - (q mod p_j)
+};
+
+template <int KQ, int KE>
+struct RescaleP {
+  int k, K, D, w, direct, dwords;
+  uint64_t q[KE], nq[KE], binv[KE], binv_s[KE];
+  double rb[KE];
+  uint64_t one_s[KQ], rq_dummy[KQ];
+  double rq[KQ];
+  uint64_t beta[KQ], beta_s[KQ];
+  uint64_t rc[KQ][KE], rc_s[KQ][KE];
+  uint64_t ntp[KQ], ntp_s[KQ];  // q_i - (tP mod q_i)
+  uint64_t qinv[KQ], qinv_s[KQ];
+  uint64_t dpw[KQ][3], dpw_s[KQ][3];
+};
+
+// canonical x mod q for any x < 2^64 (approximate-quotient product by 1)
+__device__ __forceinline__ uint64_t reduce_any(uint64_t x, uint64_t q, uint64_t one_s, uint64_t nq) {
+  const uint64_t r = mulw(x, 1, one_s, nq);
+  return csub(csub(r, 2 * q), q);
+}
+
+// Centered lift of c0/c1 into the extended base (fv.py:463-470):
+// y_i = x_i (q/q_i)^-1 (lazy, < 4 q_i), v' = round(sum y_i/q_i) (float64
+// with an exact multiword fallback near the tie), aux residue
+// = sum y_i [q/q_i]_p - v' [q]_p.
 template <int KQ, int KA, int NW>
 __global__ void __launch_bounds__(256) lift_kernel(const uint64_t* __restrict__ in, uint64_t* __restrict__ ext,
-                                                   int64_t npoly, int logn, const MulCtConst* __restrict__ cc,
-                                                   const LimbConst* __restrict__ lcs,
+                                                   int64_t npoly, int logn, const __grid_constant__ LiftP<KQ, KA> P,
+                                                   const MulCtConst* __restrict__ cc,
                                                    unsigned long long* __restrict__ fallbacks) {
   const int n = 1 << logn;
-  const int k = cc->k, m = cc->m, K = cc->K;
+  const int k = P.k, m = P.m, K = P.K;
   const int64_t total = npoly << logn;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t poly = e >> logn;
@@ -313,8 +414,8 @@ __global__ void __launch_bounds__(256) lift_kernel(const uint64_t* __restrict__ 
       if (i < k) {
         const uint64_t x = in[(poly * k + i) * n + coef];
         ext[(poly * K + i) * n + coef] = x;
-        y[i] = shoup(x, cc->qinv[i], cc->qinv_s[i], lcs[i].q);
-        f += (double)y[i] * cc->rq[i];
+        y[i] = mulw(x, P.qinv[i], P.qinv_s[i], P.nq[i]);
+        f += (double)y[i] * P.rq[i];
       }
     }
     int64_t v = (int64_t)floor(f);
@@ -338,15 +439,12 @@ __global__ void __launch_bounds__(256) lift_kernel(const uint64_t* __restrict__ 
 #pragma unroll
     for (int j = 0; j < KA; ++j) {
       if (j < m) {
-        const LimbConst& pc = lcs[k + j];
-        const uint64_t p = pc.q, p2 = pc.q2;
-        uint64_t acc = 0;
+        const uint64_t np = P.np[j];
+        uint64_t acc = mulw((uint64_t)v, P.nqp[j], P.nqp_s[j], np);
 #pragma unroll
         for (int i = 0; i < KQ; ++i)
-          if (i < k) acc = csub(acc + shoup_lazy(y[i], cc->lc[j][i], cc->lc_s[j][i], p), p2);
-        acc = csub(acc, p);
-        acc = addmod(acc, cc->lvq[j][v], p);
-        ext[(poly * K + k + j) * n + coef] = acc;
+          if (i < k) acc += mulw(y[i], P.lc[j][i], P.lc_s[j][i], np);
+        ext[(poly * K + k + j) * n + coef] = reduce_any(acc, P.p[j], P.p_one_s[j], np);
       }
     }
   }
@@ -385,22 +483,24 @@ __global__ void tensor_kernel(const uint64_t* __restrict__ A, const uint64_t* __
 
 // Exact rescale R = floor((t T + (q-1)/2) / q) mod q from the ext-base
 // residues of T (fv.py:473-490, 517-522); for the third tensor poly the
-// base-beta digits of R (fv.py:524-533) are emitted instead.
+// base-beta digits of R (fv.py:524-533) are emitted instead: one row per
+// digit when every digit is already < q_i (P.direct), else per-limb rows.
 template <int KQ, int KE, int NW>
 __global__ void __launch_bounds__(256) rescale_kernel(const uint64_t* __restrict__ T, uint64_t* __restrict__ R01,
                                                       uint64_t* __restrict__ DG, int64_t C, int logn,
+                                                      const __grid_constant__ RescaleP<KQ, KE> P,
                                                       const MulCtConst* __restrict__ cc,
-                                                      const LimbConst* __restrict__ lcs,
                                                       unsigned long long* __restrict__ fallbacks) {
   const int n = 1 << logn;
-  const int k = cc->k, K = cc->K;
+  const int k = P.k, K = P.K;
   const int64_t total = (C * 3) << logn;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t cp = e >> logn;
     const int coef = (int)(e & (n - 1));
     const int64_t ct = cp / 3;
     const int p = (int)(cp % 3);
-    // 1. y_j = T_j (B/b_j)^-1 mod b_j and the (exactly rounded) CRT overflow count v
+    // 1. y_j = T_j (B/b_j)^-1 mod b_j (lazy, < 4 b_j) and the CRT overflow count
+    //    v = round(sum y_j / b_j): |T|/B < 1/8 keeps it far from a half
     uint64_t y[KE];
     double fv = 0.0;
 #pragma unroll
@@ -408,23 +508,23 @@ __global__ void __launch_bounds__(256) rescale_kernel(const uint64_t* __restrict
       y[j] = 0;
       if (j < K) {
         const uint64_t x = T[(cp * K + j) * n + coef];
-        y[j] = shoup(x, cc->binv[j], cc->binv_s[j], lcs[j].q);
-        fv += (double)y[j] * cc->rb[j];
+        y[j] = mulw(x, P.binv[j], P.binv_s[j], P.nq[j]);
+        fv += (double)y[j] * P.rb[j];
       }
     }
-    const int v = (int)rint(fv);  // |T|/B < 1/8: never near a half
-    // 2. q-part: y_j tP/q_j = y_j floor(tP/q_j) + h_j + r_j/q_j
+    const uint64_t v = (uint64_t)rint(fv);
+    // 2. q-part: y_j tP/q_j = y_j floor(tP/q_j) + h_j + r_j/q_j (exact divmod)
     uint64_t r[KQ];
-    uint64_t sh_hi = 0, sh_lo = 0;
-    double G = cc->hq;
+    uint64_t sh = 0;
+    double G = cc_hq(cc);
 #pragma unroll
     for (int j = 0; j < KQ; ++j) {
       r[j] = 0;
       if (j < k) {
         uint64_t h;
-        r[j] = shoup_divmod(y[j], cc->beta[j], cc->beta_s[j], lcs[j].q, &h);
-        add128(sh_hi, sh_lo, 0, h);
-        G += (double)r[j] * cc->rq[j];
+        r[j] = shoup_divmod(y[j], P.beta[j], P.beta_s[j], P.q[j], &h);
+        sh += h;
+        G += (double)r[j] * P.rq[j];
       }
     }
     int64_t g = (int64_t)floor(G);
@@ -433,22 +533,21 @@ __global__ void __launch_bounds__(256) rescale_kernel(const uint64_t* __restrict
       g = exact_frac_floor<NW>(r, k, cc, g);
       atomicAdd(fallbacks, 1ull);
     }
-    // 3. residues of R mod q_i
+    // 3. residues of R mod q_i: lazy sums of < 4 q_i products, one reduction
     uint64_t out[KQ];
 #pragma unroll
     for (int i = 0; i < KQ; ++i) {
       out[i] = 0;
       if (i < k) {
-        const LimbConst& c = lcs[i];
-        uint64_t acc = 0;
+        const uint64_t qi = P.q[i], nqi = P.nq[i];
+        uint64_t acc = mulw(v, P.ntp[i], P.ntp_s[i], nqi);
 #pragma unroll
-        for (int j = 0; j < KE; ++j)
-          if (j < K) acc = csub(acc + shoup_lazy(y[j], cc->rc[i][j], cc->rc_s[i][j], c.q), c.q2);
-        const uint64_t s1 = reduce128(sh_hi, sh_lo, c);
-        acc = csub(acc, c.q) + s1 + cc->rvt[i][v] + (uint64_t)g;
-        acc = csub(acc, c.q2);
-        acc = csub(acc, c.q2);
-        out[i] = csub(acc, c.q);
+        for (int j = 0; j < KE; ++j) {
+          if (j < K) acc += mulw(y[j], P.rc[i][j], P.rc_s[i][j], nqi);
+          if (j == 15) acc = mulw(acc, 1, P.one_s[i], nqi);
+        }
+        acc = reduce_any(acc, qi, P.one_s[i], nqi) + reduce_any(sh, qi, P.one_s[i], nqi) + (uint64_t)g;
+        out[i] = csub(csub(acc, qi), qi);
       }
     }
     if (p < 2) {
@@ -463,42 +562,48 @@ __global__ void __launch_bounds__(256) rescale_kernel(const uint64_t* __restrict
 #pragma unroll
       for (int i = 0; i < KQ; ++i) {
         if (i < k) {
-          const uint64_t z = shoup(out[i], cc->qinv[i], cc->qinv_s[i], lcs[i].q);
-          fu += (double)z * cc->rq[i];
+          const uint64_t z = shoup(out[i], P.qinv[i], P.qinv_s[i], P.q[i]);
+          fu += (double)z * P.rq[i];
           mw_mac<NW>(a, cc->Qw[i], cc->qwords, z);
         }
       }
       mw_reduce_q<NW>(a, cc, (int64_t)floor(fu));
-      const int D = cc->D, w = cc->w;
-      for (int d = 0; d < D; ++d) {
-        const int bit = d * w;
-        // digit words (up to 3 for w <= 190)
-        uint64_t dw[3];
-#pragma unroll
-        for (int mword = 0; mword < 3; ++mword) {
-          const int b0 = bit + 64 * mword;
-          const int wi = b0 >> 6, bo = b0 & 63;
+      const int D = P.D, w = P.w;
+      if (P.direct) {
+        // every digit < 2^w <= min q_i: one row per digit, broadcast to the limbs by the NTT
+        const uint64_t mask = (w >= 64) ? ~0ull : ((1ull << w) - 1);
+        for (int d = 0; d < D; ++d) {
+          const int bit = d * w;
+          const int wi = bit >> 6, bo = bit & 63;
           uint64_t lo = mw_word<NW>(a, wi) >> bo;
           if (bo) lo |= mw_word<NW>(a, wi + 1) << (64 - bo);
-          const int rem = w - 64 * mword;  // bits of the digit at or above this word
-          if (rem <= 0) lo = 0;
-          else if (rem < 64) lo &= (1ull << rem) - 1;
-          dw[mword] = lo;
+          DG[(ct * D + d) * n + coef] = lo & mask;
         }
+      } else {
+        for (int d = 0; d < D; ++d) {
+          const int bit = d * w;
+          uint64_t dw[3];
 #pragma unroll
-        for (int l = 0; l < KQ; ++l) {
-          if (l < k) {
-            const LimbConst& c = lcs[l];
-            uint64_t val;
-            if (cc->direct) {
-              val = dw[0];
-            } else {
-              val = csub(shoup_lazy(dw[0], 1, c.one_s, c.q), c.q);
-              if (cc->dwords > 1) val += csub(shoup_lazy(dw[1], cc->dpw[l][1], cc->dpw_s[l][1], c.q), c.q);
-              if (cc->dwords > 2) val += csub(shoup_lazy(dw[2], cc->dpw[l][2], cc->dpw_s[l][2], c.q), c.q);
-              val = csub(csub(val, c.q2), c.q);
+          for (int mword = 0; mword < 3; ++mword) {
+            const int b0 = bit + 64 * mword;
+            const int wi = b0 >> 6, bo = b0 & 63;
+            uint64_t lo = mw_word<NW>(a, wi) >> bo;
+            if (bo) lo |= mw_word<NW>(a, wi + 1) << (64 - bo);
+            const int rem = w - 64 * mword;
+            if (rem <= 0) lo = 0;
+            else if (rem < 64) lo &= (1ull << rem) - 1;
+            dw[mword] = lo;
+          }
+#pragma unroll
+          for (int l = 0; l < KQ; ++l) {
+            if (l < k) {
+              const uint64_t ql = P.q[l];
+              uint64_t val = csub(shoup_lazy(dw[0], 1, P.one_s[l], ql), ql);
+              if (P.dwords > 1) val += csub(shoup_lazy(dw[1], P.dpw[l][1], P.dpw_s[l][1], ql), ql);
+              if (P.dwords > 2) val += csub(shoup_lazy(dw[2], P.dpw[l][2], P.dpw_s[l][2], ql), ql);
+              val = csub(csub(val, 2 * ql), ql);
+              DG[((ct * D + d) * k + l) * n + coef] = val;
             }
-            DG[((ct * D + d) * k + l) * n + coef] = val;
           }
         }
       }
@@ -507,34 +612,56 @@ __global__ void __launch_bounds__(256) rescale_kernel(const uint64_t* __restrict
 }
 
 // Key switching MAC in the NTT domain (fv.py:533-537):
-// acc0 = sum_d g_d * D_d, acc1 = sum_d a_d * D_d.
-__global__ void keymac_kernel(const uint64_t* __restrict__ DG, const uint64_t* __restrict__ kg,
-                              const uint64_t* __restrict__ ka, uint64_t* __restrict__ ACC, int64_t C, int D, int k,
-                              int logn, const LimbConst* __restrict__ lcs) {
+// acc0 = sum_d g_d * D_d, acc1 = sum_d a_d * D_d.  A thread owns two
+// consecutive residues of one limb and walks a range of ciphertexts, so its
+// key words are loaded once; 16-byte loads keep more bytes in flight.
+template <int DMAX>
+__global__ void __launch_bounds__(256) keymac_kernel(const uint64_t* __restrict__ DG, const uint64_t* __restrict__ kg,
+                                                     const uint64_t* __restrict__ ka, uint64_t* __restrict__ ACC, int64_t C,
+                                                     int D, int k, int logn, const LimbConst* __restrict__ lcs) {
   const int n = 1 << logn;
-  const int64_t total = (C * k) << logn;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t rowi = e >> logn;
-    const int coef = (int)(e & (n - 1));
-    const int64_t ct = rowi / k;
-    const int l = (int)(rowi % k);
-    const LimbConst c = lcs[l];
-    uint64_t gh = 0, gl = 0, ah = 0, al = 0;
-    for (int d = 0; d < D; ++d) {
-      const uint64_t x = DG[((ct * D + d) * k + l) * n + coef];
-      const int64_t ki = ((int64_t)d * k + l) * n + coef;
-      const uint64_t g = kg[ki], a = ka[ki];
-      add128(gh, gl, __umul64hi(x, g), x * g);
-      add128(ah, al, __umul64hi(x, a), x * a);
-      if ((d & 7) == 7) {
-        gl = reduce128(gh, gl, c);
-        gh = 0;
-        al = reduce128(ah, al, c);
-        ah = 0;
+  const int64_t lc = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;  // l * n + coef (even)
+  if (lc >= (int64_t)k * n) return;
+  const int l = (int)(lc >> logn);
+  const int coef = (int)(lc & (n - 1));
+  const LimbConst c = lcs[l];
+  ulonglong2 gk[DMAX], ak[DMAX];
+#pragma unroll
+  for (int d = 0; d < DMAX; ++d) {
+    if (d < D) {
+      gk[d] = *reinterpret_cast<const ulonglong2*>(kg + ((int64_t)d * k + l) * n + coef);
+      ak[d] = *reinterpret_cast<const ulonglong2*>(ka + ((int64_t)d * k + l) * n + coef);
+    }
+  }
+  const int64_t per = (C + gridDim.y - 1) / gridDim.y;
+  const int64_t c0 = (int64_t)blockIdx.y * per;
+  const int64_t c1 = c0 + per < C ? c0 + per : C;
+  for (int64_t ct = c0; ct < c1; ++ct) {
+    uint64_t gh0 = 0, gl0 = 0, ah0 = 0, al0 = 0, gh1 = 0, gl1 = 0, ah1 = 0, al1 = 0;
+#pragma unroll
+    for (int d = 0; d < DMAX; ++d) {
+      if (d < D) {
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(DG + ((ct * D + d) * k + l) * n + coef);
+        add128(gh0, gl0, __umul64hi(x.x, gk[d].x), x.x * gk[d].x);
+        add128(ah0, al0, __umul64hi(x.x, ak[d].x), x.x * ak[d].x);
+        add128(gh1, gl1, __umul64hi(x.y, gk[d].y), x.y * gk[d].y);
+        add128(ah1, al1, __umul64hi(x.y, ak[d].y), x.y * ak[d].y);
+        if ((d & 7) == 7) {
+          gl0 = reduce128(gh0, gl0, c);
+          gh0 = 0;
+          al0 = reduce128(ah0, al0, c);
+          ah0 = 0;
+          gl1 = reduce128(gh1, gl1, c);
+          gh1 = 0;
+          al1 = reduce128(ah1, al1, c);
+          ah1 = 0;
+        }
       }
     }
-    ACC[((ct * 2 + 0) * k + l) * n + coef] = reduce128(gh, gl, c);
-    ACC[((ct * 2 + 1) * k + l) * n + coef] = reduce128(ah, al, c);
+    *reinterpret_cast<ulonglong2*>(ACC + ((ct * 2 + 0) * k + l) * n + coef) =
+        make_ulonglong2(reduce128(gh0, gl0, c), reduce128(gh1, gl1, c));
+    *reinterpret_cast<ulonglong2*>(ACC + ((ct * 2 + 1) * k + l) * n + coef) =
+        make_ulonglong2(reduce128(ah0, al0, c), reduce128(ah1, al1, c));
   }
 }
 
@@ -693,14 +820,6 @@ static int build_mulct_const(const fcn_ctx* x, uint64_t t, MulCtConst* mc) {
   return FCN_OK;
 }
 
-// kernel variant dispatch: (max q limbs, max aux limbs)
-enum Variant { V4_5 = 0, V8_8, V16_16 };
-static Variant pick_variant(int k, int m) {
-  if (k <= 4 && m <= 5) return V4_5;
-  if (k <= 8 && m <= 8) return V8_8;
-  return V16_16;
-}
-
 }  // namespace fcn
 
 using namespace fcn;
@@ -776,6 +895,7 @@ extern "C" int fcn_ctx_create(int device, int n, int k, const uint64_t* primes, 
       return rc;
     }
   }
+  x->host_mc = host;
   DeviceGuard g(device);
   cudaError_t e = cudaMalloc(&x->d_mc, sizeof(MulCtConst) * n_lanes);
   if (e == cudaSuccess) e = cudaMemcpy(x->d_mc, host.data(), sizeof(MulCtConst) * n_lanes, cudaMemcpyHostToDevice);
@@ -894,6 +1014,13 @@ extern "C" int fcn_add_plain_terms(const fcn_ctx* x, int lane, uint64_t* d_cts, 
 extern "C" int fcn_linear_mac(const fcn_ctx* x, const uint64_t* d_in0, int64_t n_in0, const uint64_t* d_in1, int64_t n_in1,
                               const int32_t* d_rowptr, const int32_t* d_col, const int32_t* d_rot, const int64_t* d_coef,
                               uint64_t* d_out, int64_t n_out, void* stream) {
+  return fcn_linear_mac_ex(x, d_in0, n_in0, d_in1, n_in1, d_rowptr, d_col, d_rot, d_coef, d_out, n_out, 0, 0, stream);
+}
+
+extern "C" int fcn_linear_mac_ex(const fcn_ctx* x, const uint64_t* d_in0, int64_t n_in0, const uint64_t* d_in1,
+                                 int64_t n_in1, const int32_t* d_rowptr, const int32_t* d_col, const int32_t* d_rot,
+                                 const int64_t* d_coef, uint64_t* d_out, int64_t n_out, int no_rot, uint64_t max_abs_coef,
+                                 void* stream) {
   if (!x) return set_error(FCN_ERR_ARG, "null context");
   if (n_out <= 0) return FCN_OK;
   if (!d_out || !d_rowptr || (n_in0 > 0 && !d_in0) || (n_in1 > 0 && !d_in1))
@@ -901,6 +1028,24 @@ extern "C" int fcn_linear_mac(const fcn_ctx* x, const uint64_t* d_in0, int64_t n
   if (n_out > 65535) return set_error(FCN_ERR_ARG, "at most 65535 outputs per launch");
   DeviceGuard g(x->device);
   const int threads = 256;
+  // lazy 64-bit accumulation: fold * max|c| * q_max + 4 q_max < 2^64
+  uint64_t qmax = 0;
+  for (uint64_t q : x->primes) qmax = q > qmax ? q : qmax;
+  int fold = 0;
+  if (no_rot && max_abs_coef > 0 && max_abs_coef < (1ull << 32)) {
+    const unsigned __int128 room = ((unsigned __int128)1 << 64) - 4 * (unsigned __int128)qmax;
+    const unsigned __int128 per = (unsigned __int128)qmax * max_abs_coef;
+    const unsigned __int128 f = room / per;
+    fold = f > 1024 ? 1024 : (int)f;
+  }
+  if (fold >= 2 && x->n >= 4) {
+    const int per_cta = threads * 4;
+    dim3 grid((x->n + per_cta - 1) / per_cta, (unsigned)n_out, 2 * x->k);
+    mac_fast_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_coef, d_out,
+                                                               x->logn, x->k, x->ext->d_lc, fold);
+    FCN_LAUNCH_CHECK("mac_fast_kernel");
+    return FCN_OK;
+  }
   const int per_cta = threads * 2;
   dim3 grid((x->n + per_cta - 1) / per_cta, (unsigned)n_out, 2 * x->k);
   mac_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_rot, d_coef, d_out, x->logn,
@@ -909,10 +1054,11 @@ extern "C" int fcn_linear_mac(const fcn_ctx* x, const uint64_t* d_in0, int64_t n
   return FCN_OK;
 }
 
-// workspace per ciphertext in words
+// workspace per ciphertext in words: EA, EB (2K each), T (3K), R01 (2k),
+// DGN (D k), ACC (2k), raw digit rows (D)
 static int64_t mulct_words_per_ct(const fcn_ctx* x) {
   const int64_t K = x->k + x->m, k = x->k, D = x->ell + 1;
-  return (2 * K + 2 * K + 3 * K + 2 * k + D * k + 2 * k) * (int64_t)x->n;
+  return (2 * K + 2 * K + 3 * K + 2 * k + D * k + 2 * k + D) * (int64_t)x->n;
 }
 
 extern "C" size_t fcn_mul_ct_workspace_bytes(const fcn_ctx* x, int64_t chunk) {
@@ -921,19 +1067,128 @@ extern "C" size_t fcn_mul_ct_workspace_bytes(const fcn_ctx* x, int64_t chunk) {
 }
 
 template <int KQ, int KA>
-static void launch_lift(const uint64_t* in, uint64_t* ext, int64_t npoly, const fcn_ctx* x, const MulCtConst* mc,
-                        cudaStream_t st) {
-  const int64_t total = npoly << x->logn;
-  lift_kernel<KQ, KA, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, ext, npoly, x->logn, mc, x->ext->d_lc,
-                                                                     x->d_fallbacks);
+static LiftP<KQ, KA> make_lift_params(const fcn_ctx* x, const MulCtConst& mc) {
+  LiftP<KQ, KA> P;
+  memset(&P, 0, sizeof(P));
+  P.k = x->k;
+  P.m = x->m;
+  P.K = x->k + x->m;
+  const Big q = big_prod(x->primes);
+  for (int i = 0; i < x->k; ++i) {
+    P.q[i] = x->primes[i];
+    P.nq[i] = (uint64_t)0 - x->primes[i];
+    P.qinv[i] = mc.qinv[i];
+    P.qinv_s[i] = mc.qinv_s[i];
+    P.rq[i] = mc.rq[i];
+  }
+  for (int j = 0; j < x->m; ++j) {
+    const uint64_t pj = x->aux[j];
+    P.p[j] = pj;
+    P.np[j] = (uint64_t)0 - pj;
+    P.p_one_s[j] = h_shoup(1, pj);
+    for (int i = 0; i < x->k; ++i) {
+      P.lc[j][i] = mc.lc[j][i];
+      P.lc_s[j][i] = mc.lc_s[j][i];
+    }
+    const uint64_t qp = q.mod_small(pj);
+    P.nqp[j] = (pj - qp) % pj;
+    P.nqp_s[j] = h_shoup(P.nqp[j], pj);
+  }
+  return P;
 }
 
 template <int KQ, int KE>
-static void launch_rescale(const uint64_t* T, uint64_t* R01, uint64_t* DG, int64_t C, const fcn_ctx* x,
-                           const MulCtConst* mc, cudaStream_t st) {
-  const int64_t total = (C * 3) << x->logn;
-  rescale_kernel<KQ, KE, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(T, R01, DG, C, x->logn, mc, x->ext->d_lc,
-                                                                        x->d_fallbacks);
+static RescaleP<KQ, KE> make_rescale_params(const fcn_ctx* x, const MulCtConst& mc) {
+  RescaleP<KQ, KE> P;
+  memset(&P, 0, sizeof(P));
+  const int k = x->k, K = x->k + x->m;
+  P.k = k;
+  P.K = K;
+  P.D = mc.D;
+  P.w = mc.w;
+  P.direct = mc.direct;
+  P.dwords = mc.dwords;
+  for (int j = 0; j < K; ++j) {
+    P.q[j] = j < k ? x->primes[j] : x->aux[j - k];
+    P.nq[j] = (uint64_t)0 - P.q[j];
+    P.binv[j] = mc.binv[j];
+    P.binv_s[j] = mc.binv_s[j];
+    P.rb[j] = mc.rb[j];
+  }
+  for (int i = 0; i < k; ++i) {
+    const uint64_t qi = x->primes[i];
+    P.one_s[i] = h_shoup(1, qi);
+    P.rq[i] = mc.rq[i];
+    P.beta[i] = mc.beta[i];
+    P.beta_s[i] = mc.beta_s[i];
+    P.qinv[i] = mc.qinv[i];
+    P.qinv_s[i] = mc.qinv_s[i];
+    for (int j = 0; j < K; ++j) {
+      P.rc[i][j] = mc.rc[i][j];
+      P.rc_s[i][j] = mc.rc_s[i][j];
+    }
+    P.ntp[i] = mc.rvt[i][1];  // (-tP) mod q_i
+    P.ntp_s[i] = h_shoup(P.ntp[i], qi);
+    for (int mm = 0; mm < 3; ++mm) {
+      P.dpw[i][mm] = mc.dpw[i][mm];
+      P.dpw_s[i][mm] = mc.dpw_s[i][mm];
+    }
+  }
+  return P;
+}
+
+template <int KQ, int KE>
+static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t* in, uint64_t* out, int64_t cnt,
+                            uint64_t* R01, uint64_t* DG, cudaStream_t st) {
+  const MulCtConst& mc = x->host_mc[lane];
+  const MulCtConst* dmc = x->d_mc + lane;
+  if (lift) {
+    const LiftP<KQ, KE - KQ> P = make_lift_params<KQ, KE - KQ>(x, mc);
+    const int64_t total = cnt << x->logn;  // cnt = polys
+    lift_kernel<KQ, KE - KQ, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, out, cnt, x->logn, P, dmc, x->d_fallbacks);
+    FCN_LAUNCH_CHECK("lift_kernel");
+  } else {
+    const RescaleP<KQ, KE> P = make_rescale_params<KQ, KE>(x, mc);
+    const int64_t total = (cnt * 3) << x->logn;  // cnt = ciphertexts
+    rescale_kernel<KQ, KE, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, R01, DG, cnt, x->logn, P, dmc, x->d_fallbacks);
+    FCN_LAUNCH_CHECK("rescale_kernel");
+  }
+  return FCN_OK;
+}
+
+static int lift_or_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t* in, uint64_t* out, int64_t cnt,
+                           uint64_t* R01, uint64_t* DG, cudaStream_t st) {
+  const int k = x->k, m = x->m;
+#define FCN_TRY(KQ, KE) \
+  if (k <= KQ && m <= KE - KQ) return run_lift_rescale<KQ, KE>(lift, x, lane, in, out, cnt, R01, DG, st);
+  FCN_TRY(2, 6)
+  FCN_TRY(3, 6)
+  FCN_TRY(4, 9)
+  FCN_TRY(6, 12)
+  FCN_TRY(8, 16)
+  FCN_TRY(16, 32)
+#undef FCN_TRY
+  return set_error(FCN_ERR_PARAM, "unsupported limb counts k=%d m=%d", k, m);
+}
+
+static int launch_keymac(const uint64_t* DG, const fcn_keys* keys, uint64_t* ACC, int64_t C, int D, int k, const fcn_ctx* x,
+                         cudaStream_t st) {
+  const int64_t kn = (int64_t)k * x->n / 2;  // threads: two residues each
+  const int bx = (int)((kn + 255) / 256);
+  int64_t split = (148LL * 2048 * 2 + kn - 1) / kn;
+  if (split > C) split = C;
+  if (split < 1) split = 1;
+  dim3 grid(bx, (unsigned)split);
+  if (D <= 4)
+    keymac_kernel<4><<<grid, 256, 0, st>>>(DG, keys->d_g, keys->d_a, ACC, C, D, k, x->logn, x->ext->d_lc);
+  else if (D <= 8)
+    keymac_kernel<8><<<grid, 256, 0, st>>>(DG, keys->d_g, keys->d_a, ACC, C, D, k, x->logn, x->ext->d_lc);
+  else if (D <= 16)
+    keymac_kernel<16><<<grid, 256, 0, st>>>(DG, keys->d_g, keys->d_a, ACC, C, D, k, x->logn, x->ext->d_lc);
+  else
+    keymac_kernel<32><<<grid, 256, 0, st>>>(DG, keys->d_g, keys->d_a, ACC, C, D, k, x->logn, x->ext->d_lc);
+  FCN_LAUNCH_CHECK("keymac_kernel");
+  return FCN_OK;
 }
 
 extern "C" int fcn_mul_ct(const fcn_ctx* x, const fcn_keys* keys, int lane, const uint64_t* d_a, const uint64_t* d_b,
@@ -941,6 +1196,7 @@ extern "C" int fcn_mul_ct(const fcn_ctx* x, const fcn_keys* keys, int lane, cons
   if (!x || !keys) return set_error(FCN_ERR_ARG, "null context or keys");
   if (lane < 0 || lane >= x->n_lanes) return set_error(FCN_ERR_ARG, "lane %d out of range", lane);
   if (count <= 0) return FCN_OK;
+  if (x->ell + 1 > 32) return set_error(FCN_ERR_PARAM, "more than 32 decomposition digits");
   if (!d_a || !d_out || !d_workspace) return set_error(FCN_ERR_ARG, "null buffer");
   if (keys->k != x->k || keys->n != x->n || keys->D != x->ell + 1) return set_error(FCN_ERR_ARG, "keys do not match context");
   const int64_t per = mulct_words_per_ct(x);
@@ -949,8 +1205,7 @@ extern "C" int fcn_mul_ct(const fcn_ctx* x, const fcn_keys* keys, int lane, cons
   DeviceGuard gd(x->device);
   cudaStream_t st = (cudaStream_t)stream;
   const int k = x->k, K = x->k + x->m, D = x->ell + 1, n = x->n, logn = x->logn;
-  const MulCtConst* mc = x->d_mc + lane;
-  const Variant var = pick_variant(k, x->m);
+  const bool direct = x->host_mc[lane].direct != 0;
   const int64_t ct_words = 2LL * k * n;
   for (int64_t off = 0; off < count; off += chunk_max) {
     const int64_t C = (count - off) < chunk_max ? (count - off) : chunk_max;
@@ -959,21 +1214,17 @@ extern "C" int fcn_mul_ct(const fcn_ctx* x, const fcn_keys* keys, int lane, cons
     uint64_t* EB = EA + C * 2 * K * n;
     uint64_t* T = EB + C * 2 * K * n;
     uint64_t* R01 = T + C * 3 * K * n;
-    uint64_t* DG = R01 + C * 2 * k * n;
-    uint64_t* ACC = DG + C * D * k * n;
+    uint64_t* DGN = R01 + C * 2 * k * n;
+    uint64_t* ACC = DGN + C * D * k * n;
+    uint64_t* DGR = ACC + C * 2 * k * n;
     const uint64_t* a = d_a + off * ct_words;
     const uint64_t* b = d_b ? d_b + off * ct_words : nullptr;
     // (i) lift + forward NTT over the extended base
     for (int which = 0; which < (b ? 2 : 1); ++which) {
-      const uint64_t* src = which ? b : a;
       uint64_t* dst = which ? EB : EA;
-      switch (var) {
-        case V4_5: launch_lift<4, 5>(src, dst, C * 2, x, mc, st); break;
-        case V8_8: launch_lift<8, 8>(src, dst, C * 2, x, mc, st); break;
-        default: launch_lift<16, 16>(src, dst, C * 2, x, mc, st); break;
-      }
-      FCN_LAUNCH_CHECK("lift_kernel");
-      int rc = launch_ntt(x->ext, dst, C * 2 * K, K, 0, true, st);
+      int rc = lift_or_rescale(true, x, lane, which ? b : a, dst, C * 2, nullptr, nullptr, st);
+      if (rc) return rc;
+      rc = launch_ntt(x->ext, dst, C * 2 * K, K, 0, true, st);
       if (rc) return rc;
     }
     // (ii) tensor, (iii) inverse NTT
@@ -982,17 +1233,17 @@ extern "C" int fcn_mul_ct(const fcn_ctx* x, const fcn_keys* keys, int lane, cons
     int rc = launch_ntt(x->ext, T, C * 3 * K, K, 0, false, st);
     if (rc) return rc;
     // (iv) exact rescale + digit decomposition
-    switch (var) {
-      case V4_5: launch_rescale<4, 9>(T, R01, DG, C, x, mc, st); break;
-      case V8_8: launch_rescale<8, 16>(T, R01, DG, C, x, mc, st); break;
-      default: launch_rescale<16, 32>(T, R01, DG, C, x, mc, st); break;
-    }
-    FCN_LAUNCH_CHECK("rescale_kernel");
-    // (v) digits to NTT, key MAC, (vi) inverse NTT + add
-    rc = launch_ntt(x->ext, DG, C * D * k, k, 0, true, st);
+    rc = lift_or_rescale(false, x, lane, T, nullptr, C, R01, direct ? DGR : DGN, st);
     if (rc) return rc;
-    keymac_kernel<<<grid_for((C * k) << logn, 256), 256, 0, st>>>(DG, keys->d_g, keys->d_a, ACC, C, D, k, logn, x->ext->d_lc);
-    FCN_LAUNCH_CHECK("keymac_kernel");
+    // (v) digits to NTT (broadcast rows when digits are limb-independent), key MAC
+    if (direct)
+      rc = launch_ntt(x->ext, DGN, C * D * k, k, 0, true, st, DGR, k);
+    else
+      rc = launch_ntt(x->ext, DGN, C * D * k, k, 0, true, st);
+    if (rc) return rc;
+    rc = launch_keymac(DGN, keys, ACC, C, D, k, x, st);
+    if (rc) return rc;
+    // (vi) inverse NTT + add
     rc = launch_ntt(x->ext, ACC, C * 2 * k, k, 0, false, st);
     if (rc) return rc;
     const int64_t tot = (C * 2 * k) << logn;

@@ -138,7 +138,8 @@ __device__ __forceinline__ int v1_pass_size(int logs, int p, int np) {
 template <bool FWD>
 __global__ void __launch_bounds__(512) ntt_v1_kernel(uint64_t* __restrict__ data, int64_t n_segs, int logs, int logn,
                                                      int period, int offset, const LimbConst* __restrict__ lcs,
-                                                     const Twiddle* __restrict__ tws) {
+                                                     const Twiddle* __restrict__ tws, const uint64_t* __restrict__ src,
+                                                     int src_div) {
   extern __shared__ uint64_t sm[];
   const int S = 1 << logs;
   const int nseg = 1 << (logn - logs);
@@ -150,8 +151,9 @@ __global__ void __launch_bounds__(512) ntt_v1_kernel(uint64_t* __restrict__ data
     const LimbConst c = lcs[limb];
     const Twiddle* tw = tws + (int64_t)limb * n;
     uint64_t* p = data + row * (int64_t)n + (int64_t)part * S;
+    const uint64_t* ps = src + (row / src_div) * (int64_t)n + (int64_t)part * S;
     for (int i = threadIdx.x; i < S / 2; i += blockDim.x) {
-      ulonglong2 v = reinterpret_cast<const ulonglong2*>(p)[i];
+      ulonglong2 v = reinterpret_cast<const ulonglong2*>(ps)[i];
       sm[phys(2 * i)] = v.x;
       sm[phys(2 * i + 1)] = v.y;
     }
@@ -244,42 +246,6 @@ __device__ __forceinline__ Twiddle ld_tw(const Twiddle* p) {
 #endif
 }
 
-// a*w mod q in [0, 4q) for any a < 2^64, constant w < q with ws = floor(w 2^64/q),
-// nq = 2^64 - q.  The quotient estimate h = a1 s1 + hi(a1 s0) + hi(a0 s1) omits
-// a0*s0 and the low halves of the cross products, so it undershoots
-// floor(a ws / 2^64) by at most 2 (remainder < 2q + 2q).  9 IMAD-pipe ops.
-__device__ __forceinline__ uint64_t mulw(uint64_t a, uint64_t w, uint64_t ws, uint64_t nq) {
-#ifdef FCN_EXP_NO_MUL
-  return (a ^ w) + ws;
-#endif
-  uint64_t r;
-  asm("{\n\t"
-      ".reg .u32 a0, a1, w0, w1, s0, s1, n0, n1, hl, hh, rl, rh;\n\t"
-      ".reg .u64 H, R;\n\t"
-      "mov.b64 {a0, a1}, %1;\n\t"
-      "mov.b64 {w0, w1}, %2;\n\t"
-      "mov.b64 {s0, s1}, %3;\n\t"
-      "mov.b64 {n0, n1}, %4;\n\t"
-      "mul.wide.u32 H, a1, s1;\n\t"
-      "mov.b64 {hl, hh}, H;\n\t"
-      "mad.hi.cc.u32 hl, a1, s0, hl;\n\t"
-      "addc.u32 hh, hh, 0;\n\t"
-      "mad.hi.cc.u32 hl, a0, s1, hl;\n\t"
-      "addc.u32 hh, hh, 0;\n\t"
-      "mul.wide.u32 R, a0, w0;\n\t"
-      "mad.wide.u32 R, hl, n0, R;\n\t"
-      "mov.b64 {rl, rh}, R;\n\t"
-      "mad.lo.u32 rh, a0, w1, rh;\n\t"
-      "mad.lo.u32 rh, a1, w0, rh;\n\t"
-      "mad.lo.u32 rh, hl, n1, rh;\n\t"
-      "mad.lo.u32 rh, hh, n0, rh;\n\t"
-      "mov.b64 %0, {rl, rh};\n\t"
-      "}"
-      : "=l"(r)
-      : "l"(a), "l"(w), "l"(ws), "l"(nq));
-  return r;
-}
-
 // Cooley-Tukey butterfly without reduction: X' = X + wY, Y' = X - wY + 4q.
 // Bounds grow by 4q per stage (inputs < q): after <= 14 stages every value
 // is < 57q < 2^62 for q < 2^56.
@@ -288,14 +254,6 @@ __device__ __forceinline__ void bfly(uint64_t& X, uint64_t& Y, const Twiddle& w,
   const uint64_t x = X;
   X = x + t;
   Y = x + q4 - t;
-}
-
-// x mod q for x < 2^62, 2^34 <= q < 2^56: quotient from the high word
-// (m32 = floor(2^64/q)) undershoots by at most 1.
-__device__ __forceinline__ uint64_t reduce_small(uint64_t x, uint32_t m32, uint64_t q) {
-  const uint32_t qe = __umulhi((uint32_t)(x >> 32), m32);
-  const uint64_t r = x - (uint64_t)qe * q;
-  return r >= q ? r - q : r;
 }
 
 // Forward (natural in, bit-reversed out; reference ring.py:199-217): R
@@ -376,7 +334,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <int LOGN>
 __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     ntt_v2_fwd(uint64_t* __restrict__ data, int64_t n_rows, int period, int offset, const LimbConst* __restrict__ lcs,
-               const Twiddle* __restrict__ tws, const Twiddle* __restrict__ twl) {
+               const Twiddle* __restrict__ tws, const Twiddle* __restrict__ twl, const uint64_t* __restrict__ src,
+               int src_div) {
   constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
   extern __shared__ uint64_t sm[];
   const int tid = threadIdx.x;
@@ -384,7 +343,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
   if (row >= n_rows) return;
   uint64_t x[32];
   {
-    const uint64_t* p = data + row * N;
+    const uint64_t* p = src + (row / src_div) * N;
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = p[tid + j * T];
   }
@@ -429,7 +388,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     // prefetch the next row's pass-1 operands, then copy this row out (coalesced)
     const int64_t nxt = row + gridDim.x;
     if (nxt < n_rows) {
-      const uint64_t* p = data + nxt * N;
+      const uint64_t* p = src + (nxt / src_div) * N;
 #pragma unroll
       for (int j = 0; j < 32; ++j) x[j] = p[tid + j * T];
     }
@@ -571,7 +530,8 @@ static void init_tables() {
   if (e2 != cudaSuccess) g_init_err = e2;
 }
 
-static int launch_v1(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st) {
+static int launch_v1(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st,
+                     const uint64_t* src, int src_div) {
   const int logn = r->logn;
   const int logs = logn < 14 ? logn : 14;
   const int64_t segs = n_rows << (logn - logs);
@@ -583,13 +543,23 @@ static int launch_v1(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period,
   if (grid > cap) grid = cap;
   if (fwd) {
     if (logs < logn) {
+      if (src != d) {
+        // materialise the broadcast source rows, then transform in place
+        for (int64_t rr = 0; rr < n_rows; ++rr) {
+          cudaError_t e = cudaMemcpyAsync(d + rr * ((int64_t)1 << logn), src + (rr / src_div) * ((int64_t)1 << logn),
+                                          sizeof(uint64_t) << logn, cudaMemcpyDeviceToDevice, st);
+          if (e != cudaSuccess) return check_cuda(e, "ntt src copy");
+        }
+        src = d;
+        src_div = 1;
+      }
       ntt_v1_fwd_stage0<<<grid_for(n_rows << (logn - 1), 256), 256, 0, st>>>(d, n_rows, logn, period, offset, r->d_lc, r->d_fwd);
       FCN_LAUNCH_CHECK("ntt_v1_fwd_stage0");
     }
-    ntt_v1_kernel<true><<<(int)grid, threads, smem, st>>>(d, segs, logs, logn, period, offset, r->d_lc, r->d_fwd);
+    ntt_v1_kernel<true><<<(int)grid, threads, smem, st>>>(d, segs, logs, logn, period, offset, r->d_lc, r->d_fwd, src, src_div);
     FCN_LAUNCH_CHECK("ntt_v1_kernel<fwd>");
   } else {
-    ntt_v1_kernel<false><<<(int)grid, threads, smem, st>>>(d, segs, logs, logn, period, offset, r->d_lc, r->d_inv);
+    ntt_v1_kernel<false><<<(int)grid, threads, smem, st>>>(d, segs, logs, logn, period, offset, r->d_lc, r->d_inv, d, 1);
     FCN_LAUNCH_CHECK("ntt_v1_kernel<inv>");
     if (logs < logn) {
       ntt_v1_inv_last<<<grid_for(n_rows << (logn - 1), 256), 256, 0, st>>>(d, n_rows, logn, period, offset, r->d_lc);
@@ -601,16 +571,23 @@ static int launch_v1(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period,
 
 template <int LOGN>
 static void launch_v2_t(bool fwd, int grid, uint64_t* d, int64_t n_rows, int period, int offset, const fcn_ring* r,
-                        cudaStream_t st) {
+                        cudaStream_t st, const uint64_t* src, int src_div) {
   const size_t sm = v2_smem(LOGN);
   if (fwd)
-    ntt_v2_fwd<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fwd, r->d_fwd_last);
+    ntt_v2_fwd<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fwd, r->d_fwd_last,
+                                                         src, src_div);
   else
     ntt_v2_inv<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_ict, r->d_twist);
 }
 
-int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st) {
+int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st,
+               const uint64_t* src, int src_div) {
   if (n_rows <= 0) return FCN_OK;
+  if (!src) {
+    src = d;
+    src_div = 1;
+  }
+  if (!fwd && src != d) return set_error(FCN_ERR_ARG, "out-of-place inverse NTT is not supported");
   std::call_once(g_init, init_tables);
   if (g_init_err != cudaSuccess) return check_cuda(g_init_err, "ntt init");
   const int logn = r->logn;
@@ -619,16 +596,16 @@ int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int o
     const uint64_t q = r->primes[offset + l];
     v2 = q >= (1ull << 34) && q < (1ull << 56);
   }
-  if (!v2) return launch_v1(r, d, n_rows, period, offset, fwd, st);
+  if (!v2) return launch_v1(r, d, n_rows, period, offset, fwd, st, src, src_div);
   const V2Entry& e = g_v2[fwd ? 1 : 0][logn];
   int64_t grid = (int64_t)g_sms * e.ctas_per_sm;
   if (grid > n_rows) grid = n_rows;
   switch (logn) {
-    case 10: launch_v2_t<10>(fwd, (int)grid, d, n_rows, period, offset, r, st); break;
-    case 11: launch_v2_t<11>(fwd, (int)grid, d, n_rows, period, offset, r, st); break;
-    case 12: launch_v2_t<12>(fwd, (int)grid, d, n_rows, period, offset, r, st); break;
-    case 13: launch_v2_t<13>(fwd, (int)grid, d, n_rows, period, offset, r, st); break;
-    default: launch_v2_t<14>(fwd, (int)grid, d, n_rows, period, offset, r, st); break;
+    case 10: launch_v2_t<10>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div); break;
+    case 11: launch_v2_t<11>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div); break;
+    case 12: launch_v2_t<12>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div); break;
+    case 13: launch_v2_t<13>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div); break;
+    default: launch_v2_t<14>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div); break;
   }
   FCN_LAUNCH_CHECK(fwd ? "ntt_v2_fwd" : "ntt_v2_inv");
   return FCN_OK;

@@ -257,6 +257,8 @@ class _Mac:
     coef: object
     n_out: int
     n_terms: int
+    no_rot: bool = False
+    max_abs_coef: int = 0
 
 
 @dataclass
@@ -271,13 +273,17 @@ def _upload_mac(rowptr, col, rot, coef) -> _Mac:
     import torch
 
     d = "cuda"
+    rot_a = np.asarray(rot, dtype=np.int64)
+    coef_a = np.asarray(coef, dtype=np.int64)
     return _Mac(
         torch.as_tensor(np.asarray(rowptr, dtype=np.int32), device=d),
         torch.as_tensor(np.asarray(col, dtype=np.int32) if len(col) else np.zeros(1, np.int32), device=d),
-        torch.as_tensor(np.asarray(rot, dtype=np.int32) if len(rot) else np.zeros(1, np.int32), device=d),
-        torch.as_tensor(np.asarray(coef, dtype=np.int64) if len(coef) else np.zeros(1, np.int64), device=d),
+        torch.as_tensor(rot_a.astype(np.int32) if len(rot) else np.zeros(1, np.int32), device=d),
+        torch.as_tensor(coef_a if len(coef) else np.zeros(1, np.int64), device=d),
         len(rowptr) - 1,
         len(col),
+        bool(len(rot) == 0 or not np.any(rot_a)),
+        int(np.abs(coef_a).max()) if len(coef) else 0,
     )
 
 
@@ -461,9 +467,10 @@ def _run_mac(params, in0, in1, mac: _Mac, out):
     n_in0 = in0.shape[0]
     n_in1 = in1.shape[0] if in1 is not None else 0
     _lib.check(
-        _lib.lib().fcn_linear_mac(
+        _lib.lib().fcn_linear_mac_ex(
             h.ptr, in0.data_ptr(), n_in0, in1.data_ptr() if in1 is not None else None, n_in1, mac.rowptr.data_ptr(),
-            mac.col.data_ptr(), mac.rot.data_ptr(), mac.coef.data_ptr(), out.data_ptr(), mac.n_out, dev.stream_ptr(),
+            mac.col.data_ptr(), mac.rot.data_ptr(), mac.coef.data_ptr(), out.data_ptr(), mac.n_out,
+            int(mac.no_rot), min(mac.max_abs_coef, (1 << 64) - 1), dev.stream_ptr(),
         ),
         FVError,
     )
@@ -488,7 +495,7 @@ def _mac_out(params, mac: _Mac, in0, in1):
         if lo == 0 and hi == mac.n_out:
             _run_mac(params, in0, in1, mac, out)
         else:  # split launches over output rows (grid.y limit)
-            sub = _Mac(mac.rowptr[lo : hi + 1], mac.col, mac.rot, mac.coef, hi - lo, mac.n_terms)
+            sub = _Mac(mac.rowptr[lo : hi + 1], mac.col, mac.rot, mac.coef, hi - lo, mac.n_terms, mac.no_rot, mac.max_abs_coef)
             _run_mac(params, in0, in1, sub, out[lo:hi])
     return out
 
