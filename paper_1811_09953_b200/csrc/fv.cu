@@ -486,7 +486,7 @@ __global__ void tensor_kernel(const uint64_t* __restrict__ A, const uint64_t* __
 // base-beta digits of R (fv.py:524-533) are emitted instead: one row per
 // digit when every digit is already < q_i (P.direct), else per-limb rows.
 template <int KQ, int KE, int NW>
-__global__ void __launch_bounds__(256) rescale_kernel(const uint64_t* __restrict__ T, uint64_t* __restrict__ R01,
+__global__ void __launch_bounds__(256, (KQ <= 4 ? 3 : 2)) rescale_kernel(const uint64_t* __restrict__ T, uint64_t* __restrict__ R01,
                                                       uint64_t* __restrict__ DG, int64_t C, int logn,
                                                       const __grid_constant__ RescaleP<KQ, KE> P,
                                                       const MulCtConst* __restrict__ cc,
@@ -612,56 +612,49 @@ __global__ void __launch_bounds__(256) rescale_kernel(const uint64_t* __restrict
 }
 
 // Key switching MAC in the NTT domain (fv.py:533-537):
-// acc0 = sum_d g_d * D_d, acc1 = sum_d a_d * D_d.  A thread owns two
-// consecutive residues of one limb and walks a range of ciphertexts, so its
-// key words are loaded once; 16-byte loads keep more bytes in flight.
+// acc0 = sum_d g_d * D_d, acc1 = sum_d a_d * D_d.  A thread owns one
+// residue of one limb and walks a range of ciphertexts, so its 2D key words
+// are loaded once; the D digit loads of a ciphertext are issued together.
 template <int DMAX>
-__global__ void __launch_bounds__(256) keymac_kernel(const uint64_t* __restrict__ DG, const uint64_t* __restrict__ kg,
-                                                     const uint64_t* __restrict__ ka, uint64_t* __restrict__ ACC, int64_t C,
-                                                     int D, int k, int logn, const LimbConst* __restrict__ lcs) {
+__global__ void __launch_bounds__(256, 4) keymac_kernel(const uint64_t* __restrict__ DG, const uint64_t* __restrict__ kg,
+                                                        const uint64_t* __restrict__ ka, uint64_t* __restrict__ ACC,
+                                                        int64_t C, int D, int k, int logn,
+                                                        const LimbConst* __restrict__ lcs) {
   const int n = 1 << logn;
-  const int64_t lc = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;  // l * n + coef (even)
+  const int64_t lc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // l * n + coef
   if (lc >= (int64_t)k * n) return;
   const int l = (int)(lc >> logn);
   const int coef = (int)(lc & (n - 1));
   const LimbConst c = lcs[l];
-  ulonglong2 gk[DMAX], ak[DMAX];
+  uint64_t gk[DMAX], ak[DMAX];
 #pragma unroll
   for (int d = 0; d < DMAX; ++d) {
-    if (d < D) {
-      gk[d] = *reinterpret_cast<const ulonglong2*>(kg + ((int64_t)d * k + l) * n + coef);
-      ak[d] = *reinterpret_cast<const ulonglong2*>(ka + ((int64_t)d * k + l) * n + coef);
-    }
+    gk[d] = d < D ? kg[((int64_t)d * k + l) * n + coef] : 0;
+    ak[d] = d < D ? ka[((int64_t)d * k + l) * n + coef] : 0;
   }
   const int64_t per = (C + gridDim.y - 1) / gridDim.y;
   const int64_t c0 = (int64_t)blockIdx.y * per;
   const int64_t c1 = c0 + per < C ? c0 + per : C;
   for (int64_t ct = c0; ct < c1; ++ct) {
-    uint64_t gh0 = 0, gl0 = 0, ah0 = 0, al0 = 0, gh1 = 0, gl1 = 0, ah1 = 0, al1 = 0;
+    uint64_t xs[DMAX];
+#pragma unroll
+    for (int d = 0; d < DMAX; ++d) xs[d] = d < D ? DG[((ct * D + d) * k + l) * n + coef] : 0;
+    uint64_t gh = 0, gl = 0, ah = 0, al = 0;
 #pragma unroll
     for (int d = 0; d < DMAX; ++d) {
       if (d < D) {
-        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(DG + ((ct * D + d) * k + l) * n + coef);
-        add128(gh0, gl0, __umul64hi(x.x, gk[d].x), x.x * gk[d].x);
-        add128(ah0, al0, __umul64hi(x.x, ak[d].x), x.x * ak[d].x);
-        add128(gh1, gl1, __umul64hi(x.y, gk[d].y), x.y * gk[d].y);
-        add128(ah1, al1, __umul64hi(x.y, ak[d].y), x.y * ak[d].y);
+        add128(gh, gl, __umul64hi(xs[d], gk[d]), xs[d] * gk[d]);
+        add128(ah, al, __umul64hi(xs[d], ak[d]), xs[d] * ak[d]);
         if ((d & 7) == 7) {
-          gl0 = reduce128(gh0, gl0, c);
-          gh0 = 0;
-          al0 = reduce128(ah0, al0, c);
-          ah0 = 0;
-          gl1 = reduce128(gh1, gl1, c);
-          gh1 = 0;
-          al1 = reduce128(ah1, al1, c);
-          ah1 = 0;
+          gl = reduce128(gh, gl, c);
+          gh = 0;
+          al = reduce128(ah, al, c);
+          ah = 0;
         }
       }
     }
-    *reinterpret_cast<ulonglong2*>(ACC + ((ct * 2 + 0) * k + l) * n + coef) =
-        make_ulonglong2(reduce128(gh0, gl0, c), reduce128(gh1, gl1, c));
-    *reinterpret_cast<ulonglong2*>(ACC + ((ct * 2 + 1) * k + l) * n + coef) =
-        make_ulonglong2(reduce128(ah0, al0, c), reduce128(ah1, al1, c));
+    ACC[((ct * 2 + 0) * k + l) * n + coef] = reduce128(gh, gl, c);
+    ACC[((ct * 2 + 1) * k + l) * n + coef] = reduce128(ah, al, c);
   }
 }
 
@@ -1173,9 +1166,9 @@ static int lift_or_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t
 
 static int launch_keymac(const uint64_t* DG, const fcn_keys* keys, uint64_t* ACC, int64_t C, int D, int k, const fcn_ctx* x,
                          cudaStream_t st) {
-  const int64_t kn = (int64_t)k * x->n / 2;  // threads: two residues each
+  const int64_t kn = (int64_t)k * x->n;  // one residue per thread
   const int bx = (int)((kn + 255) / 256);
-  int64_t split = (148LL * 2048 * 2 + kn - 1) / kn;
+  int64_t split = (148LL * 1024 * 4 + kn - 1) / kn;
   if (split > C) split = C;
   if (split < 1) split = 1;
   dim3 grid(bx, (unsigned)split);

@@ -355,11 +355,11 @@ def _lower_pool(plan: PoolPlan, t: int, n: int, encoding: str):
     return _upload_mac(rowptr, col, rot, coef), None, taps
 
 
-def _lower_act(plan: ActPlan, t: int, n: int, encoding: str):
+def _lower_act(plan: ActPlan, t: int, n: int, encoding: str, nodes: int | None = None):
     """MAC over [sq ; x]: a2 * sq[o] + a1 * x[o]; bias terms for a0."""
     a2 = [(0, 1)] if plan.a2_int is None else const_terms(plan.a2_int, t, n, encoding)
     a1 = [] if plan.a1_mult_int is None else const_terms(plan.a1_mult_int, t, n, encoding)
-    N = plan.nodes
+    N = plan.nodes if nodes is None else nodes
     per = len(a2) + len(a1)
     o = np.arange(N, dtype=np.int64)
     col = np.concatenate([np.repeat(o[:, None], len(a2), 1), np.repeat(o[:, None] + N, len(a1), 1)], axis=1).ravel()
@@ -500,6 +500,87 @@ def _mac_out(params, mac: _Mac, in0, in1):
     return out
 
 
+# ------------------------------------------------------- range execution
+
+_range_cache: dict = {}
+
+
+def _bias_range(bias: _Bias | None, lo: int, hi: int, key):
+    """Bias terms of outputs [lo, hi), re-indexed from 0 (cached per range)."""
+    import torch
+
+    if bias is None:
+        return None
+    ck = ("bias", key, lo, hi)
+    hit = _range_cache.get(ck)
+    if hit is None:
+        idx = bias.ct_index.cpu().numpy()
+        sel = (idx >= lo) & (idx < hi)
+        if not sel.any():
+            hit = (None,)
+        else:
+            d = bias.ct_index.device
+            hit = (
+                _Bias(
+                    torch.as_tensor(idx[sel] - lo, dtype=torch.int32, device=d),
+                    bias.pos[torch.as_tensor(sel, device=d)].contiguous(),
+                    bias.coef[torch.as_tensor(sel, device=d)].contiguous(),
+                    int(sel.sum()),
+                ),
+            )
+        _range_cache[ck] = hit
+    return hit[0]
+
+
+def _act_lowered(plan, t, n, encoding, m):
+    ck = ("act", id(plan), t, n, encoding, m, dev.current_device())
+    hit = _range_cache.get(ck)
+    if hit is None or hit[0] is not plan:
+        hit = (plan, _lower_act(plan, t, n, encoding, nodes=m))
+        _range_cache[ck] = hit
+    return hit[1]
+
+
+def _layer_range(params, lane, ek, plan, lw, cur, lo: int, hi: int, encoding: str, mul_chunk=None):
+    """Outputs [lo, hi) of one compiled layer as a [hi-lo][2][k][n] buffer.
+
+    `cur` holds every input of the layer (for an activation, its inputs
+    are the same rows as its outputs, so cur may also be just [lo, hi))."""
+    t = int(params.t_lanes[lane])
+    kind = lw[0]
+    if kind in ("linear", "pool"):
+        mac, bias = lw[1], lw[2]
+        if lo == 0 and hi == mac.n_out:
+            out = _mac_out(params, mac, cur, None)
+            _run_bias(params, lane, out, bias)
+            return out
+        sub = _Mac(mac.rowptr[lo : hi + 1], mac.col, mac.rot, mac.coef, hi - lo, mac.n_terms, mac.no_rot, mac.max_abs_coef)
+        out = _mac_out(params, sub, cur, None)
+        _run_bias(params, lane, out, _bias_range(bias, lo, hi, id(plan)))
+        return out
+    x = cur if cur.shape[0] == hi - lo else cur[lo:hi]
+    sq = fv.mul_ct_batch(params, ek, lane, x, None, chunk=mul_chunk)
+    mac, bias, identity = _act_lowered(plan, t, params.n, encoding, hi - lo)
+    out = sq if identity else _mac_out(params, mac, sq, x)
+    _run_bias(params, lane, out, bias)
+    return out
+
+
+def _meta_step(plan, lw, depths, scales, scale, factor, prec):
+    """Per-ciphertext (depth, scale) and tensor-level (scale, factor) after a layer."""
+    kind = lw[0]
+    if kind == "linear":
+        depths, scales, nonempty = _gather_meta(lw[3], depths, scales, scale + prec)
+        scales = np.where(nonempty, scales + prec, scales)
+        return depths, scales, scale + prec, factor
+    if kind == "pool":
+        depths, scales, _ = _gather_meta(lw[3], depths, scales, scale)
+        if plan.reciprocal_int is not None:
+            return depths, scales + prec, scale + prec, factor
+        return depths, scales, scale + plan.pow2_shift, factor * plan.factor_mult
+    return depths + 1, 2 * scales + (prec if plan.a2_int is not None else 0), 2 * scale + plan.scale_bump, factor * factor
+
+
 # --------------------------------------------------------------- evaluator
 
 
@@ -563,39 +644,11 @@ def eval_encrypted(net, tensor: CipherTensor, ek: EvalKeys, cfg: FixedPointConfi
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()
-        kind = lw[0]
-        if kind == "linear":
-            _, mac, bias, taps = lw
-            depths, scales, nonempty = _gather_meta(taps, depths, scales, scale + prec)
-            scales = np.where(nonempty, scales + prec, scales)
-            nxt = _mac_out(params, mac, cur, None)
-            _run_bias(params, lane, nxt, bias)
-            scale += prec
-        elif kind == "pool":
-            _, mac, _, taps = lw
-            depths, scales, _ = _gather_meta(taps, depths, scales, scale)
-            nxt = _mac_out(params, mac, cur, None)
-            if plan.reciprocal_int is not None:
-                scales = scales + prec
-                scale += prec
-            else:
-                scale += plan.pow2_shift
-                factor *= plan.factor_mult
-        else:
-            _, mac, bias, identity = lw
-            sq = fv.mul_ct_batch(params, ek, lane, cur, None, chunk=mul_chunk)
-            if identity:
-                nxt = sq
-            else:
-                nxt = _mac_out(params, mac, sq, cur)
-            _run_bias(params, lane, nxt, bias)
-            depths = depths + 1
-            scales = 2 * scales + (prec if plan.a2_int is not None else 0)
-            scale = 2 * scale + plan.scale_bump
-            factor = factor * factor
+        n_out = lw[1].n_out if lw[0] in ("linear", "pool") else plan.nodes
+        depths, scales, scale, factor = _meta_step(plan, lw, depths, scales, scale, factor, prec)
+        cur = _layer_range(params, lane, ek, plan, lw, cur, 0, n_out, encoding, mul_chunk)
         ev1.record()
         events.append((ev0, ev1))
-        cur = nxt
     torch.cuda.current_stream().synchronize()
     for c, (a, b) in zip(counter.layer_counts, events):
         c.wall_ms = a.elapsed_time(b)

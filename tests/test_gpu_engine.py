@@ -201,3 +201,38 @@ def test_eval_errors(E):
         E.eval_encrypted(net, tensor, ek, FixedPointConfig((65537,), 4))
     with pytest.raises(E.EngineError):
         E.eval_encrypted(net, tensor, ek, cfg, encoding="nope")
+
+
+def test_sharded_evaluator_single_rank_nccl(E):
+    """dist.eval_encrypted_sharded over an NCCL group of one rank equals the
+    single-GPU evaluator byte for byte (the N>1 schedule is covered on CPU by
+    tests/test_dist_gloo.py)."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1811_09953_b200 import dist as fdist
+    from paper_1811_09953_b200 import fv
+    from paper_1811_09953_b200.encode import FixedPointConfig
+
+    P, OP, net = _small_batched_setup(E, fv)
+    cfg = FixedPointConfig((65537,), 4)
+    sk, pk, ek = fv.keygen(P, 2)
+    x = np.random.default_rng(0).integers(0, 16, (16, P.n))
+    tensor = E.encrypt_tensor_batched(pk, P, x.reshape(1, 4, 4, P.n), cfg, 0, 3)
+    want, wc = E.eval_encrypted(net, tensor, ek, cfg, encoding="batched")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        got, gc = fdist.eval_encrypted_sharded(net, tensor, ek, cfg, encoding="batched")
+    finally:
+        dist.destroy_process_group()
+    assert np.array_equal(got.host_bodies(), want.host_bodies())
+    assert list(got.depths) == list(want.depths) and list(got.scales) == list(want.scales)
+    assert gc.same_ops(wc)
