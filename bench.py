@@ -125,6 +125,32 @@ def _peaks():
     return 6650.0, "fallback"
 
 
+def _int_peak():
+    p = os.path.join(REPO, "profiles", "int_peak.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f)
+
+
+def _config(W, workload, ws, shard, hops=None, l2=None):
+    cfg = {
+        "workload": workload,
+        "n": W.n,
+        "limbs": len(W.primes),
+        "t": W.t,
+        "slots": W.slots,
+        "encoding": "batched",
+        "parallelism": f"{shard}{ws}" if ws > 1 else "single",
+    }
+    if hops is not None:
+        cfg["hops"] = {"pt_ct_mul": hops.pt_ct_mul, "ct_ct_add": hops.ct_ct_add, "ct_ct_mul": hops.ct_ct_mul,
+                       "pt_ct_add": hops.pt_ct_add}
+    if l2 is not None:
+        cfg["l2"] = l2
+    return cfg
+
+
 def _profile_traffic(name: str):
     """dram bytes per launch of a kernel from the committed ncu summary."""
     p = os.path.join(REPO, "profiles", "kernel_traffic.json")
@@ -299,7 +325,9 @@ def run_reference(args, ws, rank):
         "vs_baseline": None,
         "dtype": "u64",
         "data": "synthetic (seeded uniform ciphertexts at the workload's ring shape)",
-        "config": {"workload": args.workload, "n": W.n, "limbs": len(W.primes), "t": W.t, "slots": W.slots},
+        "config": _config(W, args.workload, ws, args.shard, tot,
+                          "inputs larger than L2 (%d MB of input ciphertexts per step)" % (784 * 2 * len(W.primes) * W.n * 8 >> 20)
+                          if args.workload in ("cfg1", "cfg2") else None),
         "cpu_baseline": {
             "value": value,
             "unit": "images/s",
@@ -399,8 +427,15 @@ def run_gpu(args, ws, rank, local):
     t_avg = (r["t_fwd_s"] + r["t_inv_s"]) / 2
     achieved = r["bytes"] / t_avg / 1e9
     tr = _profile_traffic(f"ntt_{args.workload}")
+    ip = _int_peak()
+    bfly = r["rows"] * (r["n"] // 2) * (r["n"].bit_length() - 1)
+    int_roof = None
+    if ip:
+        ach = bfly / t_avg
+        int_roof = {"achieved_mulw_per_s": ach, "peak_mulw_per_s": ip["mulw_per_s"], "frac": ach / ip["mulw_per_s"],
+                    "peak_source": "profiles/int_peak.json (measured, tools/intpeak.cu)"}
     roofline = {
-        "kernel": "ntt_smem_kernel (batched forward/inverse NTT)",
+        "kernel": "ntt_v2_fwd / ntt_v2_inv (batched negacyclic NTT, one CTA per row slot)",
         "bound": "hbm",
         "achieved": achieved,
         "peak": peak,
@@ -412,6 +447,8 @@ def run_gpu(args, ws, rank, local):
         "rows_per_launch": r["rows"],
         "ms_fwd": r["t_fwd_s"] * 1e3,
         "ms_inv": r["t_inv_s"] * 1e3,
+        "int_roofline": int_roof,
+        "note": "the NTT is integer-multiply bound on B200: one mulw per butterfly caps it near 48% of HBM at n=8192",
     }
     hops = engine.plan_hops(comp, "batched", W.t).totals
     cpu = None
@@ -436,17 +473,8 @@ def run_gpu(args, ws, rank, local):
         "vs_baseline": None,
         "dtype": "u64",
         "data": "synthetic (seeded uint8 images, one per slot; random-init pruned pow2 weights)",
-        "config": {
-            "workload": args.workload,
-            "n": W.n,
-            "limbs": len(W.primes),
-            "t": W.t,
-            "slots": W.slots,
-            "encoding": "batched",
-            "parallelism": f"{args.shard}{ws}" if ws > 1 else "single",
-            "hops": {"pt_ct_mul": hops.pt_ct_mul, "ct_ct_add": hops.ct_ct_add, "ct_ct_mul": hops.ct_ct_mul, "pt_ct_add": hops.pt_ct_add},
-            "l2": "inputs larger than L2 (%d MB of input ciphertexts per step)" % (tensor.buf.numel() * 8 >> 20),
-        },
+        "config": _config(W, args.workload, ws, args.shard, hops,
+                          "inputs larger than L2 (%d MB of input ciphertexts per step)" % (tensor.buf.numel() * 8 >> 20)),
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
         "decrypt_check": check,
