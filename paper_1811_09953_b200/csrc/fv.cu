@@ -451,33 +451,35 @@ __global__ void __launch_bounds__(256) lift_kernel(const uint64_t* __restrict__ 
 }
 
 // NTT-domain tensor: (a0 b0, a0 b1 + a1 b0, a1 b1) per ext limb (fv.py:511-515).
+// Two residues per thread (16-byte loads and stores).
 __global__ void tensor_kernel(const uint64_t* __restrict__ A, const uint64_t* __restrict__ B, uint64_t* __restrict__ T,
                               int64_t C, int K, int logn, const LimbConst* __restrict__ lcs) {
   const int n = 1 << logn;
-  const int64_t total = (C * K) << logn;
+  const int64_t total = (C * K) << (logn - 1);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t rowi = e >> logn;
-    const int coef = (int)(e & (n - 1));
+    const int64_t rowi = e >> (logn - 1);
+    const int coef = (int)(e & ((n >> 1) - 1)) * 2;
     const int64_t ct = rowi / K;
     const int j = (int)(rowi % K);
     const LimbConst c = lcs[j];
     const int64_t i0 = ((ct * 2 + 0) * K + j) * n + coef, i1 = ((ct * 2 + 1) * K + j) * n + coef;
-    const uint64_t a0 = A[i0], a1 = A[i1];
-    uint64_t t0, t1, t2;
+    const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(A + i0), a1 = *reinterpret_cast<const ulonglong2*>(A + i1);
+    ulonglong2 t0, t1, t2;
     if (B) {
-      const uint64_t b0 = B[i0], b1 = B[i1];
-      t0 = mulmod(a0, b0, c);
-      t1 = addmod(mulmod(a0, b1, c), mulmod(a1, b0, c), c.q);
-      t2 = mulmod(a1, b1, c);
+      const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(B + i0), b1 = *reinterpret_cast<const ulonglong2*>(B + i1);
+      t0 = make_ulonglong2(mulmod(a0.x, b0.x, c), mulmod(a0.y, b0.y, c));
+      t1 = make_ulonglong2(addmod(mulmod(a0.x, b1.x, c), mulmod(a1.x, b0.x, c), c.q),
+                           addmod(mulmod(a0.y, b1.y, c), mulmod(a1.y, b0.y, c), c.q));
+      t2 = make_ulonglong2(mulmod(a1.x, b1.x, c), mulmod(a1.y, b1.y, c));
     } else {
-      t0 = mulmod(a0, a0, c);
-      const uint64_t x = mulmod(a0, a1, c);
-      t1 = addmod(x, x, c.q);
-      t2 = mulmod(a1, a1, c);
+      t0 = make_ulonglong2(mulmod(a0.x, a0.x, c), mulmod(a0.y, a0.y, c));
+      const uint64_t x = mulmod(a0.x, a1.x, c), y = mulmod(a0.y, a1.y, c);
+      t1 = make_ulonglong2(addmod(x, x, c.q), addmod(y, y, c.q));
+      t2 = make_ulonglong2(mulmod(a1.x, a1.x, c), mulmod(a1.y, a1.y, c));
     }
-    T[((ct * 3 + 0) * K + j) * n + coef] = t0;
-    T[((ct * 3 + 1) * K + j) * n + coef] = t1;
-    T[((ct * 3 + 2) * K + j) * n + coef] = t2;
+    *reinterpret_cast<ulonglong2*>(T + ((ct * 3 + 0) * K + j) * n + coef) = t0;
+    *reinterpret_cast<ulonglong2*>(T + ((ct * 3 + 1) * K + j) * n + coef) = t1;
+    *reinterpret_cast<ulonglong2*>(T + ((ct * 3 + 2) * K + j) * n + coef) = t2;
   }
 }
 
@@ -660,9 +662,11 @@ __global__ void __launch_bounds__(256, 4) keymac_kernel(const uint64_t* __restri
 
 __global__ void add_rows_kernel(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, uint64_t* __restrict__ out,
                                 int64_t total, int logn, int k, const LimbConst* __restrict__ lcs) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int limb = (int)((e >> logn) % k);
-    out[e] = addmod(a[e], b[e], lcs[limb].q);
+  const int64_t pairs = total >> 1;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pairs; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t q = lcs[(int)(((e << 1) >> logn) % k)].q;
+    const ulonglong2 x = reinterpret_cast<const ulonglong2*>(a)[e], y = reinterpret_cast<const ulonglong2*>(b)[e];
+    reinterpret_cast<ulonglong2*>(out)[e] = make_ulonglong2(addmod(x.x, y.x, q), addmod(x.y, y.y, q));
   }
 }
 
@@ -1221,7 +1225,7 @@ extern "C" int fcn_mul_ct(const fcn_ctx* x, const fcn_keys* keys, int lane, cons
       if (rc) return rc;
     }
     // (ii) tensor, (iii) inverse NTT
-    tensor_kernel<<<grid_for((C * K) << logn, 256), 256, 0, st>>>(EA, b ? EB : nullptr, T, C, K, logn, x->ext->d_lc);
+    tensor_kernel<<<grid_for((C * K) << (logn - 1), 256), 256, 0, st>>>(EA, b ? EB : nullptr, T, C, K, logn, x->ext->d_lc);
     FCN_LAUNCH_CHECK("tensor_kernel");
     int rc = launch_ntt(x->ext, T, C * 3 * K, K, 0, false, st);
     if (rc) return rc;
@@ -1240,7 +1244,7 @@ extern "C" int fcn_mul_ct(const fcn_ctx* x, const fcn_keys* keys, int lane, cons
     rc = launch_ntt(x->ext, ACC, C * 2 * k, k, 0, false, st);
     if (rc) return rc;
     const int64_t tot = (C * 2 * k) << logn;
-    add_rows_kernel<<<grid_for(tot, 256), 256, 0, st>>>(R01, ACC, d_out + off * ct_words, tot, logn, k, x->ext->d_lc);
+    add_rows_kernel<<<grid_for(tot / 2, 256), 256, 0, st>>>(R01, ACC, d_out + off * ct_words, tot, logn, k, x->ext->d_lc);
     FCN_LAUNCH_CHECK("add_rows_kernel");
   }
   return FCN_OK;

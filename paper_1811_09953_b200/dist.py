@@ -134,11 +134,11 @@ def eval_encrypted_sharded(net, tensor, ek, cfg, encoding: str = "integer", grou
         return out
 
     out = run_stages(plans, tensor.buf, rank, world, compute, lambda loc, c, b: _torch_gather(loc, c, b, group))
-    torch.cuda.current_stream().synchronize()
+    from .netplan import TimedLayerCounts
+
     for st, a, b in events:
-        ms = a.elapsed_time(b)
         for idx in st:
-            counter.layer_counts[idx].wall_ms += ms / len(st)
+            counter.layer_counts[idx] = TimedLayerCounts(counter.layer_counts[idx], (a, b, 1.0 / len(st)))
     res = engine.CipherTensor(compiled.out_shape, scale_exponent=scale, scale_factor=factor, buf=out, params=params,
                               lane=lane, depths=depths, scales=scales)
     return res, counter

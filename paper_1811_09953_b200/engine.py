@@ -58,6 +58,7 @@ from .netplan import (  # noqa: F401  (re-exported: reference engine API surface
     project_hops,
     square_activation,
 )
+from .netplan import TimedLayerCounts
 
 ENCODINGS = ("integer", "batched")
 
@@ -649,9 +650,8 @@ def eval_encrypted(net, tensor: CipherTensor, ek: EvalKeys, cfg: FixedPointConfi
         cur = _layer_range(params, lane, ek, plan, lw, cur, 0, n_out, encoding, mul_chunk)
         ev1.record()
         events.append((ev0, ev1))
-    torch.cuda.current_stream().synchronize()
-    for c, (a, b) in zip(counter.layer_counts, events):
-        c.wall_ms = a.elapsed_time(b)
+    # wall_ms resolves from the events on first access (no device sync here)
+    counter.layer_counts = [TimedLayerCounts(c, (a, b, 1.0)) for c, (a, b) in zip(counter.layer_counts, events)]
     out = CipherTensor(compiled.out_shape, scale_exponent=scale, scale_factor=factor, buf=cur, params=params, lane=lane,
                        depths=depths, scales=scales)
     return out, counter

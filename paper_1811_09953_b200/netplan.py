@@ -254,6 +254,25 @@ class LayerCounts:
         )
 
 
+class TimedLayerCounts(LayerCounts):
+    """LayerCounts whose wall_ms is read from CUDA events on first access,
+    so an evaluation does not have to synchronise the device to return."""
+
+    def __init__(self, base: LayerCounts, events=None):
+        super().__init__(base.pt_ct_add, base.ct_ct_add, base.pt_ct_mul, base.ct_ct_mul, base.fast_path_hits, 0.0)
+        object.__setattr__(self, "_events", events)
+
+    def __getattribute__(self, name):
+        if name == "wall_ms":
+            ev = object.__getattribute__(self, "_events")
+            if ev is not None:
+                a, b, share = ev
+                b.synchronize()
+                object.__setattr__(self, "_events", None)
+                object.__setattr__(self, "wall_ms", a.elapsed_time(b) * share + object.__getattribute__(self, "wall_ms"))
+        return object.__getattribute__(self, name)
+
+
 @dataclass
 class HopCounter:
     layer_names: list = field(default_factory=list)

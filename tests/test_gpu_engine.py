@@ -236,3 +236,59 @@ def test_sharded_evaluator_single_rank_nccl(E):
     assert np.array_equal(got.host_bodies(), want.host_bodies())
     assert list(got.depths) == list(want.depths) and list(got.scales) == list(want.scales)
     assert gc.same_ops(wc)
+
+
+def _sampled_first_stage(E, name, n_check, seed=5):
+    """Full-size config: run the GPU evaluator on the complete network, check
+    every decrypted slot against the mod-t integer model, and check the
+    first linear+activation stage's ciphertexts bit-exactly against the
+    oracle on a sample of nodes (the oracle needs ~0.5-2 s per mul_ct)."""
+    from paper_1811_09953_b200 import configs
+    from paper_1811_09953_b200 import fv
+
+    W = configs.WORKLOADS[name]
+    P = fv.EncryptionParams(W.n, W.primes, (W.t,), W.beta)
+    OP = ob.Params(W.n, W.primes, (W.t,), W.beta)
+    cfg = W.fixed_point()
+    net = configs.build_network(name)
+    sk, pk, ek = fv.keygen(P, configs.SEED_KEYS)
+    x = configs.build_inputs(name)
+    tensor = E.encrypt_tensor_batched(pk, P, x, cfg, 0, configs.SEED_ENC)
+    out, counter = E.eval_encrypted(net, tensor, ek, cfg, encoding="batched")
+    comp = E.compile_network(net, cfg)
+    slots = E.decrypt_tensor_slots(sk, out)
+    assert np.array_equal(slots, od.plain_model_batched(comp, x << cfg.precision_bits, W.t))
+    assert counter.same_ops(E.plan_hops(comp, "batched", W.t))
+    # first stage on a sample of nodes, through the oracle
+    first = E.NetworkSpec(net.input_shape, net.layers[:2])
+    mid, _ = E.eval_encrypted(first, tensor, ek, cfg, encoding="batched")
+    got = mid.host_bodies()
+    K = ob.Keys(sk.s.host(), pk.p0.host(), pk.p1.host(), [a.host() for a in ek.a], [g.host() for g in ek.g])
+    bodies = tensor.host_bodies()
+    lin, act = comp.plans[0], comp.plans[1]
+    t = W.t
+    for o in np.random.default_rng(seed).choice(len(lin.outputs), n_check, replace=False):
+        acc = None
+        for tp in lin.outputs[o].taps:
+            term = ob.mul_pt(OP, ob.Ct(bodies[tp.in_index, 0], bodies[tp.in_index, 1], 0, cfg.precision_bits),
+                             [tp.weight_int % t], cfg.precision_bits)
+            acc = term if acc is None else ob.add_ct(OP, acc, term)
+        sq = ob.mul_ct(OP, acc, acc, K)
+        y = sq if act.a2_int is None else ob.mul_pt(OP, sq, [act.a2_int % t], cfg.precision_bits)
+        if act.a1_mult_int is not None:
+            y = ob.add_ct(OP, y, ob.mul_pt(OP, acc, [act.a1_mult_int % t], y.scale - acc.scale))
+        assert np.array_equal(got[o], np.stack([y.c0, y.c1])), o
+        assert int(mid.scales[o]) == y.scale and int(mid.depths[o]) == y.depth
+
+
+def test_cfg2_full_network_sampled_parity(E):
+    _sampled_first_stage(E, "cfg2", 3)
+
+
+def test_cfg4_full_network_sampled_parity(E):
+    _sampled_first_stage(E, "cfg4", 3)
+
+
+@pytest.mark.slow
+def test_cfg3_full_network_sampled_parity(E):
+    _sampled_first_stage(E, "cfg3", 2)

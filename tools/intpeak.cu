@@ -38,6 +38,20 @@ __global__ void k_wide(uint64_t* out, uint32_t a) {
   if (s == 0x12345) out[0] = s;
 }
 
+__global__ void k_imadhi(uint32_t* out, uint32_t a, uint32_t b) {
+  uint32_t x[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) x[c] = threadIdx.x + c;
+  for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) x[c] = __umulhi(x[c], a) + x[c];
+  }
+  uint32_t s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s ^= x[c];
+  if (s == 0x12345) out[0] = s;
+}
+
 __global__ void k_mulw(uint64_t* out, uint64_t w, uint64_t ws, uint64_t nq) {
   uint64_t x[CH];
 #pragma unroll
@@ -77,6 +91,7 @@ int main() {
            ops / (ms * 1e-3) / sms / 1.965e9);
   };
   run("imad", (double)ITERS * CH, [&] { k_imad<<<blocks, threads>>>((uint32_t*)buf, 3, 5); });
+  run("imad.hi", (double)ITERS * CH, [&] { k_imadhi<<<blocks, threads>>>((uint32_t*)buf, 0x9E3779B9u, 5); });
   run("imad.wide", (double)ITERS * CH, [&] { k_wide<<<blocks, threads>>>((uint64_t*)buf, 3); });
   const uint64_t q = 36028797018972161ull;
   const uint64_t w = 1234567891234567ull % q;
