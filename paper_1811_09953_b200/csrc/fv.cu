@@ -858,11 +858,16 @@ extern "C" int fcn_ctx_create(int device, int n, int k, const uint64_t* primes, 
   }
   // ell = max e with beta^e <= q  (fv.py:78-85)
   x->ell = (q.bits() - 1) / log2_beta;
-  // auxiliary base (fv.py:99-107): find_ntt_primes(n, need//54 + 1, bits=55, exclude=q)
+  // Auxiliary base.  The reference scans find_ntt_primes(n, need//54 + 1,
+  // bits=55, exclude=q) (fv.py:99-107); the base only has to make the
+  // extended-base CRT of the tensor exact, which needs P > 2nq.  We use the
+  // same scan (primes > 2^55) with the smallest count giving P >= 8nq, so
+  // |T|/B <= 1/16 (section 5 of DESIGN.md); outputs do not depend on the
+  // choice of auxiliary primes.
   int nb = 0;
   while ((1 << nb) <= n) ++nb;
-  const int need = nb + q.bits() + 1;
-  const int count = need / 54 + 1;
+  const int need = nb + q.bits() + 3;
+  const int count = (need + 54) / 55;
   const uint64_t step = 2ull * (uint64_t)n;
   uint64_t p = ((1ull << 55) / step) * step + 1;
   while ((int)x->aux.size() < count) {
@@ -1158,8 +1163,10 @@ static int lift_or_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t
   const int k = x->k, m = x->m;
 #define FCN_TRY(KQ, KE) \
   if (k <= KQ && m <= KE - KQ) return run_lift_rescale<KQ, KE>(lift, x, lane, in, out, cnt, R01, DG, st);
+  FCN_TRY(2, 5)
   FCN_TRY(2, 6)
   FCN_TRY(3, 6)
+  FCN_TRY(4, 8)
   FCN_TRY(4, 9)
   FCN_TRY(6, 12)
   FCN_TRY(8, 16)

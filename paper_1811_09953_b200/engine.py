@@ -655,3 +655,64 @@ def eval_encrypted(net, tensor: CipherTensor, ek: EvalKeys, cfg: FixedPointConfi
     out = CipherTensor(compiled.out_shape, scale_exponent=scale, scale_factor=factor, buf=cur, params=params, lane=lane,
                        depths=depths, scales=scales)
     return out, counter
+
+
+# ---------------------------------------------------------------- streaming
+
+
+def evaluate_stream(net, host_batches, ek: EvalKeys, cfg: FixedPointConfig, params: EncryptionParams, shape,
+                    scale_exponent: int, lane: int = 0, encoding: str = "batched"):
+    """Serve a sequence of encrypted batches held in (pinned) host memory.
+
+    host_batches: iterable of [count][2][k][n] int64 CPU tensors (the
+    serialized ciphertext bodies).  For each batch this uploads it, runs
+    `eval_encrypted`, and yields the output bodies as a CPU tensor.  Uploads
+    run on a separate copy stream into two preallocated device buffers, so
+    batch i+1 crosses PCIe while batch i is evaluated (what a server loop
+    does); every batch's H2D copy and its result's D2H read stay in the loop."""
+    import torch
+
+    compute = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()
+    it = iter(host_batches)
+    bufs = [None, None]
+    done = [None, None]  # compute-stream event: eval reading bufs[s] finished
+
+    def upload(i, hb):
+        s = i % 2
+        with torch.cuda.stream(copy):
+            if bufs[s] is None or tuple(bufs[s].shape) != tuple(hb.shape):
+                bufs[s] = torch.empty(hb.shape, dtype=hb.dtype, device="cuda")
+            if done[s] is not None:
+                copy.wait_event(done[s])
+            bufs[s].copy_(hb, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+        return ev
+
+    i = 0
+    hb = next(it, None)
+    ready = upload(0, hb) if hb is not None else None
+    pending = None  # (pinned host result, event) of the previous batch
+    while ready is not None:
+        s = i % 2
+        compute.wait_event(ready)
+        nxt = next(it, None)
+        ready = upload(i + 1, nxt) if nxt is not None else None
+        t_in = CipherTensor(shape, scale_exponent=scale_exponent, buf=bufs[s], params=params, lane=lane)
+        out, _ = eval_encrypted(net, t_in, ek, cfg, encoding=encoding)
+        ev = torch.cuda.Event()
+        ev.record(compute)
+        done[s] = ev
+        res = torch.empty(out.buf.shape, dtype=out.buf.dtype, pin_memory=True)
+        res.copy_(out.buf, non_blocking=True)
+        rev = torch.cuda.Event()
+        rev.record(compute)
+        if pending is not None:  # hand back batch i-1 while batch i runs
+            pending[1].synchronize()
+            yield pending[0]
+        pending = (res, rev)
+        i += 1
+    if pending is not None:
+        pending[1].synchronize()
+        yield pending[0]

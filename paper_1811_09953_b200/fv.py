@@ -38,6 +38,27 @@ DEFAULT_SIGMA = 3.2
 DEFAULT_BETA = 1 << 32
 
 
+def _is_prime(v: int) -> bool:
+    for w in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37):
+        if v % w == 0:
+            return v == w
+    d, r = v - 1, 0
+    while d % 2 == 0:
+        d //= 2
+        r += 1
+    for a in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37):
+        x = pow(a, d, v)
+        if x in (1, v - 1):
+            continue
+        for _ in range(r - 1):
+            x = x * x % v
+            if x == v - 1:
+                break
+        else:
+            return False
+    return True
+
+
 class FVError(ValueError):
     """Parameter, lane, or scale mismatch in scheme operations (fv.py:38)."""
 
@@ -145,9 +166,22 @@ class EncryptionParams:
             _ctx_handles[key] = h
         return h
 
-    @property
+    @cached_property
     def aux_primes(self) -> tuple:
-        return self.native().aux
+        """The reference's auxiliary base (fv.py:99-107), for API parity.
+
+        libfcn's exact multiplication uses its own (possibly smaller)
+        extended base, `native().aux`; results do not depend on it."""
+        need = self.n.bit_length() + self.q.bit_length() + 1
+        count = need // 54 + 1
+        step = 2 * self.n
+        p = (1 << 55) // step * step + 1
+        out, skip = [], set(self.limb_primes)
+        while len(out) < count:
+            p += step
+            if p not in skip and _is_prime(p):
+                out.append(p)
+        return tuple(out)
 
     def describe(self) -> str:
         return (

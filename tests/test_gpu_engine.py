@@ -292,3 +292,26 @@ def test_cfg4_full_network_sampled_parity(E):
 @pytest.mark.slow
 def test_cfg3_full_network_sampled_parity(E):
     _sampled_first_stage(E, "cfg3", 2)
+
+
+def test_evaluate_stream_matches_eval(E):
+    """The streaming public API (double-buffered uploads) returns exactly the
+    bodies eval_encrypted produces, in order."""
+    import torch
+
+    from paper_1811_09953_b200 import fv
+    from paper_1811_09953_b200.encode import FixedPointConfig
+
+    P, OP, net = _small_batched_setup(E, fv)
+    cfg = FixedPointConfig((65537,), 4)
+    sk, pk, ek = fv.keygen(P, 2)
+    hosts, wants = [], []
+    for seed in range(3):
+        x = np.random.default_rng(seed).integers(0, 16, (16, P.n))
+        t = E.encrypt_tensor_batched(pk, P, x.reshape(1, 4, 4, P.n), cfg, 0, 10 + seed)
+        hosts.append(t.buf.cpu().pin_memory())
+        wants.append(E.eval_encrypted(net, t, ek, cfg, encoding="batched")[0].host_bodies())
+    got = list(E.evaluate_stream(net, hosts, ek, cfg, P, (1, 4, 4), 4))
+    assert len(got) == 3
+    for g, w in zip(got, wants):
+        assert np.array_equal(g.numpy().view(np.uint64), w)
