@@ -7,7 +7,10 @@
 #include "../paper_1811_09953_b200/csrc/fcn_common.cuh"
 
 using namespace fcn;
-constexpr int CH = 8;      // independent chains per thread
+#ifndef CH_N
+#define CH_N 8
+#endif
+constexpr int CH = CH_N;   // independent chains per thread
 constexpr int ITERS = 4096;
 
 __global__ void k_imad(uint32_t* out, uint32_t a, uint32_t b) {
@@ -66,13 +69,16 @@ __global__ void k_mulw(uint64_t* out, uint64_t w, uint64_t ws, uint64_t nq) {
   if (s == 0x12345) out[0] = s;
 }
 
-int main() {
+#include <cstdlib>
+int main(int argc, char** argv) {
   int dev = 0, sms = 0, clk = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   void* buf;
   cudaMalloc(&buf, 64);
-  const int blocks = sms * 8, threads = 256;
+  const int bps = argc > 1 ? atoi(argv[1]) : 8;
+  const int blocks = sms * bps, threads = 256;
+  printf("blocks/SM %d, chains/thread %d\n", bps, CH);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
