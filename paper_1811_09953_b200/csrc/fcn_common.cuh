@@ -63,6 +63,8 @@ struct LimbConst {
   uint64_t nq;      // 2^64 - q
   uint32_t m32;     // floor(2^64 / q) when q > 2^32, else 0
   uint32_t pad2;
+  double fq;        // q as a double (exact), for the FP64 path (q < 2^51)
+  double fqi;       // 1 / q rounded
 };
 
 struct __align__(16) Twiddle {
@@ -89,6 +91,13 @@ struct fcn_ring {
   // the register pass that owns 32 contiguous residues per thread:
   // [L][u][blk][t] = psi[2^(logn-5+u) + t 2^u + blk], t < n/32 (n >= 32)
   fcn::Twiddle* d_fwd_last = nullptr;
+  // FP64 copies of the four NTT tables for limbs below 2^51 (fp_ok): each
+  // entry {w, w / q} with w the signed representative in (-q/2, q/2].
+  bool fp_ok = false;
+  double2* d_ffwd = nullptr;
+  double2* d_fict = nullptr;
+  double2* d_ftwist = nullptr;
+  double2* d_ffl = nullptr;
 };
 
 namespace fcn {
@@ -192,6 +201,38 @@ __device__ __forceinline__ uint64_t reduce_small(uint64_t x, uint32_t m32, uint6
   const uint32_t qe = __umulhi((uint32_t)(x >> 32), m32);
   const uint64_t r = x - (uint64_t)qe * q;
   return r >= q ? r - q : r;
+}
+
+// ----------------------------------------------- FP64 signed residues
+// For q < 2^51 a residue is held as an integer-valued double x, |x| < 2^53
+// (so every value and every intermediate below is exact).  The FP64 pipe
+// issues these at ~60 ops/clk/SM on B200 (tools/fp64bench.cu), more than
+// twice the integer mulw rate.
+
+// r == a w (mod q), |r| < 1.5 q, for |a| < 2^53, |w| <= q/2, wq = RN(w/q):
+// h + l = a w exactly (FMA error-free product); qt = rint(a wq) is within
+// 1.5 of a w / q, so h - qt q and then + l are exact integers below 2^53.
+__device__ __forceinline__ double fmulq(double a, double w, double wq, double q) {
+  const double h = a * w;
+  const double l = fma(a, w, -h);
+  const double qt = rint(a * wq);
+  return fma(-qt, q, h) + l;
+}
+// x mod q centred: |r| <= q/2 + 2^-40 q for |x| < 2^53 (magic-constant rint,
+// valid since |x / q| < 2^51).
+__device__ __forceinline__ double fredq(double x, double qi, double q) {
+  const double M = 6755399441055744.0;  // 1.5 * 2^52
+  const double qt = fma(x, qi, M) - M;
+  return fma(-qt, q, x);
+}
+// u64 residue (< 2^52) <-> double, bit tricks instead of the slow I2F/F2I.
+__device__ __forceinline__ double u2f(uint64_t x) {
+  return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - 4503599627370496.0;
+}
+// centred |x| <= q/2 + small (any |x| < q) -> canonical [0, q)
+__device__ __forceinline__ uint64_t f2u_canon(double x, double q) {
+  const double y = x < 0.0 ? x + q : x;
+  return (uint64_t)__double_as_longlong(y + 4503599627370496.0) & 0x000FFFFFFFFFFFFFull;
 }
 
 // ---------------------------------------------------- host-side helpers

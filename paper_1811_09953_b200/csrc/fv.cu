@@ -860,21 +860,26 @@ extern "C" int fcn_ctx_create(int device, int n, int k, const uint64_t* primes, 
   x->ell = (q.bits() - 1) / log2_beta;
   // Auxiliary base.  The reference scans find_ntt_primes(n, need//54 + 1,
   // bits=55, exclude=q) (fv.py:99-107); the base only has to make the
-  // extended-base CRT of the tensor exact, which needs P > 2nq.  We use the
-  // same scan (primes > 2^55) with the smallest count giving P >= 8nq, so
-  // |T|/B <= 1/16 (section 5 of DESIGN.md); outputs do not depend on the
-  // choice of auxiliary primes.
+  // extended-base CRT of the tensor exact, which needs P > 2nq.  We take
+  // NTT primes just below 2^51 (descending scan, limb primes excluded) so
+  // every extended-base limb runs the FP64 NTT (q < 2^51), with the
+  // smallest count giving P >= 8nq (each prime > 2^50), so |T|/B <= 1/16
+  // (section 5 of DESIGN.md); outputs do not depend on the choice.
   int nb = 0;
   while ((1 << nb) <= n) ++nb;
   const int need = nb + q.bits() + 3;
-  const int count = (need + 54) / 55;
+  const int count = (need + 49) / 50;
   const uint64_t step = 2ull * (uint64_t)n;
-  uint64_t p = ((1ull << 55) / step) * step + 1;
-  while ((int)x->aux.size() < count) {
-    p += step;
+  uint64_t p = ((1ull << 51) / step) * step + 1;
+  while ((int)x->aux.size() < count && p > (1ull << 50) + step) {
+    p -= step;
     bool skip = false;
     for (uint64_t qq : x->primes) skip |= qq == p;
     if (!skip && h_is_prime(p)) x->aux.push_back(p);
+  }
+  if ((int)x->aux.size() < count) {
+    delete x;
+    return set_error(FCN_ERR_PARAM, "not enough auxiliary NTT primes in (2^50, 2^51)");
   }
   x->m = count;
   if (k + count > KE_LIM) {
@@ -1169,7 +1174,9 @@ static int lift_or_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t
   FCN_TRY(4, 8)
   FCN_TRY(4, 9)
   FCN_TRY(6, 12)
+  FCN_TRY(6, 13)
   FCN_TRY(8, 16)
+  FCN_TRY(8, 17)
   FCN_TRY(16, 32)
 #undef FCN_TRY
   return set_error(FCN_ERR_PARAM, "unsupported limb counts k=%d m=%d", k, m);

@@ -87,6 +87,8 @@ LimbConst make_limb_const(uint64_t q, int n, uint64_t ipsi1) {
   c.nq = (uint64_t)0 - q;
   const unsigned __int128 m = (((unsigned __int128)1) << 64) / q;
   c.m32 = (m >> 32) ? 0u : (uint32_t)m;
+  c.fq = (double)q;
+  c.fqi = 1.0 / (double)q;
   return c;
 }
 
@@ -273,6 +275,31 @@ extern "C" int fcn_ring_create(int device, int n, int count, const uint64_t* pri
   if (e == cudaSuccess) e = cudaMemcpy(r->d_twist, tws.data(), sizeof(Twiddle) * tws.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&r->d_fwd_last, sizeof(Twiddle) * fl.size());
   if (e == cudaSuccess) e = cudaMemcpy(r->d_fwd_last, fl.data(), sizeof(Twiddle) * fl.size(), cudaMemcpyHostToDevice);
+  // FP64 tables for the limbs below 2^51 (entries of larger limbs stay zero)
+  r->fp_ok = true;
+  for (int l = 0; l < count; ++l) r->fp_ok &= primes[l] < (1ull << 51);
+  {
+    const std::vector<Twiddle>* src[4] = {&fw, &ict, &tws, &fl};
+    double2** dst[4] = {&r->d_ffwd, &r->d_fict, &r->d_ftwist, &r->d_ffl};
+    std::vector<double2> f((size_t)count * n);
+    for (int tb = 0; tb < 4 && e == cudaSuccess; ++tb) {
+      for (int l = 0; l < count; ++l) {
+        const uint64_t q = primes[l];
+        for (int i = 0; i < n; ++i) {
+          const size_t o = (size_t)l * n + i;
+          if (q >= (1ull << 51) || (tb == 3 && n < 32)) {
+            f[o] = make_double2(0.0, 0.0);
+            continue;
+          }
+          const uint64_t w = (*src[tb])[o].w;
+          const double ws = w > q / 2 ? -(double)(q - w) : (double)w;
+          f[o] = make_double2(ws, ws / (double)q);
+        }
+      }
+      e = cudaMalloc(dst[tb], sizeof(double2) * f.size());
+      if (e == cudaSuccess) e = cudaMemcpy(*dst[tb], f.data(), sizeof(double2) * f.size(), cudaMemcpyHostToDevice);
+    }
+  }
   if (e != cudaSuccess) {
     fcn_ring_destroy(r);
     return check_cuda(e, "fcn_ring_create upload");
@@ -291,6 +318,10 @@ extern "C" int fcn_ring_destroy(fcn_ring* r) {
     cudaFree(r->d_ict);
     cudaFree(r->d_twist);
     cudaFree(r->d_fwd_last);
+    cudaFree(r->d_ffwd);
+    cudaFree(r->d_fict);
+    cudaFree(r->d_ftwist);
+    cudaFree(r->d_ffl);
   }
   delete r;
   return FCN_OK;
