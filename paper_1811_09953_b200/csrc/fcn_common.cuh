@@ -218,6 +218,15 @@ __device__ __forceinline__ double fmulq(double a, double w, double wq, double q)
   const double qt = rint(a * wq);
   return fma(-qt, q, h) + l;
 }
+// fmulq with the quotient rounded by the 1.5*2^52 magic constant (two FP64
+// pipe ops instead of DMUL + FRND on the XU pipe); requires |a wq| < 2^51.
+__device__ __forceinline__ double fmulq_m(double a, double w, double wq, double q) {
+  const double M = 6755399441055744.0;
+  const double h = a * w;
+  const double l = fma(a, w, -h);
+  const double qt = fma(a, wq, M) - M;
+  return fma(-qt, q, h) + l;
+}
 // x mod q centred: |r| <= q/2 + 2^-40 q for |x| < 2^53 (magic-constant rint,
 // valid since |x / q| < 2^51).
 __device__ __forceinline__ double fredq(double x, double qi, double q) {

@@ -19,6 +19,8 @@
 #include <mutex>
 
 #include "bigint.hpp"
+#include <cstdlib>
+
 #include "fcn_common.cuh"
 
 namespace fcn {
@@ -67,6 +69,7 @@ struct fcn_ctx {
   fcn::MulCtConst* d_mc = nullptr;  // [n_lanes]
   std::vector<fcn::MulCtConst> host_mc;
   unsigned long long* d_fallbacks = nullptr;
+  bool fp = false;  // every ext prime < 2^51: FP64-pipe lift / rescale kernels
 };
 
 struct fcn_keys {
@@ -369,6 +372,9 @@ struct LiftP {
   uint64_t p[KA], np[KA], p_one_s[KA];
   uint64_t lc[KA][KQ], lc_s[KA][KQ];
   uint64_t nqp[KA], nqp_s[KA];  // p_j - (q mod p_j)
+  // FP64 path: signed multipliers {w, w/q}
+  double fq[KQ], fqinv[KQ], fqinvq[KQ];
+  double fp[KA], fpi[KA], flc[KA][KQ], flcq[KA][KQ], fnqp[KA], fnqpq[KA];
 };
 
 template <int KQ, int KE>
@@ -383,6 +389,12 @@ struct RescaleP {
   uint64_t ntp[KQ], ntp_s[KQ];  // q_i - (tP mod q_i)
   uint64_t qinv[KQ], qinv_s[KQ];
   uint64_t dpw[KQ][3], dpw_s[KQ][3];
+  // FP64 path (every ext prime < 2^51): signed multipliers {w, w/q}
+  double fb[KE], fbinv[KE], fbinvq[KE];
+  double fbeta[KQ], fbetaq[KQ];
+  double fq[KQ], fqi[KQ];
+  double frc[KQ][KE], frcq[KQ][KE];
+  double fntp[KQ], fntpq[KQ];
 };
 
 // canonical x mod q for any x < 2^64 (approximate-quotient product by 1)
@@ -450,6 +462,105 @@ __global__ void __launch_bounds__(256) lift_kernel(const uint64_t* __restrict__ 
   }
 }
 
+// FP64-pipe variant of lift_kernel (every ext prime < 2^51): y_i signed
+// (|y_i| < 0.75 q_i), v = floor(sum y_i/q_i + 1/2) (centred: invariant under
+// y_i -> y_i + q_i together with v -> v + 1), aux residues as in
+// rescale_f64_kernel with a reduction after every 4 products.  The K input
+// loads of the next coefficient are issued before this one computes.
+template <int KQ, int KA, int NW>
+__global__ void __launch_bounds__(256) lift_f64_kernel(const uint64_t* __restrict__ in, uint64_t* __restrict__ ext,
+                                                       int64_t npoly, int logn, const __grid_constant__ LiftP<KQ, KA> P,
+                                                       const MulCtConst* __restrict__ cc,
+                                                       unsigned long long* __restrict__ fallbacks) {
+  const int n = 1 << logn;
+  const int k = P.k, m = P.m, K = P.K;
+  const int64_t total = npoly << logn;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  constexpr double M = 6755399441055744.0;
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  uint64_t nx[KQ];
+  if (e < total) {
+#pragma unroll
+    for (int i = 0; i < KQ; ++i) nx[i] = i < k ? in[((e >> logn) * k + i) * n + (e & (n - 1))] : 0;
+  }
+  for (; e < total; e += stride) {
+    const int64_t poly = e >> logn;
+    const int coef = (int)(e & (n - 1));
+    uint64_t cur[KQ];
+#pragma unroll
+    for (int i = 0; i < KQ; ++i) cur[i] = nx[i];
+    if (e + stride < total) {
+      const int64_t e2 = e + stride;
+#pragma unroll
+      for (int i = 0; i < KQ; ++i)
+        if (i < k) nx[i] = in[((e2 >> logn) * k + i) * n + (e2 & (n - 1))];
+    }
+    double y[KQ];
+    double f = 0.5;
+#pragma unroll
+    for (int i = 0; i < KQ; ++i) {
+      y[i] = 0.0;
+      if (i < k) {
+        ext[(poly * K + i) * n + coef] = cur[i];
+        y[i] = fmulq_m(u2f(cur[i]), P.fqinv[i], P.fqinvq[i], P.fq[i]);
+        f = fma(y[i], P.rq[i], f);
+      }
+    }
+    double v = floor(f);
+    const double fr = f - v;
+    if (fr < kEps || fr > 1.0 - kEps) {
+      // exact on the canonical y: x = sum y_i Q_i - u q, then v = u + (x > (q-1)/2)
+      uint64_t yc[KQ];
+      double fc = 0.0;
+#pragma unroll
+      for (int i = 0; i < KQ; ++i) {
+        yc[i] = 0;
+        if (i < k) {
+          double t = y[i];
+          if (t < 0.0) t += P.fq[i];
+          y[i] = t;
+          yc[i] = (uint64_t)t;
+          fc = fma(t, P.rq[i], fc);
+        }
+      }
+      uint64_t a[NW];
+      mw_zero<NW>(a);
+      for (int i = 0; i < k; ++i) mw_mac<NW>(a, cc->Qw[i], cc->qwords, yc[i]);
+      const int64_t u = mw_reduce_q<NW>(a, cc, (int64_t)floor(fc));
+      bool gt = false, decided = false;
+      for (int i = NW - 1; i >= 0; --i) {
+        if (!decided && a[i] != cc->hw[i]) {
+          gt = a[i] > cc->hw[i];
+          decided = true;
+        }
+      }
+      v = (double)(u + (gt ? 1 : 0));
+      atomicAdd(fallbacks, 1ull);
+    }
+#pragma unroll
+    for (int j = 0; j < KA; ++j) {
+      if (j < m) {
+        const double pj = P.fp[j], pji = P.fpi[j];
+        double acc = fmulq_m(v, P.fnqp[j], P.fnqpq[j], pj);
+        int cnt = 1;
+#pragma unroll
+        for (int i = 0; i < KQ; ++i) {
+          if (i < k) {
+            if (cnt == 4) {
+              acc = fredq(acc, pji, pj);
+              cnt = 0;
+            }
+            acc += fmulq_m(y[i], P.flc[j][i], P.flcq[j][i], pj);
+            ++cnt;
+          }
+        }
+        ext[(poly * K + k + j) * n + coef] = f2u_canon(fredq(acc, pji, pj), pj);
+      }
+    }
+  }
+  (void)M;
+}
+
 // NTT-domain tensor: (a0 b0, a0 b1 + a1 b0, a1 b1) per ext limb (fv.py:511-515).
 // Two residues per thread (16-byte loads and stores).
 __global__ void tensor_kernel(const uint64_t* __restrict__ A, const uint64_t* __restrict__ B, uint64_t* __restrict__ T,
@@ -480,6 +591,67 @@ __global__ void tensor_kernel(const uint64_t* __restrict__ A, const uint64_t* __
     *reinterpret_cast<ulonglong2*>(T + ((ct * 3 + 0) * K + j) * n + coef) = t0;
     *reinterpret_cast<ulonglong2*>(T + ((ct * 3 + 1) * K + j) * n + coef) = t1;
     *reinterpret_cast<ulonglong2*>(T + ((ct * 3 + 2) * K + j) * n + coef) = t2;
+  }
+}
+
+// Base-beta digits of the canonical R2 (fv.py:524-533) from its residues:
+// one row per digit when every digit is already < q_i (P.direct), else
+// per-limb rows.
+template <int KQ, int KE, int NW>
+__device__ __forceinline__ void emit_digits(const uint64_t* out, const RescaleP<KQ, KE>& P,
+                                            const MulCtConst* __restrict__ cc, uint64_t* __restrict__ DG, int64_t ct,
+                                            int coef, int n) {
+  const int k = P.k;
+  uint64_t a[NW];
+  mw_zero<NW>(a);
+  double fu = 0.0;
+#pragma unroll
+  for (int i = 0; i < KQ; ++i) {
+    if (i < k) {
+      const uint64_t z = shoup(out[i], P.qinv[i], P.qinv_s[i], P.q[i]);
+      fu += (double)z * P.rq[i];
+      mw_mac<NW>(a, cc->Qw[i], cc->qwords, z);
+    }
+  }
+  mw_reduce_q<NW>(a, cc, (int64_t)floor(fu));
+  const int D = P.D, w = P.w;
+  if (P.direct) {
+    // every digit < 2^w <= min q_i: one row per digit, broadcast to the limbs by the NTT
+    const uint64_t mask = (w >= 64) ? ~0ull : ((1ull << w) - 1);
+    for (int d = 0; d < D; ++d) {
+      const int bit = d * w;
+      const int wi = bit >> 6, bo = bit & 63;
+      uint64_t lo = mw_word<NW>(a, wi) >> bo;
+      if (bo) lo |= mw_word<NW>(a, wi + 1) << (64 - bo);
+      DG[(ct * D + d) * n + coef] = lo & mask;
+    }
+  } else {
+    for (int d = 0; d < D; ++d) {
+      const int bit = d * w;
+      uint64_t dw[3];
+#pragma unroll
+      for (int mword = 0; mword < 3; ++mword) {
+        const int b0 = bit + 64 * mword;
+        const int wi = b0 >> 6, bo = b0 & 63;
+        uint64_t lo = mw_word<NW>(a, wi) >> bo;
+        if (bo) lo |= mw_word<NW>(a, wi + 1) << (64 - bo);
+        const int rem = w - 64 * mword;
+        if (rem <= 0) lo = 0;
+        else if (rem < 64) lo &= (1ull << rem) - 1;
+        dw[mword] = lo;
+      }
+#pragma unroll
+      for (int l = 0; l < KQ; ++l) {
+        if (l < k) {
+          const uint64_t ql = P.q[l];
+          uint64_t val = csub(shoup_lazy(dw[0], 1, P.one_s[l], ql), ql);
+          if (P.dwords > 1) val += csub(shoup_lazy(dw[1], P.dpw[l][1], P.dpw_s[l][1], ql), ql);
+          if (P.dwords > 2) val += csub(shoup_lazy(dw[2], P.dpw[l][2], P.dpw_s[l][2], ql), ql);
+          val = csub(csub(val, 2 * ql), ql);
+          DG[((ct * D + d) * k + l) * n + coef] = val;
+        }
+      }
+    }
   }
 }
 
@@ -557,58 +729,131 @@ __global__ void __launch_bounds__(256, (KQ <= 4 ? 3 : 2)) rescale_kernel(const u
       for (int i = 0; i < KQ; ++i)
         if (i < k) R01[((ct * 2 + p) * k + i) * n + coef] = out[i];
     } else {
-      // 4. canonical multiword R2 = sum z_i Q_i - u q, then base-beta digits
-      uint64_t a[NW];
-      mw_zero<NW>(a);
-      double fu = 0.0;
+      emit_digits<KQ, KE, NW>(out, P, cc, DG, ct, coef, n);
+    }
+  }
+}
+
+// FP64-pipe variant of rescale_kernel for ext primes < 2^51 (same math,
+// signed integer-valued doubles, fcn_common.cuh fmulq/fredq):
+//  1. y_j = T_j binv_j (|y_j| < 0.75 b_j), v = rint(sum y_j / b_j);
+//  2. y_j beta_j = h_j q_j + r_j with any integer h_j (|r_j| < 0.9 q_j):
+//     R is invariant under (h_j, r_j) -> (h_j + 1, r_j - q_j), so only the
+//     rare exact fallback canonicalises r;
+//     (every quotient |a w/q| < 0.75 2^51: magic-constant rounding is exact)
+//  3. R mod q_i = sum_j y_j rc_ij + sum h_j + g - v tP, every product
+//     |.| < 0.7 q_i, reduced to |.| <= q_i/2 + 1 after every 4 terms so
+//     all partial sums stay below 4 q_i < 2^53.
+template <int KQ, int KE, int NW>
+__global__ void __launch_bounds__(256, 2)
+    rescale_f64_kernel(const uint64_t* __restrict__ T, uint64_t* __restrict__ R01, uint64_t* __restrict__ DG, int64_t C,
+                       int logn, const __grid_constant__ RescaleP<KQ, KE> P, const MulCtConst* __restrict__ cc,
+                       unsigned long long* __restrict__ fallbacks) {
+  const int n = 1 << logn;
+  const int k = P.k, K = P.K;
+  const int64_t total = (C * 3) << logn;
+  constexpr int NSH = (KQ + 3) / 4;  // groups of <= 4 quotients (|h_j| < 0.75 2^51): exact sums
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // the K loads of the next coefficient are issued before this one computes
+  uint64_t nx[KE];
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < total) {
 #pragma unroll
-      for (int i = 0; i < KQ; ++i) {
-        if (i < k) {
-          const uint64_t z = shoup(out[i], P.qinv[i], P.qinv_s[i], P.q[i]);
-          fu += (double)z * P.rq[i];
-          mw_mac<NW>(a, cc->Qw[i], cc->qwords, z);
+    for (int j = 0; j < KE; ++j) nx[j] = j < K ? T[((e >> logn) * K + j) * n + (e & (n - 1))] : 0;
+  }
+  for (; e < total; e += stride) {
+    const int64_t cp = e >> logn;
+    const int coef = (int)(e & (n - 1));
+    const int64_t ct = cp / 3;
+    const int p = (int)(cp % 3);
+    uint64_t cur[KE];
+#pragma unroll
+    for (int j = 0; j < KE; ++j) cur[j] = nx[j];
+    if (e + stride < total) {
+      const int64_t e2 = e + stride;
+#pragma unroll
+      for (int j = 0; j < KE; ++j)
+        if (j < K) nx[j] = T[((e2 >> logn) * K + j) * n + (e2 & (n - 1))];
+    }
+    double y[KE];
+    double fv = 0.0;
+#pragma unroll
+    for (int j = 0; j < KE; ++j) {
+      y[j] = 0.0;
+      if (j < K) {
+        const double x = u2f(cur[j]);
+        y[j] = fmulq_m(x, P.fbinv[j], P.fbinvq[j], P.fb[j]);
+        fv = fma(y[j], P.rb[j], fv);
+      }
+    }
+    const double v = rint(fv);
+    double r[KQ];
+    double sh[NSH];
+#pragma unroll
+    for (int g = 0; g < NSH; ++g) sh[g] = 0.0;
+    double G = cc_hq(cc);
+#pragma unroll
+    for (int j = 0; j < KQ; ++j) {
+      r[j] = 0.0;
+      if (j < k) {
+        const double h = y[j] * P.fbeta[j];
+        const double l = fma(y[j], P.fbeta[j], -h);
+        const double hq = fma(y[j], P.fbetaq[j], 6755399441055744.0) - 6755399441055744.0;
+        r[j] = fma(-hq, P.fq[j], h) + l;
+        sh[j / 4] += hq;
+        G = fma(r[j], P.rq[j], G);
+      }
+    }
+    int64_t g = (int64_t)floor(G);
+    const double fr = G - (double)g;
+    if (fr < kEps || fr > 1.0 - kEps) {
+      uint64_t rc[KQ];
+      int64_t corr = 0;
+#pragma unroll
+      for (int j = 0; j < KQ; ++j) {
+        rc[j] = 0;
+        if (j < k) {
+          double rr = r[j];
+          while (rr < 0.0) { rr += P.fq[j]; ++corr; }
+          while (rr >= P.fq[j]) { rr -= P.fq[j]; --corr; }
+          rc[j] = (uint64_t)rr;
         }
       }
-      mw_reduce_q<NW>(a, cc, (int64_t)floor(fu));
-      const int D = P.D, w = P.w;
-      if (P.direct) {
-        // every digit < 2^w <= min q_i: one row per digit, broadcast to the limbs by the NTT
-        const uint64_t mask = (w >= 64) ? ~0ull : ((1ull << w) - 1);
-        for (int d = 0; d < D; ++d) {
-          const int bit = d * w;
-          const int wi = bit >> 6, bo = bit & 63;
-          uint64_t lo = mw_word<NW>(a, wi) >> bo;
-          if (bo) lo |= mw_word<NW>(a, wi + 1) << (64 - bo);
-          DG[(ct * D + d) * n + coef] = lo & mask;
-        }
-      } else {
-        for (int d = 0; d < D; ++d) {
-          const int bit = d * w;
-          uint64_t dw[3];
+      // floor(G) of the canonical r' = r + corr_j q_j is floor(G) + corr
+      g = exact_frac_floor<NW>(rc, k, cc, g + corr) - corr;
+      atomicAdd(fallbacks, 1ull);
+    }
+    const double gd = (double)g;
+    uint64_t out[KQ];
 #pragma unroll
-          for (int mword = 0; mword < 3; ++mword) {
-            const int b0 = bit + 64 * mword;
-            const int wi = b0 >> 6, bo = b0 & 63;
-            uint64_t lo = mw_word<NW>(a, wi) >> bo;
-            if (bo) lo |= mw_word<NW>(a, wi + 1) << (64 - bo);
-            const int rem = w - 64 * mword;
-            if (rem <= 0) lo = 0;
-            else if (rem < 64) lo &= (1ull << rem) - 1;
-            dw[mword] = lo;
-          }
+    for (int i = 0; i < KQ; ++i) {
+      out[i] = 0;
+      if (i < k) {
+        const double qi = P.fq[i], qii = P.fqi[i];
+        double acc = gd + fmulq_m(v, P.fntp[i], P.fntpq[i], qi);
 #pragma unroll
-          for (int l = 0; l < KQ; ++l) {
-            if (l < k) {
-              const uint64_t ql = P.q[l];
-              uint64_t val = csub(shoup_lazy(dw[0], 1, P.one_s[l], ql), ql);
-              if (P.dwords > 1) val += csub(shoup_lazy(dw[1], P.dpw[l][1], P.dpw_s[l][1], ql), ql);
-              if (P.dwords > 2) val += csub(shoup_lazy(dw[2], P.dpw[l][2], P.dpw_s[l][2], ql), ql);
-              val = csub(csub(val, 2 * ql), ql);
-              DG[((ct * D + d) * k + l) * n + coef] = val;
+        for (int g2 = 0; g2 < NSH; ++g2) acc += fredq(sh[g2], qii, qi);
+        int cnt = 1 + NSH;
+#pragma unroll
+        for (int j = 0; j < KE; ++j) {
+          if (j < K) {
+            if (cnt == 4) {
+              acc = fredq(acc, qii, qi);
+              cnt = 0;
             }
+            acc += fmulq_m(y[j], P.frc[i][j], P.frcq[i][j], qi);
+            ++cnt;
           }
         }
+        out[i] = f2u_canon(fredq(acc, qii, qi), qi);
       }
+    }
+    if (p < 2) {
+#pragma unroll
+      for (int i = 0; i < KQ; ++i)
+        if (i < k) R01[((ct * 2 + p) * k + i) * n + coef] = out[i];
+    } else {
+      emit_digits<KQ, KE, NW>(out, P, cc, DG, ct, coef, n);
     }
   }
 }
@@ -894,6 +1139,10 @@ extern "C" int fcn_ctx_create(int device, int n, int k, const uint64_t* primes, 
     return rc;
   }
   x->logn = x->ext->logn;
+  {
+    const char* ev = getenv("FCN_NTT_INT");  // A/B switch: integer kernels only
+    x->fp = x->ext->fp_ok && !(ev && ev[0] == '1');
+  }
   std::vector<MulCtConst> host(n_lanes);
   for (int l = 0; l < n_lanes; ++l) {
     rc = build_mulct_const(x, x->lanes[l], &host[l]);
@@ -1073,6 +1322,9 @@ extern "C" size_t fcn_mul_ct_workspace_bytes(const fcn_ctx* x, int64_t chunk) {
   return (size_t)(mulct_words_per_ct(x) * chunk * 8);
 }
 
+// signed representative in (-q/2, q/2] as a double (q < 2^51: exact)
+static double h_signed(uint64_t w, uint64_t q) { return w > q / 2 ? -(double)(q - w) : (double)w; }
+
 template <int KQ, int KA>
 static LiftP<KQ, KA> make_lift_params(const fcn_ctx* x, const MulCtConst& mc) {
   LiftP<KQ, KA> P;
@@ -1087,9 +1339,18 @@ static LiftP<KQ, KA> make_lift_params(const fcn_ctx* x, const MulCtConst& mc) {
     P.qinv[i] = mc.qinv[i];
     P.qinv_s[i] = mc.qinv_s[i];
     P.rq[i] = mc.rq[i];
+    P.fq[i] = (double)x->primes[i];
+    P.fqinv[i] = h_signed(mc.qinv[i], x->primes[i]);
+    P.fqinvq[i] = P.fqinv[i] / P.fq[i];
   }
   for (int j = 0; j < x->m; ++j) {
     const uint64_t pj = x->aux[j];
+    P.fp[j] = (double)pj;
+    P.fpi[j] = 1.0 / (double)pj;
+    for (int i = 0; i < x->k; ++i) {
+      P.flc[j][i] = h_signed(mc.lc[j][i], pj);
+      P.flcq[j][i] = P.flc[j][i] / (double)pj;
+    }
     P.p[j] = pj;
     P.np[j] = (uint64_t)0 - pj;
     P.p_one_s[j] = h_shoup(1, pj);
@@ -1100,6 +1361,8 @@ static LiftP<KQ, KA> make_lift_params(const fcn_ctx* x, const MulCtConst& mc) {
     const uint64_t qp = q.mod_small(pj);
     P.nqp[j] = (pj - qp) % pj;
     P.nqp_s[j] = h_shoup(P.nqp[j], pj);
+    P.fnqp[j] = h_signed(P.nqp[j], pj);
+    P.fnqpq[j] = P.fnqp[j] / (double)pj;
   }
   return P;
 }
@@ -1121,6 +1384,9 @@ static RescaleP<KQ, KE> make_rescale_params(const fcn_ctx* x, const MulCtConst& 
     P.binv[j] = mc.binv[j];
     P.binv_s[j] = mc.binv_s[j];
     P.rb[j] = mc.rb[j];
+    P.fb[j] = (double)P.q[j];
+    P.fbinv[j] = h_signed(mc.binv[j], P.q[j]);
+    P.fbinvq[j] = P.fbinv[j] / (double)P.q[j];
   }
   for (int i = 0; i < k; ++i) {
     const uint64_t qi = x->primes[i];
@@ -1136,6 +1402,16 @@ static RescaleP<KQ, KE> make_rescale_params(const fcn_ctx* x, const MulCtConst& 
     }
     P.ntp[i] = mc.rvt[i][1];  // (-tP) mod q_i
     P.ntp_s[i] = h_shoup(P.ntp[i], qi);
+    P.fq[i] = (double)qi;
+    P.fqi[i] = 1.0 / (double)qi;
+    P.fbeta[i] = (double)mc.beta[i];
+    P.fbetaq[i] = (double)mc.beta[i] / (double)qi;
+    P.fntp[i] = h_signed(P.ntp[i], qi);
+    P.fntpq[i] = P.fntp[i] / (double)qi;
+    for (int j = 0; j < K; ++j) {
+      P.frc[i][j] = h_signed(mc.rc[i][j], qi);
+      P.frcq[i][j] = P.frc[i][j] / (double)qi;
+    }
     for (int mm = 0; mm < 3; ++mm) {
       P.dpw[i][mm] = mc.dpw[i][mm];
       P.dpw_s[i][mm] = mc.dpw_s[i][mm];
@@ -1152,13 +1428,23 @@ static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_
   if (lift) {
     const LiftP<KQ, KE - KQ> P = make_lift_params<KQ, KE - KQ>(x, mc);
     const int64_t total = cnt << x->logn;  // cnt = polys
-    lift_kernel<KQ, KE - KQ, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, out, cnt, x->logn, P, dmc, x->d_fallbacks);
-    FCN_LAUNCH_CHECK("lift_kernel");
+    if (x->fp)
+      lift_f64_kernel<KQ, KE - KQ, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, out, cnt, x->logn, P, dmc,
+                                                                                 x->d_fallbacks);
+    else
+      lift_kernel<KQ, KE - KQ, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, out, cnt, x->logn, P, dmc,
+                                                                             x->d_fallbacks);
+    FCN_LAUNCH_CHECK(x->fp ? "lift_f64_kernel" : "lift_kernel");
   } else {
     const RescaleP<KQ, KE> P = make_rescale_params<KQ, KE>(x, mc);
     const int64_t total = (cnt * 3) << x->logn;  // cnt = ciphertexts
-    rescale_kernel<KQ, KE, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, R01, DG, cnt, x->logn, P, dmc, x->d_fallbacks);
-    FCN_LAUNCH_CHECK("rescale_kernel");
+    if (x->fp)
+      rescale_f64_kernel<KQ, KE, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, R01, DG, cnt, x->logn, P, dmc,
+                                                                               x->d_fallbacks);
+    else
+      rescale_kernel<KQ, KE, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, R01, DG, cnt, x->logn, P, dmc,
+                                                                           x->d_fallbacks);
+    FCN_LAUNCH_CHECK(x->fp ? "rescale_f64_kernel" : "rescale_kernel");
   }
   return FCN_OK;
 }

@@ -195,13 +195,15 @@ def _sqrt_mod_p(a, p):
     return r
 
 
-def test_exact_fallback_paths(F):
+@pytest.mark.parametrize("primes", [(36028797018972161, 36028797018990593), (1125899906826241, 1125899906820097)],
+                         ids=["int64-55bit", "fp64-50bit"])
+def test_exact_fallback_paths(F, primes):
     """Inputs placed on the float64 ambiguity bands must take the exact
-    multiword path and still match the oracle bit-for-bit."""
+    multiword path and still match the oracle bit-for-bit (55-bit limbs run
+    the integer kernels, 50-bit limbs the FP64-pipe kernels)."""
     from paper_1811_09953_b200 import device as dev
 
     n = 1024
-    primes = (36028797018972161, 36028797018990593)
     P = F.EncryptionParams(n, primes, (1099511922689,))
     OP = ob.Params(n, primes, P.t_lanes, P.beta)
     sk, pk, ek = F.keygen(P, 42)
