@@ -482,9 +482,12 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 // ================================================================= f64
 // Same three-pass structure as v2, butterflies on the FP64 pipe with signed
 // integer-valued doubles (fcn_common.cuh fmulq/fredq) for limbs q < 2^51.
-// Bounds: inputs |x| < q; a butterfly adds |t| < 1.5q; every value is
-// reduced to |x| <= q/2 + 1 before each even stage s >= 2, so nothing exceeds
-// 4q < 2^53 and all arithmetic is exact.
+// Bounds (q < 2^51): for |Y| <= Bq the quotient rint(Y w/q) is within
+// 1/2 + B/4 of the exact one (|w| <= q/2, two roundings of 2^-53), so a
+// butterfly adds |t| <= (1/2 + B/4) q.  From canonical inputs (B = 1) three
+// stages reach B = 3.86; from a reduced |x| <= q/2 + 1, three stages reach
+// 2.88.  Every value is therefore reduced before stages 3, 6, 9, 12 and
+// nothing ever exceeds 3.86 q < 2^53: all arithmetic is exact.
 
 __device__ __forceinline__ double2 ld_ftw(const double2* p) { return __ldg(p); }
 
@@ -506,7 +509,7 @@ __device__ __forceinline__ void fwd_ctf(double* x, int b, const double2* __restr
   constexpr int G = 1 << R;
 #pragma unroll
   for (int u = 0; u < R; ++u) {
-    if (S0 + u >= 2 && ((S0 + u) & 1) == 0) fred_all<G>(x, q, qi);
+    if (S0 + u > 0 && (S0 + u) % 3 == 0) fred_all<G>(x, q, qi);
     const int tb = (1 << (S0 + u)) + (b << u);
     const int h = G >> (u + 1);
 #pragma unroll
@@ -527,7 +530,7 @@ __device__ __forceinline__ void fwd_ctf_last(double* x, int t, int T, const doub
   int off = 0;
 #pragma unroll
   for (int u = 0; u < 5; ++u) {
-    if (S0 + u >= 2 && ((S0 + u) & 1) == 0) fred_all<32>(x, q, qi);
+    if (S0 + u > 0 && (S0 + u) % 3 == 0) fred_all<32>(x, q, qi);
     const int h = 32 >> (u + 1);
 #pragma unroll
     for (int blk = 0; blk < (1 << u); ++blk) {
@@ -547,7 +550,7 @@ __device__ __forceinline__ void inv_ctf(double* x, int o, const double2* __restr
   constexpr int G = 1 << R;
 #pragma unroll
   for (int u = 0; u < R; ++u) {
-    if (S0 + u >= 2 && ((S0 + u) & 1) == 0) fred_all<G>(x, q, qi);
+    if (S0 + u > 0 && (S0 + u) % 3 == 0) fred_all<G>(x, q, qi);
     const int hd = 1 << u;
     const int tb = (1 << (S0 + u)) + o;
 #pragma unroll
