@@ -77,6 +77,8 @@ struct fcn_keys {
   int D = 0, k = 0, n = 0;
   uint64_t* d_g = nullptr;  // [D][k][n] NTT domain
   uint64_t* d_a = nullptr;
+  double2* d_fg = nullptr;  // FP64 path: {signed w, w / q_l} of d_g / d_a
+  double2* d_fa = nullptr;
 };
 
 namespace fcn {
@@ -655,6 +657,63 @@ __device__ __forceinline__ void emit_digits(const uint64_t* out, const RescaleP<
   }
 }
 
+// FP64-pipe tensor (every ext prime < 2^51).  Inputs are centred
+// (|a| <= q/2) so a product's quotient estimate rint(ab/q) is within 0.75
+// and the remainder |r| <= 0.75 q canonicalises with one conditional add.
+__device__ __forceinline__ double fcentre(uint64_t x, uint64_t qh, double q) {
+  const double d = u2f(x);
+  return x > qh ? d - q : d;
+}
+__device__ __forceinline__ double fprod(double a, double b, double q, double qi) {
+  const double M = 6755399441055744.0;
+  const double h = a * b;
+  const double l = fma(a, b, -h);
+  const double qt = fma(h, qi, M) - M;
+  return fma(-qt, q, h) + l;
+}
+
+__global__ void tensor_f64_kernel(const uint64_t* __restrict__ A, const uint64_t* __restrict__ B, uint64_t* __restrict__ T,
+                                  int64_t C, int K, int logn, const LimbConst* __restrict__ lcs) {
+  const int n = 1 << logn;
+  const int64_t total = (C * K) << (logn - 1);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rowi = e >> (logn - 1);
+    const int coef = (int)(e & ((n >> 1) - 1)) * 2;
+    const int64_t ct = rowi / K;
+    const int j = (int)(rowi % K);
+    const LimbConst& c = lcs[j];
+    const uint64_t qh = c.q >> 1;
+    const double q = c.fq, qi = c.fqi;
+    const int64_t i0 = ((ct * 2 + 0) * K + j) * n + coef, i1 = ((ct * 2 + 1) * K + j) * n + coef;
+    const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(A + i0), a1 = *reinterpret_cast<const ulonglong2*>(A + i1);
+    const double x0[2] = {fcentre(a0.x, qh, q), fcentre(a0.y, qh, q)};
+    const double x1[2] = {fcentre(a1.x, qh, q), fcentre(a1.y, qh, q)};
+    uint64_t t0[2], t1[2], t2[2];
+    if (B) {
+      const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(B + i0), b1 = *reinterpret_cast<const ulonglong2*>(B + i1);
+      const double y0[2] = {fcentre(b0.x, qh, q), fcentre(b0.y, qh, q)};
+      const double y1[2] = {fcentre(b1.x, qh, q), fcentre(b1.y, qh, q)};
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        t0[v] = f2u_canon(fprod(x0[v], y0[v], q, qi), q);
+        t1[v] = f2u_canon(fredq(fprod(x0[v], y1[v], q, qi) + fprod(x1[v], y0[v], q, qi), qi, q), q);
+        t2[v] = f2u_canon(fprod(x1[v], y1[v], q, qi), q);
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        t0[v] = f2u_canon(fprod(x0[v], x0[v], q, qi), q);
+        const double m = fprod(x0[v], x1[v], q, qi);
+        t1[v] = f2u_canon(fredq(m + m, qi, q), q);
+        t2[v] = f2u_canon(fprod(x1[v], x1[v], q, qi), q);
+      }
+    }
+    *reinterpret_cast<ulonglong2*>(T + ((ct * 3 + 0) * K + j) * n + coef) = make_ulonglong2(t0[0], t0[1]);
+    *reinterpret_cast<ulonglong2*>(T + ((ct * 3 + 1) * K + j) * n + coef) = make_ulonglong2(t1[0], t1[1]);
+    *reinterpret_cast<ulonglong2*>(T + ((ct * 3 + 2) * K + j) * n + coef) = make_ulonglong2(t2[0], t2[1]);
+  }
+}
+
 // Exact rescale R = floor((t T + (q-1)/2) / q) mod q from the ext-base
 // residues of T (fv.py:473-490, 517-522); for the third tensor poly the
 // base-beta digits of R (fv.py:524-533) are emitted instead: one row per
@@ -902,6 +961,74 @@ __global__ void __launch_bounds__(256, 4) keymac_kernel(const uint64_t* __restri
     }
     ACC[((ct * 2 + 0) * k + l) * n + coef] = reduce128(gh, gl, c);
     ACC[((ct * 2 + 1) * k + l) * n + coef] = reduce128(ah, al, c);
+  }
+}
+
+// FP64 copies of the NTT-domain key words: {signed w, w / q_l}.
+__global__ void key_to_f64_kernel(const uint64_t* __restrict__ w, double2* __restrict__ f, int64_t total, int k, int logn,
+                                  const LimbConst* __restrict__ lcs) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int l = (int)((e >> logn) % k);
+    const uint64_t q = lcs[l].q;
+    const uint64_t v = w[e];
+    const double s = v > q / 2 ? -(double)(q - v) : (double)v;
+    f[e] = make_double2(s, s / (double)q);
+  }
+}
+
+// FP64-pipe key MAC (every limb < 2^51): digits are canonical NTT outputs,
+// so each product fmulq_m(x, w, w/q) has |x w/q| < 2^50 (magic rounding
+// exact) and |.| < 0.75 q; sums are reduced after every 4 products (< 3.5 q).
+// Both outputs' 2D key words stay in registers across the ciphertexts the
+// thread walks; the next ciphertext's D digit loads are issued early.
+template <int DMAX>
+__global__ void __launch_bounds__(256, 2) keymac_f64_kernel(const uint64_t* __restrict__ DG, const double2* __restrict__ kg,
+                                                            const double2* __restrict__ ka, uint64_t* __restrict__ ACC,
+                                                            int64_t C, int D, int k, int logn,
+                                                            const LimbConst* __restrict__ lcs) {
+  const int n = 1 << logn;
+  const int64_t lc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // l * n + coef
+  if (lc >= (int64_t)k * n) return;
+  const int l = (int)(lc >> logn);
+  const int coef = (int)(lc & (n - 1));
+  const double q = lcs[l].fq, qi = lcs[l].fqi;
+  double2 gk[DMAX], ak[DMAX];
+#pragma unroll
+  for (int d = 0; d < DMAX; ++d) {
+    gk[d] = d < D ? kg[((int64_t)d * k + l) * n + coef] : make_double2(0.0, 0.0);
+    ak[d] = d < D ? ka[((int64_t)d * k + l) * n + coef] : make_double2(0.0, 0.0);
+  }
+  const int64_t per = (C + gridDim.y - 1) / gridDim.y;
+  const int64_t c0 = (int64_t)blockIdx.y * per;
+  const int64_t c1 = c0 + per < C ? c0 + per : C;
+  uint64_t nx[DMAX];
+  if (c0 < c1) {
+#pragma unroll
+    for (int d = 0; d < DMAX; ++d) nx[d] = d < D ? DG[((c0 * D + d) * k + l) * n + coef] : 0;
+  }
+  for (int64_t ct = c0; ct < c1; ++ct) {
+    double xs[DMAX];
+#pragma unroll
+    for (int d = 0; d < DMAX; ++d) xs[d] = u2f(nx[d]);
+    if (ct + 1 < c1) {
+#pragma unroll
+      for (int d = 0; d < DMAX; ++d)
+        if (d < D) nx[d] = DG[(((ct + 1) * D + d) * k + l) * n + coef];
+    }
+    double g = 0.0, a = 0.0;
+#pragma unroll
+    for (int d = 0; d < DMAX; ++d) {
+      if (d < D) {
+        if (d > 0 && (d & 3) == 0) {
+          g = fredq(g, qi, q);
+          a = fredq(a, qi, q);
+        }
+        g += fmulq_m(xs[d], gk[d].x, gk[d].y, q);
+        a += fmulq_m(xs[d], ak[d].x, ak[d].y, q);
+      }
+    }
+    ACC[((ct * 2 + 0) * k + l) * n + coef] = f2u_canon(fredq(g, qi, q), q);
+    ACC[((ct * 2 + 1) * k + l) * n + coef] = f2u_canon(fredq(a, qi, q), q);
   }
 }
 
@@ -1231,6 +1358,20 @@ extern "C" int fcn_keys_create(const fcn_ctx* x, const uint64_t* a, const uint64
   }
   int rc = launch_ntt(x->ext, kk->d_g, (int64_t)kk->D * kk->k, kk->k, 0, true, 0);
   if (!rc) rc = launch_ntt(x->ext, kk->d_a, (int64_t)kk->D * kk->k, kk->k, 0, true, 0);
+  if (!rc && x->fp && kk->D <= 8) {
+    e = cudaMalloc(&kk->d_fg, words * sizeof(double2));
+    if (e == cudaSuccess) e = cudaMalloc(&kk->d_fa, words * sizeof(double2));
+    if (e != cudaSuccess) {
+      rc = check_cuda(e, "fcn_keys_create fp64 copies");
+    } else {
+      key_to_f64_kernel<<<grid_for((int64_t)words, 256), 256>>>(kk->d_g, kk->d_fg, (int64_t)words, kk->k, x->logn,
+                                                                x->ext->d_lc);
+      key_to_f64_kernel<<<grid_for((int64_t)words, 256), 256>>>(kk->d_a, kk->d_fa, (int64_t)words, kk->k, x->logn,
+                                                                x->ext->d_lc);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) rc = check_cuda(e, "key_to_f64_kernel");
+    }
+  }
   if (!rc) {
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) rc = check_cuda(e, "fcn_keys_create ntt");
@@ -1249,6 +1390,8 @@ extern "C" int fcn_keys_destroy(fcn_keys* kk) {
     DeviceGuard g(kk->device);
     cudaFree(kk->d_g);
     cudaFree(kk->d_a);
+    cudaFree(kk->d_fg);
+    cudaFree(kk->d_fa);
   }
   delete kk;
   return FCN_OK;
@@ -1476,6 +1619,18 @@ static int launch_keymac(const uint64_t* DG, const fcn_keys* keys, uint64_t* ACC
   if (split > C) split = C;
   if (split < 1) split = 1;
   dim3 grid(bx, (unsigned)split);
+  if (keys->d_fg && D <= 8) {
+    // exact digit count as the template argument: key words of unused digits take no registers
+    // (beyond 8 digits the 4D key doubles no longer fit the register budget: integer kernel)
+    switch (D) {
+#define FCN_KM(DD) \
+  case DD: keymac_f64_kernel<DD><<<grid, 256, 0, st>>>(DG, keys->d_fg, keys->d_fa, ACC, C, DD, k, x->logn, x->ext->d_lc); break;
+      FCN_KM(1) FCN_KM(2) FCN_KM(3) FCN_KM(4) FCN_KM(5) FCN_KM(6) FCN_KM(7) FCN_KM(8)
+#undef FCN_KM
+    }
+    FCN_LAUNCH_CHECK("keymac_f64_kernel");
+    return FCN_OK;
+  }
   if (D <= 4)
     keymac_kernel<4><<<grid, 256, 0, st>>>(DG, keys->d_g, keys->d_a, ACC, C, D, k, x->logn, x->ext->d_lc);
   else if (D <= 8)
@@ -1525,8 +1680,13 @@ extern "C" int fcn_mul_ct(const fcn_ctx* x, const fcn_keys* keys, int lane, cons
       if (rc) return rc;
     }
     // (ii) tensor, (iii) inverse NTT
-    tensor_kernel<<<grid_for((C * K) << (logn - 1), 256), 256, 0, st>>>(EA, b ? EB : nullptr, T, C, K, logn, x->ext->d_lc);
-    FCN_LAUNCH_CHECK("tensor_kernel");
+    if (x->fp)
+      tensor_f64_kernel<<<grid_for((C * K) << (logn - 1), 256), 256, 0, st>>>(EA, b ? EB : nullptr, T, C, K, logn,
+                                                                              x->ext->d_lc);
+    else
+      tensor_kernel<<<grid_for((C * K) << (logn - 1), 256), 256, 0, st>>>(EA, b ? EB : nullptr, T, C, K, logn,
+                                                                          x->ext->d_lc);
+    FCN_LAUNCH_CHECK(x->fp ? "tensor_f64_kernel" : "tensor_kernel");
     int rc = launch_ntt(x->ext, T, C * 3 * K, K, 0, false, st);
     if (rc) return rc;
     // (iv) exact rescale + digit decomposition
