@@ -203,6 +203,16 @@ __device__ __forceinline__ uint64_t reduce_small(uint64_t x, uint32_t m32, uint6
   return r >= q ? r - q : r;
 }
 
+// async global -> shared copies (Ampere+ cp.async; completion per thread)
+__device__ __forceinline__ void cp_async8(uint64_t* smem_dst, const uint64_t* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 // ----------------------------------------------- FP64 signed residues
 // For q < 2^51 a residue is held as an integer-valued double x, |x| < 2^53
 // (so every value and every intermediate below is exact).  The FP64 pipe

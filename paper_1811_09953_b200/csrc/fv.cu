@@ -467,15 +467,16 @@ __global__ void __launch_bounds__(256) lift_kernel(const uint64_t* __restrict__ 
 // FP64-pipe variant of lift_kernel (every ext prime < 2^51): y_i signed
 // (|y_i| < 0.75 q_i), v = floor(sum y_i/q_i + 1/2) (centred: invariant under
 // y_i -> y_i + q_i together with v -> v + 1), aux residues as in
-// rescale_f64_kernel with a reduction after every 4 products.  The K input
+// rescale_f64_kernel with a reduction before every 4th product.  The K input
 // loads of the next coefficient are issued before this one computes.
+// Instantiated for exact limb counts (k = KQ, m = KA) only.
 template <int KQ, int KA, int NW>
 __global__ void __launch_bounds__(256) lift_f64_kernel(const uint64_t* __restrict__ in, uint64_t* __restrict__ ext,
                                                        int64_t npoly, int logn, const __grid_constant__ LiftP<KQ, KA> P,
                                                        const MulCtConst* __restrict__ cc,
                                                        unsigned long long* __restrict__ fallbacks) {
   const int n = 1 << logn;
-  const int k = P.k, m = P.m, K = P.K;
+  constexpr int k = KQ, m = KA, K = KQ + KA;  // exact-size instantiations only
   const int64_t total = npoly << logn;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   constexpr double M = 6755399441055744.0;
@@ -544,17 +545,10 @@ __global__ void __launch_bounds__(256) lift_f64_kernel(const uint64_t* __restric
       if (j < m) {
         const double pj = P.fp[j], pji = P.fpi[j];
         double acc = fmulq_m(v, P.fnqp[j], P.fnqpq[j], pj);
-        int cnt = 1;
 #pragma unroll
         for (int i = 0; i < KQ; ++i) {
-          if (i < k) {
-            if (cnt == 4) {
-              acc = fredq(acc, pji, pj);
-              cnt = 0;
-            }
-            acc += fmulq_m(y[i], P.flc[j][i], P.flcq[j][i], pj);
-            ++cnt;
-          }
+          if ((i & 3) == 3) acc = fredq(acc, pji, pj);
+          acc += fmulq_m(y[i], P.flc[j][i], P.flcq[j][i], pj);
         }
         ext[(poly * K + k + j) * n + coef] = f2u_canon(fredq(acc, pji, pj), pj);
       }
@@ -801,39 +795,51 @@ __global__ void __launch_bounds__(256, (KQ <= 4 ? 3 : 2)) rescale_kernel(const u
 //     rare exact fallback canonicalises r;
 //     (every quotient |a w/q| < 0.75 2^51: magic-constant rounding is exact)
 //  3. R mod q_i = sum_j y_j rc_ij + sum h_j + g - v tP, every product
-//     |.| < 0.7 q_i, reduced to |.| <= q_i/2 + 1 after every 4 terms so
-//     all partial sums stay below 4 q_i < 2^53.
+//     |.| < 0.7 q_i, reduced to |.| <= q_i/2 + 1 before products 3, 7, 11..
+//     so all partial sums stay below 3.6 q_i < 2^53.
+// Instantiated for exact limb counts (k = KQ, K = KE) only.
 template <int KQ, int KE, int NW>
-__global__ void __launch_bounds__(256, 2)
-    rescale_f64_kernel(const uint64_t* __restrict__ T, uint64_t* __restrict__ R01, uint64_t* __restrict__ DG, int64_t C,
+__global__ void __launch_bounds__(256, 3)
+    rescale_f64_kernel(const uint64_t* __restrict__ T_in, uint64_t* __restrict__ R01, uint64_t* __restrict__ DG, int64_t C,
                        int logn, const __grid_constant__ RescaleP<KQ, KE> P, const MulCtConst* __restrict__ cc,
                        unsigned long long* __restrict__ fallbacks) {
   const int n = 1 << logn;
-  const int k = P.k, K = P.K;
+  constexpr int k = KQ, K = KE;  // exact-size instantiations only
   const int64_t total = (C * 3) << logn;
   constexpr int NSH = (KQ + 3) / 4;  // groups of <= 4 quotients (|h_j| < 0.75 2^51): exact sums
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  // the K loads of the next coefficient are issued before this one computes
-  uint64_t nx[KE];
+  // thread-private two-stage cp.async ring [stage][j][thread]: the K loads of
+  // the next coefficient are in flight while this one computes, without
+  // holding registers (coalesced: consecutive threads, consecutive words)
+  extern __shared__ uint64_t stage_buf[];
+  const int tid = threadIdx.x, T = blockDim.x;
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e < total) {
 #pragma unroll
-    for (int j = 0; j < KE; ++j) nx[j] = j < K ? T[((e >> logn) * K + j) * n + (e & (n - 1))] : 0;
+    for (int j = 0; j < KE; ++j)
+      if (j < K) cp_async8(&stage_buf[j * T + tid], &T_in[((e >> logn) * K + j) * n + (e & (n - 1))]);
   }
+  cp_async_commit();
+  int sb = 0;
   for (; e < total; e += stride) {
     const int64_t cp = e >> logn;
     const int coef = (int)(e & (n - 1));
     const int64_t ct = cp / 3;
     const int p = (int)(cp % 3);
-    uint64_t cur[KE];
-#pragma unroll
-    for (int j = 0; j < KE; ++j) cur[j] = nx[j];
     if (e + stride < total) {
       const int64_t e2 = e + stride;
+      uint64_t* nb = stage_buf + (sb ^ 1) * KE * T;
 #pragma unroll
       for (int j = 0; j < KE; ++j)
-        if (j < K) nx[j] = T[((e2 >> logn) * K + j) * n + (e2 & (n - 1))];
+        if (j < K) cp_async8(&nb[j * T + tid], &T_in[((e2 >> logn) * K + j) * n + (e2 & (n - 1))]);
     }
+    cp_async_commit();
+    cp_async_wait<1>();
+    uint64_t cur[KE];
+    const uint64_t* cb = stage_buf + sb * KE * T;
+#pragma unroll
+    for (int j = 0; j < KE; ++j) cur[j] = j < K ? cb[j * T + tid] : 0;
+    sb ^= 1;
     double y[KE];
     double fv = 0.0;
 #pragma unroll
@@ -892,17 +898,11 @@ __global__ void __launch_bounds__(256, 2)
         double acc = gd + fmulq_m(v, P.fntp[i], P.fntpq[i], qi);
 #pragma unroll
         for (int g2 = 0; g2 < NSH; ++g2) acc += fredq(sh[g2], qii, qi);
-        int cnt = 1 + NSH;
+        if (NSH > 1) acc = fredq(acc, qii, qi);
 #pragma unroll
         for (int j = 0; j < KE; ++j) {
-          if (j < K) {
-            if (cnt == 4) {
-              acc = fredq(acc, qii, qi);
-              cnt = 0;
-            }
-            acc += fmulq_m(y[j], P.frc[i][j], P.frcq[i][j], qi);
-            ++cnt;
-          }
+          if ((j & 3) == 3) acc = fredq(acc, qii, qi);
+          acc += fmulq_m(y[j], P.frc[i][j], P.frcq[i][j], qi);
         }
         out[i] = f2u_canon(fredq(acc, qii, qi), qi);
       }
@@ -1566,28 +1566,35 @@ static RescaleP<KQ, KE> make_rescale_params(const fcn_ctx* x, const MulCtConst& 
 template <int KQ, int KE>
 static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t* in, uint64_t* out, int64_t cnt,
                             uint64_t* R01, uint64_t* DG, cudaStream_t st) {
+  const bool f64 = x->fp && x->k == KQ && x->k + x->m == KE;  // FP64 kernels: exact sizes
   const MulCtConst& mc = x->host_mc[lane];
   const MulCtConst* dmc = x->d_mc + lane;
   if (lift) {
     const LiftP<KQ, KE - KQ> P = make_lift_params<KQ, KE - KQ>(x, mc);
     const int64_t total = cnt << x->logn;  // cnt = polys
-    if (x->fp)
+    if (f64)
       lift_f64_kernel<KQ, KE - KQ, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, out, cnt, x->logn, P, dmc,
                                                                                  x->d_fallbacks);
     else
       lift_kernel<KQ, KE - KQ, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, out, cnt, x->logn, P, dmc,
                                                                              x->d_fallbacks);
-    FCN_LAUNCH_CHECK(x->fp ? "lift_f64_kernel" : "lift_kernel");
+    FCN_LAUNCH_CHECK(f64 ? "lift_f64_kernel" : "lift_kernel");
   } else {
     const RescaleP<KQ, KE> P = make_rescale_params<KQ, KE>(x, mc);
     const int64_t total = (cnt * 3) << x->logn;  // cnt = ciphertexts
-    if (x->fp)
-      rescale_f64_kernel<KQ, KE, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, R01, DG, cnt, x->logn, P, dmc,
-                                                                               x->d_fallbacks);
+    if (f64) {
+      const int smem = 2 * KE * 256 * 8;
+      static std::once_flag once;
+      std::call_once(once, [&] {
+        cudaFuncSetAttribute(rescale_f64_kernel<KQ, KE, KQ + 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      });
+      rescale_f64_kernel<KQ, KE, KQ + 2><<<grid_for(total, 256), 256, smem, st>>>(in, R01, DG, cnt, x->logn, P, dmc,
+                                                                                  x->d_fallbacks);
+    }
     else
       rescale_kernel<KQ, KE, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, R01, DG, cnt, x->logn, P, dmc,
                                                                            x->d_fallbacks);
-    FCN_LAUNCH_CHECK(x->fp ? "rescale_f64_kernel" : "rescale_kernel");
+    FCN_LAUNCH_CHECK(f64 ? "rescale_f64_kernel" : "rescale_kernel");
   }
   return FCN_OK;
 }

@@ -325,12 +325,6 @@ __device__ __forceinline__ void inv_ct(uint64_t* x, int s0, int o, const Twiddle
   }
 }
 
-__device__ __forceinline__ void cp_async8(uint64_t* smem_dst, const uint64_t* gsrc) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 template <int LOGN>
 __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
