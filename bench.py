@@ -125,6 +125,14 @@ def _peaks():
     return 6650.0, "fallback"
 
 
+def _fp64_peak():
+    p = os.path.join(REPO, "profiles", "fp64_peak.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f)
+
+
 def _int_peak():
     p = os.path.join(REPO, "profiles", "int_peak.json")
     if not os.path.exists(p):
@@ -438,15 +446,16 @@ def run_gpu(args, ws, rank, local):
     t_avg = (r["t_fwd_s"] + r["t_inv_s"]) / 2
     achieved = r["bytes"] / t_avg / 1e9
     tr = _profile_traffic(f"ntt_{args.workload}")
-    ip = _int_peak()
+    fp = _fp64_peak()
     bfly = r["rows"] * (r["n"] // 2) * (r["n"].bit_length() - 1)
-    int_roof = None
-    if ip:
+    fp_roof = None
+    if fp:
         ach = bfly / t_avg
-        int_roof = {"achieved_mulw_per_s": ach, "peak_mulw_per_s": ip["mulw_per_s"], "frac": ach / ip["mulw_per_s"],
-                    "peak_source": "profiles/int_peak.json (measured, tools/intpeak.cu)"}
+        fp_roof = {"achieved_butterflies_per_s": ach, "peak_butterflies_per_s": fp["butterfly_per_s"],
+                   "frac": ach / fp["butterfly_per_s"],
+                   "peak_source": "profiles/fp64_peak.json (measured register-resident FP64 butterfly, tools/fp64bench.cu)"}
     roofline = {
-        "kernel": "ntt_v2_fwd / ntt_v2_inv (batched negacyclic NTT, one CTA per row slot)",
+        "kernel": "ntt_f64_fwd / ntt_f64_inv (batched negacyclic NTT on the FP64 pipe, one CTA per row slot)",
         "bound": "hbm",
         "achieved": achieved,
         "peak": peak,
@@ -458,8 +467,9 @@ def run_gpu(args, ws, rank, local):
         "rows_per_launch": r["rows"],
         "ms_fwd": r["t_fwd_s"] * 1e3,
         "ms_inv": r["t_inv_s"] * 1e3,
-        "int_roofline": int_roof,
-        "note": "the NTT is integer-multiply bound on B200: one mulw per butterfly caps it near 48% of HBM at n=8192",
+        "fp64_roofline": fp_roof,
+        "note": "the NTT is FP64-pipe bound on B200 (one exact signed modmul = 5 DP ops + FRND per butterfly): "
+                "the register-resident butterfly ceiling is ~60% of the HBM roofline at n=8192",
     }
     hops = engine.plan_hops(comp, "batched", W.t).totals
     cpu = None

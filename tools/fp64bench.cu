@@ -50,6 +50,8 @@ __device__ __forceinline__ double redq(double x, double qi, double q) {
   return fma(-qt, q, x);
 }
 
+// 15 stages per iteration (three 5-stage register passes), values reduced
+// before every third stage -- the NTT kernel's schedule (ntt.cu, f64 family)
 template <int MAGIC>
 __global__ void __launch_bounds__(256, 2) k_bfly(double* out, const double2* __restrict__ tw, double q, int reps) {
   double x[32];
@@ -58,7 +60,12 @@ __global__ void __launch_bounds__(256, 2) k_bfly(double* out, const double2* __r
   const double qi = 1.0 / q;
   for (int r = 0; r < reps; ++r) {
 #pragma unroll
-    for (int u = 0; u < 5; ++u) {
+    for (int s = 0; s < 15; ++s) {
+      const int u = s % 5;
+      if (s > 0 && s % 3 == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[j] = redq(x[j], qi, q);
+      }
       const int h = 32 >> (u + 1);
 #pragma unroll
       for (int blk = 0; blk < (1 << u); ++blk) {
@@ -71,10 +78,6 @@ __global__ void __launch_bounds__(256, 2) k_bfly(double* out, const double2* __r
           x[j] = X + t;
           x[j + h] = X - t;
         }
-      }
-      if (u & 1) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) x[j] = redq(x[j], qi, q);
       }
     }
 #pragma unroll
@@ -126,7 +129,7 @@ int main() {
   cudaMalloc(&d, sizeof(h));
   cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice);
   for (int mg = 0; mg < 2; ++mg) {
-    const int br = 256;
+    const int br = 86;
     auto launch = [&] {
       if (mg) k_bfly<1><<<sms * 2, 256>>>(o, d, q, br);
       else k_bfly<0><<<sms * 2, 256>>>(o, d, q, br);
@@ -139,7 +142,7 @@ int main() {
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
-    const double bf = 5.0 * sms * 2 * 256.0 * br * 80;
+    const double bf = 5.0 * sms * 2 * 256.0 * br * 16 * 15;
     printf("fp64 butterfly (%s): %.3f T/s (%.2f per SM per clk)  err=%s\n", mg ? "magic" : "rint", bf / (ms * 1e-3) / 1e12,
            bf / (ms * 1e-3) / sms / 1.965e9, cudaGetErrorString(cudaGetLastError()));
   }
