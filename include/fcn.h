@@ -157,6 +157,18 @@ int fcn_mul_ct(const fcn_ctx* ctx, const fcn_keys* keys, int lane, const uint64_
                const uint64_t* d_b, uint64_t* d_out, int64_t count, void* d_workspace,
                size_t workspace_bytes, void* stream);
 
+/* fcn_mul_ct with an optional fused epilogue.  flags & FCN_MUL_ACT (squares
+ * only, d_b == NULL): out = act_c2 * a^2 + act_c1 * a (mod q), i.e. the
+ * reference's polynomial activation a2*x^2 + a1*x (engine.py:744-770:
+ * mul_ct, two mul_pt of constant plaintexts, add_ct) evaluated in the last
+ * kernel of the product;
+ * identical to fcn_mul_ct followed by fcn_linear_mac over [a^2 ; a] with the
+ * coefficients (act_c2, act_c1).  flags == 0: plain fcn_mul_ct.           */
+#define FCN_MUL_ACT 1
+int fcn_mul_ct_ex(const fcn_ctx* ctx, const fcn_keys* keys, int lane, const uint64_t* d_a,
+                  const uint64_t* d_b, uint64_t* d_out, int64_t count, int flags, int64_t act_c2,
+                  int64_t act_c1, void* d_workspace, size_t workspace_bytes, void* stream);
+
 /* fv.decrypt core (fv.py:337-353): given w = [c0 + c1 s]_q as RNS rows
  * [count][k][n], write m = floor((w t + q>>1)/q) mod t as [count][n].     */
 int fcn_decrypt_round(const fcn_ctx* ctx, int lane, const uint64_t* d_w, uint64_t* d_m, int64_t count,

@@ -273,10 +273,22 @@ inline uint64_t h_shoup(uint64_t w, uint64_t q) { return (uint64_t)(((unsigned _
 bool h_is_prime(uint64_t v);
 int bitlen64(uint64_t v);
 LimbConst make_limb_const(uint64_t q, int n, uint64_t ipsi1);
+// Inverse-NTT epilogue (row-aligned with the transformed rows, period/offset
+// limb indexing): mode 1: out = v + add; mode 2: out = c2 (v + add) + c1 lin;
+// mode 3: out = add + c2 v (mod q_l).  Coefficients per limb index: canonical u64 and FP64 {w, w/q}.
+constexpr int kEpiLimbs = 64;
+struct NttEpi {
+  int mode = 0;
+  const uint64_t* add = nullptr;
+  const uint64_t* lin = nullptr;
+  uint64_t* out = nullptr;
+  uint64_t c2[kEpiLimbs], c1[kEpiLimbs];
+  double fc2[kEpiLimbs], fc2q[kEpiLimbs], fc1[kEpiLimbs], fc1q[kEpiLimbs];
+};
 // Batched NTT over rows; the forward may read row r's input from
 // src + (r / src_div) * n (broadcast of one source row to several limbs).
 int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st,
-               const uint64_t* src = nullptr, int src_div = 1);
+               const uint64_t* src = nullptr, int src_div = 1, const NttEpi* epi = nullptr);
 
 inline int grid_for(int64_t work, int block, int max_blocks = 148 * 16) {
   int64_t g = (work + block - 1) / block;

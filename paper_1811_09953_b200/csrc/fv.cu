@@ -397,6 +397,9 @@ struct RescaleP {
   double fq[KQ], fqi[KQ];
   double frc[KQ][KE], frcq[KQ][KE];
   double fntp[KQ], fntpq[KQ];
+  // fused activation (FP64 path): R01 rows become c2 R + c1 lin (mod q_i)
+  int act;
+  double fc2[KQ], fc2q[KQ], fc1[KQ], fc1q[KQ];
 };
 
 // canonical x mod q for any x < 2^64 (approximate-quotient product by 1)
@@ -802,7 +805,7 @@ template <int KQ, int KE, int NW>
 __global__ void __launch_bounds__(256, 3)
     rescale_f64_kernel(const uint64_t* __restrict__ T_in, uint64_t* __restrict__ R01, uint64_t* __restrict__ DG, int64_t C,
                        int logn, const __grid_constant__ RescaleP<KQ, KE> P, const MulCtConst* __restrict__ cc,
-                       unsigned long long* __restrict__ fallbacks) {
+                       unsigned long long* __restrict__ fallbacks, const uint64_t* __restrict__ lin) {
   const int n = 1 << logn;
   constexpr int k = KQ, K = KE;  // exact-size instantiations only
   const int64_t total = (C * 3) << logn;
@@ -908,6 +911,15 @@ __global__ void __launch_bounds__(256, 3)
       }
     }
     if (p < 2) {
+      if (P.act) {
+#pragma unroll
+        for (int i = 0; i < KQ; ++i) {
+          const double qi = P.fq[i], qii = P.fqi[i];
+          const double a = u2f(lin[((ct * 2 + p) * k + i) * n + coef]);
+          const double s2 = fmulq(u2f(out[i]), P.fc2[i], P.fc2q[i], qi) + fmulq(a, P.fc1[i], P.fc1q[i], qi);
+          out[i] = f2u_canon(fredq(s2, qii, qi), qi);
+        }
+      }
 #pragma unroll
       for (int i = 0; i < KQ; ++i)
         if (i < k) R01[((ct * 2 + p) * k + i) * n + coef] = out[i];
@@ -1563,9 +1575,16 @@ static RescaleP<KQ, KE> make_rescale_params(const fcn_ctx* x, const MulCtConst& 
   return P;
 }
 
+struct ActArgs {
+  bool on = false;
+  int64_t c2 = 1, c1 = 0;
+  const uint64_t* lin = nullptr;
+  bool applied = false;  // set when the rescale kernel folded it into R01
+};
+
 template <int KQ, int KE>
 static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t* in, uint64_t* out, int64_t cnt,
-                            uint64_t* R01, uint64_t* DG, cudaStream_t st) {
+                            uint64_t* R01, uint64_t* DG, cudaStream_t st, ActArgs* act) {
   const bool f64 = x->fp && x->k == KQ && x->k + x->m == KE;  // FP64 kernels: exact sizes
   const MulCtConst& mc = x->host_mc[lane];
   const MulCtConst* dmc = x->d_mc + lane;
@@ -1580,7 +1599,21 @@ static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_
                                                                              x->d_fallbacks);
     FCN_LAUNCH_CHECK(f64 ? "lift_f64_kernel" : "lift_kernel");
   } else {
-    const RescaleP<KQ, KE> P = make_rescale_params<KQ, KE>(x, mc);
+    RescaleP<KQ, KE> P = make_rescale_params<KQ, KE>(x, mc);
+    if (f64 && act && act->on) {
+      P.act = 1;
+      for (int i = 0; i < x->k; ++i) {
+        const int64_t qi = (int64_t)x->primes[i];
+        int64_t m2 = act->c2 % qi, m1 = act->c1 % qi;
+        if (m2 < 0) m2 += qi;
+        if (m1 < 0) m1 += qi;
+        P.fc2[i] = h_signed((uint64_t)m2, (uint64_t)qi);
+        P.fc2q[i] = P.fc2[i] / (double)qi;
+        P.fc1[i] = h_signed((uint64_t)m1, (uint64_t)qi);
+        P.fc1q[i] = P.fc1[i] / (double)qi;
+      }
+      act->applied = true;
+    }
     const int64_t total = (cnt * 3) << x->logn;  // cnt = ciphertexts
     if (f64) {
       const int smem = 2 * KE * 256 * 8;
@@ -1589,7 +1622,7 @@ static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_
         cudaFuncSetAttribute(rescale_f64_kernel<KQ, KE, KQ + 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       });
       rescale_f64_kernel<KQ, KE, KQ + 2><<<grid_for(total, 256), 256, smem, st>>>(in, R01, DG, cnt, x->logn, P, dmc,
-                                                                                  x->d_fallbacks);
+                                                                                  x->d_fallbacks, act ? act->lin : nullptr);
     }
     else
       rescale_kernel<KQ, KE, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, R01, DG, cnt, x->logn, P, dmc,
@@ -1600,10 +1633,10 @@ static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_
 }
 
 static int lift_or_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t* in, uint64_t* out, int64_t cnt,
-                           uint64_t* R01, uint64_t* DG, cudaStream_t st) {
+                           uint64_t* R01, uint64_t* DG, cudaStream_t st, ActArgs* act = nullptr) {
   const int k = x->k, m = x->m;
 #define FCN_TRY(KQ, KE) \
-  if (k <= KQ && m <= KE - KQ) return run_lift_rescale<KQ, KE>(lift, x, lane, in, out, cnt, R01, DG, st);
+  if (k <= KQ && m <= KE - KQ) return run_lift_rescale<KQ, KE>(lift, x, lane, in, out, cnt, R01, DG, st, act);
   FCN_TRY(2, 5)
   FCN_TRY(2, 6)
   FCN_TRY(3, 6)
@@ -1652,6 +1685,12 @@ static int launch_keymac(const uint64_t* DG, const fcn_keys* keys, uint64_t* ACC
 
 extern "C" int fcn_mul_ct(const fcn_ctx* x, const fcn_keys* keys, int lane, const uint64_t* d_a, const uint64_t* d_b,
                           uint64_t* d_out, int64_t count, void* d_workspace, size_t workspace_bytes, void* stream) {
+  return fcn_mul_ct_ex(x, keys, lane, d_a, d_b, d_out, count, 0, 1, 0, d_workspace, workspace_bytes, stream);
+}
+
+extern "C" int fcn_mul_ct_ex(const fcn_ctx* x, const fcn_keys* keys, int lane, const uint64_t* d_a, const uint64_t* d_b,
+                             uint64_t* d_out, int64_t count, int flags, int64_t act_c2, int64_t act_c1, void* d_workspace,
+                             size_t workspace_bytes, void* stream) {
   if (!x || !keys) return set_error(FCN_ERR_ARG, "null context or keys");
   if (lane < 0 || lane >= x->n_lanes) return set_error(FCN_ERR_ARG, "lane %d out of range", lane);
   if (count <= 0) return FCN_OK;
@@ -1666,6 +1705,19 @@ extern "C" int fcn_mul_ct(const fcn_ctx* x, const fcn_keys* keys, int lane, cons
   const int k = x->k, K = x->k + x->m, D = x->ell + 1, n = x->n, logn = x->logn;
   const bool direct = x->host_mc[lane].direct != 0;
   const int64_t ct_words = 2LL * k * n;
+  const bool act = (flags & FCN_MUL_ACT) != 0;
+  if (act && d_b) return set_error(FCN_ERR_ARG, "the activation epilogue applies to squares only (b must be null)");
+  NttEpi epi;
+  for (int l = 0; l < k; ++l) {
+    const uint64_t ql = x->primes[l];
+    const int64_t m2 = act_c2 % (int64_t)ql, m1 = act_c1 % (int64_t)ql;
+    epi.c2[l] = (uint64_t)(m2 < 0 ? m2 + (int64_t)ql : m2);
+    epi.c1[l] = (uint64_t)(m1 < 0 ? m1 + (int64_t)ql : m1);
+    epi.fc2[l] = h_signed(epi.c2[l], ql);
+    epi.fc2q[l] = epi.fc2[l] / (double)ql;
+    epi.fc1[l] = h_signed(epi.c1[l], ql);
+    epi.fc1q[l] = epi.fc1[l] / (double)ql;
+  }
   for (int64_t off = 0; off < count; off += chunk_max) {
     const int64_t C = (count - off) < chunk_max ? (count - off) : chunk_max;
     uint64_t* ws = (uint64_t*)d_workspace;
@@ -1696,9 +1748,15 @@ extern "C" int fcn_mul_ct(const fcn_ctx* x, const fcn_keys* keys, int lane, cons
     FCN_LAUNCH_CHECK(x->fp ? "tensor_f64_kernel" : "tensor_kernel");
     int rc = launch_ntt(x->ext, T, C * 3 * K, K, 0, false, st);
     if (rc) return rc;
-    // (iv) exact rescale + digit decomposition
-    rc = lift_or_rescale(false, x, lane, T, nullptr, C, R01, direct ? DGR : DGN, st);
+    // (iv) exact rescale + digit decomposition (FP64: R01 <- c2 R01 + c1 a for the activation)
+    ActArgs aa;
+    aa.on = act;
+    aa.c2 = act_c2;
+    aa.c1 = act_c1;
+    aa.lin = a;
+    rc = lift_or_rescale(false, x, lane, T, nullptr, C, R01, direct ? DGR : DGN, st, &aa);
     if (rc) return rc;
+    epi.mode = !act ? 1 : (aa.applied ? 3 : 2);
     // (v) digits to NTT (broadcast rows when digits are limb-independent), key MAC
     if (direct)
       rc = launch_ntt(x->ext, DGN, C * D * k, k, 0, true, st, DGR, k);
@@ -1707,12 +1765,13 @@ extern "C" int fcn_mul_ct(const fcn_ctx* x, const fcn_keys* keys, int lane, cons
     if (rc) return rc;
     rc = launch_keymac(DGN, keys, ACC, C, D, k, x, st);
     if (rc) return rc;
-    // (vi) inverse NTT + add
-    rc = launch_ntt(x->ext, ACC, C * 2 * k, k, 0, false, st);
+    // (vi) inverse NTT with the fused epilogue: out = R01 + INTT(ACC)
+    //      [ * c2 + c1 * a  when FCN_MUL_ACT: the a2 x^2 + a1 x activation]
+    epi.add = R01;
+    epi.lin = a;
+    epi.out = d_out + off * ct_words;
+    rc = launch_ntt(x->ext, ACC, C * 2 * k, k, 0, false, st, nullptr, 1, &epi);
     if (rc) return rc;
-    const int64_t tot = (C * 2 * k) << logn;
-    add_rows_kernel<<<grid_for(tot / 2, 256), 256, 0, st>>>(R01, ACC, d_out + off * ct_words, tot, logn, k, x->ext->d_lc);
-    FCN_LAUNCH_CHECK("add_rows_kernel");
   }
   return FCN_OK;
 }

@@ -702,6 +702,110 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
   cp_async_wait_all();
 }
 
+// Inverse with a fused epilogue out = add + v (SCALE: add + c2 v), out of
+// place.  The epilogue row `add` streams into shared memory with cp.async
+// during the last pass (each thread fetches exactly the residues it will
+// combine, so no barrier is needed); the next input row is prefetched into
+// registers instead (coalesced, as in the forward kernel).
+template <int LOGN, bool SCALE>
+__global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
+    ntt_f64_inv_epi(const uint64_t* __restrict__ data, int64_t n_rows, int period, int offset,
+                    const LimbConst* __restrict__ lcs, const double2* __restrict__ tws,
+                    const double2* __restrict__ twists, const __grid_constant__ NttEpi E) {
+  constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
+  extern __shared__ uint64_t sm[];
+  double* fs = reinterpret_cast<double*>(sm);
+  const int tid = threadIdx.x;
+  int64_t row = blockIdx.x;
+  if (row >= n_rows) return;
+  double x[32];  // raw u64 bits of the next row between iterations
+  {
+    const uint64_t* p = data + row * N;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
+  }
+  for (; row < n_rows; row += gridDim.x) {
+    const int limb = offset + (int)(row % period);
+    const LimbConst& c = lcs[limb];
+    const double q = c.fq, qi = c.fqi;
+    const double2* tw = tws + (int64_t)limb * N;
+    const double2* twist = twists + (int64_t)limb * N;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) sm[phys(tid + j * T)] = (uint64_t)__double_as_longlong(x[j]);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = u2f(sm[tid * 33 + j]);
+    inv_ctf<5, 0>(x, 0, tw, q, qi);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) fs[tid * 33 + j] = x[j];
+    __syncthreads();
+    if (RM > 0) {
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) {
+        const int g = tid + i * T;
+        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
+#pragma unroll
+        for (int j = 0; j < GM; ++j) x[i * GM + j] = fs[phys(base + j * 32)];
+      }
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) inv_ctf<(RM > 0 ? RM : 1), 5>(x + i * GM, (tid + i * T) & 31, tw, q, qi);
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) {
+        const int g = tid + i * T;
+        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
+#pragma unroll
+        for (int j = 0; j < GM; ++j) fs[phys(base + j * 32)] = x[i * GM + j];
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = fs[phys(tid + j * T)];
+    {
+      // own slots only: no barrier between these reads and the cp.async writes
+      const uint64_t* pa = E.add + row * N;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) cp_async8(&sm[phys(tid + j * T)], pa + tid + j * T);
+      cp_async_commit();
+    }
+    inv_ctf<5, LOGN - 5>(x, tid, tw, q, qi);
+    cp_async_wait_all();
+    uint64_t* po = E.out + row * N;
+    const double c2 = E.fc2[limb], c2q = E.fc2q[limb];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double2 w = ld_ftw(twist + tid + j * T);
+      double y = fredq(fmulq(x[j], w.x, w.y, q), qi, q);  // |y| <= q/2 + 1
+      if (SCALE) y = fmulq(y, c2, c2q, q);              // |y| < 0.7 q
+      po[tid + j * T] = f2u_canon(fredq(y + u2f(sm[phys(tid + j * T)]), qi, q), q);
+    }
+    const int64_t nxt = row + gridDim.x;
+    if (nxt < n_rows) {
+      const uint64_t* p = data + nxt * N;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
+    }
+  }
+}
+
+// Integer epilogue for the non-FP64 kernels, applied after the transform.
+__global__ void ntt_epi_kernel(const uint64_t* __restrict__ data, int64_t n_rows, int logn, int period, int offset,
+                               const LimbConst* __restrict__ lcs, const __grid_constant__ NttEpi E) {
+  const int64_t total = n_rows << logn;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int limb = offset + (int)((e >> logn) % period);
+    const LimbConst& c = lcs[limb];
+    uint64_t v = data[e];
+    if (E.mode == 3) {
+      v = addmod(E.add[e], mulmod(v, E.c2[limb], c), c.q);
+    } else {
+      v = addmod(v, E.add[e], c.q);
+      if (E.mode == 2) v = addmod(mulmod(v, E.c2[limb], c), mulmod(E.lin[e], E.c1[limb], c), c.q);
+    }
+    E.out[e] = v;
+  }
+}
+
 // ============================================================== dispatch
 
 static size_t v1_smem(int logs) { return (size_t)((1 << logs) + (1 << logs) / 32 + 2) * sizeof(uint64_t); }
@@ -716,9 +820,11 @@ template <int LOGN, bool FWD>
 static const void* v2_ptr() {
   return FWD ? (const void*)ntt_v2_fwd<LOGN> : (const void*)ntt_v2_inv<LOGN>;
 }
-template <int LOGN, bool FWD>
+template <int LOGN, bool FWD, int EPI = 0>
 static const void* f64_ptr() {
-  return FWD ? (const void*)ntt_f64_fwd<LOGN> : (const void*)ntt_f64_inv<LOGN>;
+  return FWD ? (const void*)ntt_f64_fwd<LOGN>
+             : (EPI == 0 ? (const void*)ntt_f64_inv<LOGN>
+                         : (EPI == 1 ? (const void*)ntt_f64_inv_epi<LOGN, false> : (const void*)ntt_f64_inv_epi<LOGN, true>));
 }
 
 static int g_sms = 0;
@@ -771,6 +877,16 @@ static void init_tables() {
       if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ffns[f][lg], (1 << lg) / 32, sm);
       if (e != cudaSuccess) g_init_err = e;
       g_f64[f][lg] = {ffns[f][lg], occ > 0 ? occ : 1};
+    }
+  }
+  {
+    const void* epis[10] = {f64_ptr<10, false, 1>(), f64_ptr<11, false, 1>(), f64_ptr<12, false, 1>(),
+                            f64_ptr<13, false, 1>(), f64_ptr<14, false, 1>(), f64_ptr<10, false, 2>(),
+                            f64_ptr<11, false, 2>(), f64_ptr<12, false, 2>(), f64_ptr<13, false, 2>(),
+                            f64_ptr<14, false, 2>()};
+    for (int i = 0; i < 10; ++i) {
+      cudaError_t e = cudaFuncSetAttribute(epis[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v2_smem(10 + i % 5));
+      if (e != cudaSuccess) g_init_err = e;
     }
   }
   const size_t mx = v1_smem(14);
@@ -832,20 +948,35 @@ static void launch_v2_t(bool fwd, int grid, uint64_t* d, int64_t n_rows, int per
 
 template <int LOGN>
 static void launch_f64_t(bool fwd, int grid, uint64_t* d, int64_t n_rows, int period, int offset, const fcn_ring* r,
-                         cudaStream_t st, const uint64_t* src, int src_div) {
+                         cudaStream_t st, const uint64_t* src, int src_div, const NttEpi* epi) {
   const size_t sm = v2_smem(LOGN);
   if (fwd)
     ntt_f64_fwd<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_ffwd, r->d_ffl, src,
                                                           src_div);
-  else
+  else if (!epi || epi->mode == 0)
     ntt_f64_inv<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict, r->d_ftwist);
+  else if (epi->mode == 1)
+    ntt_f64_inv_epi<LOGN, false><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict,
+                                                                     r->d_ftwist, *epi);
+  else
+    ntt_f64_inv_epi<LOGN, true><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict,
+                                                                    r->d_ftwist, *epi);
+}
+
+static int launch_epi_int(const fcn_ring* r, const uint64_t* d, int64_t n_rows, int period, int offset, cudaStream_t st,
+                          const NttEpi* epi) {
+  if (!epi || epi->mode == 0) return FCN_OK;
+  ntt_epi_kernel<<<grid_for(n_rows << r->logn, 256), 256, 0, st>>>(d, n_rows, r->logn, period, offset, r->d_lc, *epi);
+  FCN_LAUNCH_CHECK("ntt_epi_kernel");
+  return FCN_OK;
 }
 
 static int g_force_int = -1;  // FCN_NTT_INT=1 selects the integer kernels (A/B tests)
 
 int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st,
-               const uint64_t* src, int src_div) {
+               const uint64_t* src, int src_div, const NttEpi* epi) {
   if (n_rows <= 0) return FCN_OK;
+  if (fwd) epi = nullptr;
   if (!src) {
     src = d;
     src_div = 1;
@@ -859,23 +990,30 @@ int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int o
     const uint64_t q = r->primes[offset + l];
     v2 = q >= (1ull << 34) && q < (1ull << 56);
   }
-  if (!v2) return launch_v1(r, d, n_rows, period, offset, fwd, st, src, src_div);
+  if (!v2) {
+    const int rc = launch_v1(r, d, n_rows, period, offset, fwd, st, src, src_div);
+    return rc ? rc : launch_epi_int(r, d, n_rows, period, offset, st, epi);
+  }
   if (g_force_int < 0) {
     const char* ev = getenv("FCN_NTT_INT");
     g_force_int = (ev && ev[0] == '1') ? 1 : 0;
   }
   bool f64 = !g_force_int && r->d_ffwd;
   for (int l = 0; f64 && l < period; ++l) f64 = r->primes[offset + l] < (1ull << 51);
+  if (f64 && epi && epi->mode == 2) {  // no fused FP64 form: plain inverse, then the integer epilogue
+    const int rc = launch_ntt(r, d, n_rows, period, offset, false, st);
+    return rc ? rc : launch_epi_int(r, d, n_rows, period, offset, st, epi);
+  }
   if (f64) {
     const V2Entry& e = g_f64[fwd ? 1 : 0][logn];
     int64_t grid = (int64_t)g_sms * e.ctas_per_sm;
     if (grid > n_rows) grid = n_rows;
     switch (logn) {
-      case 10: launch_f64_t<10>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div); break;
-      case 11: launch_f64_t<11>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div); break;
-      case 12: launch_f64_t<12>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div); break;
-      case 13: launch_f64_t<13>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div); break;
-      default: launch_f64_t<14>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div); break;
+      case 10: launch_f64_t<10>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div, epi); break;
+      case 11: launch_f64_t<11>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div, epi); break;
+      case 12: launch_f64_t<12>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div, epi); break;
+      case 13: launch_f64_t<13>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div, epi); break;
+      default: launch_f64_t<14>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div, epi); break;
     }
     FCN_LAUNCH_CHECK(fwd ? "ntt_f64_fwd" : "ntt_f64_inv");
     return FCN_OK;
@@ -891,7 +1029,7 @@ int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int o
     default: launch_v2_t<14>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div); break;
   }
   FCN_LAUNCH_CHECK(fwd ? "ntt_v2_fwd" : "ntt_v2_inv");
-  return FCN_OK;
+  return launch_epi_int(r, d, n_rows, period, offset, st, epi);
 }
 
 }  // namespace fcn

@@ -560,11 +560,28 @@ def _layer_range(params, lane, ek, plan, lw, cur, lo: int, hi: int, encoding: st
         _run_bias(params, lane, out, _bias_range(bias, lo, hi, id(plan)))
         return out
     x = cur if cur.shape[0] == hi - lo else cur[lo:hi]
-    sq = fv.mul_ct_batch(params, ek, lane, x, None, chunk=mul_chunk)
     mac, bias, identity = _act_lowered(plan, t, params.n, encoding, hi - lo)
-    out = sq if identity else _mac_out(params, mac, sq, x)
+    fused = _act_scalars(plan, t, params.n, encoding)
+    if fused is not None and not identity:
+        # a2 x^2 + a1 x with constant plaintexts: one fused product epilogue
+        out = fv.mul_ct_batch(params, ek, lane, x, None, chunk=mul_chunk, act=fused)
+    else:
+        sq = fv.mul_ct_batch(params, ek, lane, x, None, chunk=mul_chunk)
+        out = sq if identity else _mac_out(params, mac, sq, x)
     _run_bias(params, lane, out, bias)
     return out
+
+
+def _act_scalars(plan, t: int, n: int, encoding: str):
+    """(c2, c1) when the activation's MAC is c2*sq[o] + c1*x[o] with constant
+    (rotation-0) multipliers -- the batched encoding -- else None."""
+    if encoding != "batched":
+        return None
+    a2 = [(0, 1)] if plan.a2_int is None else const_terms(plan.a2_int, t, n, encoding)
+    a1 = [(0, 0)] if plan.a1_mult_int is None else const_terms(plan.a1_mult_int, t, n, encoding)
+    if len(a2) != 1 or len(a1) != 1 or a2[0][0] != 0 or a1[0][0] != 0:
+        return None
+    return a2[0][1], a1[0][1]
 
 
 def _meta_step(plan, lw, depths, scales, scale, factor, prec):

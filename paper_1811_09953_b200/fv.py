@@ -492,25 +492,35 @@ def mul_ct_workspace(params: EncryptionParams, chunk: int):
     return dev.empty(((nbytes + 7) // 8,))
 
 
-def mul_ct_batch(params: EncryptionParams, ek: EvalKeys, lane: int, a, b=None, out=None, chunk: int | None = None, workspace=None):
-    """Relinearised products of [B][2][k][n] buffers (b=None: squares)."""
+MUL_CT_WORKSPACE_CAP = 12 << 30  # default scratch cap per call (bytes)
+
+
+def mul_ct_batch(params: EncryptionParams, ek: EvalKeys, lane: int, a, b=None, out=None, chunk: int | None = None,
+                 workspace=None, act: tuple | None = None):
+    """Relinearised products of [B][2][k][n] buffers (b=None: squares).
+
+    act=(c2, c1): fused activation epilogue, out = c2*a^2 + c1*a (mod q)
+    (squares only; fcn_mul_ct_ex, include/fcn.h)."""
     B = a.shape[0]
     if out is None:
         out = dev.empty(a.shape)
     if B == 0:
         return out
+    if act is not None and b is not None:
+        raise FVError("the activation epilogue applies to squares only")
     h = params.native()
     kh = ek.native(params)
     if workspace is None:
         per = _lib.lib().fcn_mul_ct_workspace_bytes(h.ptr, 1)
         if chunk is None:
-            chunk = max(1, min(B, (4 << 30) // max(1, per)))
+            chunk = max(1, min(B, MUL_CT_WORKSPACE_CAP // max(1, per)))
         workspace = mul_ct_workspace(params, chunk)
     nbytes = workspace.numel() * 8
+    flags, c2, c1 = (0, 1, 0) if act is None else (1, int(act[0]), int(act[1]))
     _lib.check(
-        _lib.lib().fcn_mul_ct(
-            h.ptr, kh.ptr, lane, a.data_ptr(), b.data_ptr() if b is not None else None, out.data_ptr(), B, workspace.data_ptr(), nbytes,
-            dev.stream_ptr(),
+        _lib.lib().fcn_mul_ct_ex(
+            h.ptr, kh.ptr, lane, a.data_ptr(), b.data_ptr() if b is not None else None, out.data_ptr(), B, flags, c2, c1,
+            workspace.data_ptr(), nbytes, dev.stream_ptr(),
         ),
         FVError,
     )

@@ -148,6 +148,33 @@ def test_config_shape_square_vs_oracle(F, cfg):
         assert np.array_equal(out[b], np.stack([want.c0, want.c1]))
 
 
+@pytest.mark.parametrize("primes", [(36028797018972161, 36028797018990593), (1125899906826241, 1125899906820097)],
+                         ids=["int64-55bit", "fp64-50bit"])
+@pytest.mark.parametrize("c2,c1", [(1, 0), (-3, 5), (64, -1), (12345, -32768)])
+def test_fused_activation_epilogue(F, primes, c2, c1):
+    """mul_ct_batch(act=(c2, c1)) == c2 * mul_ct(x, x) + c1 * x (mod q_i),
+    bit-exact, on the FP64 and the integer kernel families."""
+    from oracle import rns as orn
+    from paper_1811_09953_b200 import device as dev
+
+    n = 1024
+    P = F.EncryptionParams(n, primes, (65537,))
+    OP = ob.Params(n, primes, P.t_lanes, P.beta)
+    sk, pk, ek = F.keygen(P, 5)
+    K = ob.keygen(OP, 5)
+    rng = np.random.default_rng(3)
+    B = 4
+    x = np.stack([np.stack([orn.random_uniform(primes, n, rng) for _ in range(2)]) for _ in range(B)])
+    got = dev.to_host(F.mul_ct_batch(P, ek, 0, dev.to_device(x), act=(c2, c1), chunk=3))
+    for b in range(B):
+        c = ob.Ct(x[b, 0], x[b, 1])
+        sq = ob.mul_ct(OP, c, c, K)
+        for p_i, (pa, xa) in enumerate(zip((sq.c0, sq.c1), (x[b, 0], x[b, 1]))):
+            for l, q in enumerate(primes):
+                want = (pa[l].astype(object) * (c2 % q) + xa[l].astype(object) * (c1 % q)) % q
+                assert np.array_equal(got[b, p_i, l].astype(object), want), (b, p_i, l)
+
+
 def test_general_product_and_batch_chunking(F, golden_meta, golden_npz):
     """a*b with distinct operands, across several workspace chunks."""
     from oracle import rns as orn
