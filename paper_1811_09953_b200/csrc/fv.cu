@@ -815,13 +815,23 @@ __global__ void __launch_bounds__(256, 3)
   // the next coefficient are in flight while this one computes, without
   // holding registers (coalesced: consecutive threads, consecutive words)
   extern __shared__ uint64_t stage_buf[];
+  constexpr int SL = KE + KQ;  // staged words per coefficient: K tensor residues (+ k activation inputs)
   const int tid = threadIdx.x, T = blockDim.x;
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e < total) {
+  const bool act = P.act != 0;
+  auto stage = [&](int64_t ee, uint64_t* buf) {
+    const int64_t cpp = ee >> logn;
+    const int cf = (int)(ee & (n - 1));
 #pragma unroll
-    for (int j = 0; j < KE; ++j)
-      if (j < K) cp_async8(&stage_buf[j * T + tid], &T_in[((e >> logn) * K + j) * n + (e & (n - 1))]);
-  }
+    for (int j = 0; j < KE; ++j) cp_async8(&buf[j * T + tid], &T_in[(cpp * K + j) * n + cf]);
+    const int pp = (int)(cpp % 3);
+    if (act && pp < 2) {
+      const int64_t ctt = cpp / 3;
+#pragma unroll
+      for (int i = 0; i < KQ; ++i) cp_async8(&buf[(KE + i) * T + tid], &lin[((ctt * 2 + pp) * k + i) * n + cf]);
+    }
+  };
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < total) stage(e, stage_buf);
   cp_async_commit();
   int sb = 0;
   for (; e < total; e += stride) {
@@ -829,19 +839,13 @@ __global__ void __launch_bounds__(256, 3)
     const int coef = (int)(e & (n - 1));
     const int64_t ct = cp / 3;
     const int p = (int)(cp % 3);
-    if (e + stride < total) {
-      const int64_t e2 = e + stride;
-      uint64_t* nb = stage_buf + (sb ^ 1) * KE * T;
-#pragma unroll
-      for (int j = 0; j < KE; ++j)
-        if (j < K) cp_async8(&nb[j * T + tid], &T_in[((e2 >> logn) * K + j) * n + (e2 & (n - 1))]);
-    }
+    if (e + stride < total) stage(e + stride, stage_buf + (sb ^ 1) * SL * T);
     cp_async_commit();
     cp_async_wait<1>();
     uint64_t cur[KE];
-    const uint64_t* cb = stage_buf + sb * KE * T;
+    const uint64_t* cb = stage_buf + sb * SL * T;
 #pragma unroll
-    for (int j = 0; j < KE; ++j) cur[j] = j < K ? cb[j * T + tid] : 0;
+    for (int j = 0; j < KE; ++j) cur[j] = cb[j * T + tid];
     sb ^= 1;
     double y[KE];
     double fv = 0.0;
@@ -915,7 +919,7 @@ __global__ void __launch_bounds__(256, 3)
 #pragma unroll
         for (int i = 0; i < KQ; ++i) {
           const double qi = P.fq[i], qii = P.fqi[i];
-          const double a = u2f(lin[((ct * 2 + p) * k + i) * n + coef]);
+          const double a = u2f(cb[(KE + i) * T + tid]);
           const double s2 = fmulq(u2f(out[i]), P.fc2[i], P.fc2q[i], qi) + fmulq(a, P.fc1[i], P.fc1q[i], qi);
           out[i] = f2u_canon(fredq(s2, qii, qi), qi);
         }
@@ -1616,7 +1620,7 @@ static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_
     }
     const int64_t total = (cnt * 3) << x->logn;  // cnt = ciphertexts
     if (f64) {
-      const int smem = 2 * KE * 256 * 8;
+      const int smem = 2 * (KE + KQ) * 256 * 8;
       static std::once_flag once;
       std::call_once(once, [&] {
         cudaFuncSetAttribute(rescale_f64_kernel<KQ, KE, KQ + 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
