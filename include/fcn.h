@@ -146,6 +146,18 @@ int fcn_linear_mac_ex(const fcn_ctx* ctx, const uint64_t* d_in0, int64_t n_in0, 
                       const int64_t* d_coef, uint64_t* d_out, int64_t n_out, int no_rot, uint64_t max_abs_coef,
                       void* stream);
 
+/* Output fan-out (sharded evaluation): the kernel's final
+ * store writes the same n_out ciphertexts to each of the n_dst (1..8)
+ * destinations -- this GPU's buffer and the peers' buffers mapped over
+ * NVLink (torch symmetric memory) -- so the per-stage all-gather
+ * (engine.py:682-690 merges independent outputs) happens inside the layer
+ * kernel.  d_outs is a HOST array of device pointers.                     */
+#define FCN_MAX_FANOUT 8
+int fcn_linear_mac_multi(const fcn_ctx* ctx, const uint64_t* d_in0, int64_t n_in0, const uint64_t* d_in1,
+                         int64_t n_in1, const int32_t* d_rowptr, const int32_t* d_col, const int32_t* d_rot,
+                         const int64_t* d_coef, uint64_t* const* d_outs, int n_dst, int64_t n_out, int no_rot,
+                         uint64_t max_abs_coef, void* stream);
+
 /* fv.mul_ct (fv.py:498-549): exact tensor in the extended base, exact
  * floor((t*T + q>>1)/q) mod q, base-beta digits of c2', key switching.
  * d_b == NULL computes the square a*a.  `count` ciphertexts [count][2][k][n].
@@ -168,6 +180,10 @@ int fcn_mul_ct(const fcn_ctx* ctx, const fcn_keys* keys, int lane, const uint64_
 int fcn_mul_ct_ex(const fcn_ctx* ctx, const fcn_keys* keys, int lane, const uint64_t* d_a,
                   const uint64_t* d_b, uint64_t* d_out, int64_t count, int flags, int64_t act_c2,
                   int64_t act_c1, void* d_workspace, size_t workspace_bytes, void* stream);
+/* fcn_mul_ct_ex with output fan-out to n_dst destinations (see above).   */
+int fcn_mul_ct_multi(const fcn_ctx* ctx, const fcn_keys* keys, int lane, const uint64_t* d_a,
+                     const uint64_t* d_b, uint64_t* const* d_outs, int n_dst, int64_t count, int flags,
+                     int64_t act_c2, int64_t act_c1, void* d_workspace, size_t workspace_bytes, void* stream);
 
 /* fv.decrypt core (fv.py:337-353): given w = [c0 + c1 s]_q as RNS rows
  * [count][k][n], write m = floor((w t + q>>1)/q) mod t as [count][n].     */

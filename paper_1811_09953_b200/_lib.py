@@ -64,9 +64,11 @@ SIGNATURES = {
     "fcn_add_plain_terms": (_I, [_P, _I, _P, _I64, _P, _P, _P, _P]),
     "fcn_linear_mac": (_I, [_P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _I64, _P]),
     "fcn_linear_mac_ex": (_I, [_P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _I64, _I, C.c_uint64, _P]),
+    "fcn_linear_mac_multi": (_I, [_P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _I, _I64, _I, C.c_uint64, _P]),
     "fcn_mul_ct_workspace_bytes": (C.c_size_t, [_P, _I64]),
     "fcn_mul_ct": (_I, [_P, _P, _I, _P, _P, _P, _I64, _P, C.c_size_t, _P]),
     "fcn_mul_ct_ex": (_I, [_P, _P, _I, _P, _P, _P, _I64, _I, _I64, _I64, _P, C.c_size_t, _P]),
+    "fcn_mul_ct_multi": (_I, [_P, _P, _I, _P, _P, _P, _I, _I64, _I, _I64, _I64, _P, C.c_size_t, _P]),
     "fcn_decrypt_round": (_I, [_P, _I, _P, _P, _I64, _P]),
 }
 
@@ -104,6 +106,12 @@ def check(rc: int, exc_type=None):
     if exc_type is not None and rc in (FCN_ERR_ARG, FCN_ERR_PARAM):
         raise exc_type(msg)
     raise FcnError(rc, msg)
+
+
+def ptr_array(ptrs):
+    """Host array of device pointers (uint64_t* const*) for the fan-out entry points."""
+    arr = (C.c_void_p * len(ptrs))(*[int(p) for p in ptrs])
+    return arr
 
 
 def u64_array(values):

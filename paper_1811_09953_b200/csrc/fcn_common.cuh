@@ -273,6 +273,14 @@ inline uint64_t h_shoup(uint64_t w, uint64_t q) { return (uint64_t)(((unsigned _
 bool h_is_prime(uint64_t v);
 int bitlen64(uint64_t v);
 LimbConst make_limb_const(uint64_t q, int n, uint64_t ipsi1);
+// Output fan-out: the final store of a kernel goes to every destination
+// (this GPU's buffer and, for sharded evaluation, the peers' buffers mapped
+// over NVLink), replacing the all-gather that would otherwise follow.
+constexpr int kMaxFanout = 8;
+struct Fanout {
+  int n = 0;
+  uint64_t* dst[kMaxFanout] = {};
+};
 // Inverse-NTT epilogue (row-aligned with the transformed rows, period/offset
 // limb indexing): mode 1: out = v + add; mode 2: out = c2 (v + add) + c1 lin;
 // mode 3: out = add + c2 v (mod q_l).  Coefficients per limb index: canonical u64 and FP64 {w, w/q}.
@@ -281,7 +289,7 @@ struct NttEpi {
   int mode = 0;
   const uint64_t* add = nullptr;
   const uint64_t* lin = nullptr;
-  uint64_t* out = nullptr;
+  Fanout out;  // destinations, row-aligned
   uint64_t c2[kEpiLimbs], c1[kEpiLimbs];
   double fc2[kEpiLimbs], fc2q[kEpiLimbs], fc1[kEpiLimbs], fc1q[kEpiLimbs];
 };

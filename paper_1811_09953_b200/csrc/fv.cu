@@ -232,7 +232,7 @@ __global__ void add_plain_kernel(uint64_t* __restrict__ cts, int64_t n_terms, co
 __global__ void __launch_bounds__(256) mac_kernel(const uint64_t* __restrict__ in0, int64_t n_in0,
                                                   const uint64_t* __restrict__ in1, const int32_t* __restrict__ rowptr,
                                                   const int32_t* __restrict__ col, const int32_t* __restrict__ rot,
-                                                  const int64_t* __restrict__ coef, uint64_t* __restrict__ out,
+                                                  const int64_t* __restrict__ coef, const __grid_constant__ Fanout F,
                                                   int logn, int k, const LimbConst* __restrict__ lcs) {
   const int n = 1 << logn;
   const int o = blockIdx.y;
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(256) mac_kernel(const uint64_t* __restrict__ i
   ulonglong2 res;
   res.x = submod(reduce128(ph0, pl0, c), reduce128(nh0, nl0, c), c.q);
   res.y = submod(reduce128(ph1, pl1, c), reduce128(nh1, nl1, c), c.q);
-  *reinterpret_cast<ulonglong2*>(out + (int64_t)o * ct_words + (int64_t)r * n + j0) = res;
+  for (int d = 0; d < F.n; ++d) *reinterpret_cast<ulonglong2*>(F.dst[d] + (int64_t)o * ct_words + (int64_t)r * n + j0) = res;
 }
 
 // Fast path: all rotations 0 (constant plaintexts) and max|coef| * q small
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restric
                                                        const uint64_t* __restrict__ in1,
                                                        const int32_t* __restrict__ rowptr,
                                                        const int32_t* __restrict__ col,
-                                                       const int64_t* __restrict__ coef, uint64_t* __restrict__ out,
+                                                       const int64_t* __restrict__ coef, const __grid_constant__ Fanout F,
                                                        int logn, int k, const LimbConst* __restrict__ lcs, int fold) {
   const int n = 1 << logn;
   const int o = blockIdx.y;
@@ -357,9 +357,11 @@ __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restric
     const uint64_t b = csub(csub(mulw(neg[v], 1, one_s, nq), 2 * q), q);
     res[v] = submod(a, b, q);
   }
-  uint64_t* dst = out + (int64_t)o * ct_words + (int64_t)r * n + j0;
-  *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(res[0], res[1]);
-  *reinterpret_cast<ulonglong2*>(dst + 2) = make_ulonglong2(res[2], res[3]);
+  for (int d = 0; d < F.n; ++d) {
+    uint64_t* dst = F.dst[d] + (int64_t)o * ct_words + (int64_t)r * n + j0;
+    *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(res[0], res[1]);
+    *reinterpret_cast<ulonglong2*>(dst + 2) = make_ulonglong2(res[2], res[3]);
+  }
 }
 
 // ------------------------------------------------------------- mul_ct
@@ -1436,10 +1438,25 @@ extern "C" int fcn_linear_mac_ex(const fcn_ctx* x, const uint64_t* d_in0, int64_
                                  int64_t n_in1, const int32_t* d_rowptr, const int32_t* d_col, const int32_t* d_rot,
                                  const int64_t* d_coef, uint64_t* d_out, int64_t n_out, int no_rot, uint64_t max_abs_coef,
                                  void* stream) {
+  uint64_t* outs[1] = {d_out};
+  return fcn_linear_mac_multi(x, d_in0, n_in0, d_in1, n_in1, d_rowptr, d_col, d_rot, d_coef, outs, 1, n_out, no_rot,
+                              max_abs_coef, stream);
+}
+
+extern "C" int fcn_linear_mac_multi(const fcn_ctx* x, const uint64_t* d_in0, int64_t n_in0, const uint64_t* d_in1,
+                                    int64_t n_in1, const int32_t* d_rowptr, const int32_t* d_col, const int32_t* d_rot,
+                                    const int64_t* d_coef, uint64_t* const* d_outs, int n_dst, int64_t n_out, int no_rot,
+                                    uint64_t max_abs_coef, void* stream) {
   if (!x) return set_error(FCN_ERR_ARG, "null context");
   if (n_out <= 0) return FCN_OK;
-  if (!d_out || !d_rowptr || (n_in0 > 0 && !d_in0) || (n_in1 > 0 && !d_in1))
-    return set_error(FCN_ERR_ARG, "null argument");
+  if (n_dst < 1 || n_dst > kMaxFanout || !d_outs) return set_error(FCN_ERR_ARG, "1..%d destinations", kMaxFanout);
+  Fanout F;
+  F.n = n_dst;
+  for (int d = 0; d < n_dst; ++d) {
+    if (!d_outs[d]) return set_error(FCN_ERR_ARG, "null destination %d", d);
+    F.dst[d] = d_outs[d];
+  }
+  if (!d_rowptr || (n_in0 > 0 && !d_in0) || (n_in1 > 0 && !d_in1)) return set_error(FCN_ERR_ARG, "null argument");
   if (n_out > 65535) return set_error(FCN_ERR_ARG, "at most 65535 outputs per launch");
   DeviceGuard g(x->device);
   const int threads = 256;
@@ -1456,14 +1473,14 @@ extern "C" int fcn_linear_mac_ex(const fcn_ctx* x, const uint64_t* d_in0, int64_
   if (fold >= 2 && x->n >= 4) {
     const int per_cta = threads * 4;
     dim3 grid((x->n + per_cta - 1) / per_cta, (unsigned)n_out, 2 * x->k);
-    mac_fast_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_coef, d_out,
+    mac_fast_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_coef, F,
                                                                x->logn, x->k, x->ext->d_lc, fold);
     FCN_LAUNCH_CHECK("mac_fast_kernel");
     return FCN_OK;
   }
   const int per_cta = threads * 2;
   dim3 grid((x->n + per_cta - 1) / per_cta, (unsigned)n_out, 2 * x->k);
-  mac_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_rot, d_coef, d_out, x->logn,
+  mac_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_rot, d_coef, F, x->logn,
                                                          x->k, x->ext->d_lc);
   FCN_LAUNCH_CHECK("mac_kernel");
   return FCN_OK;
@@ -1695,11 +1712,22 @@ extern "C" int fcn_mul_ct(const fcn_ctx* x, const fcn_keys* keys, int lane, cons
 extern "C" int fcn_mul_ct_ex(const fcn_ctx* x, const fcn_keys* keys, int lane, const uint64_t* d_a, const uint64_t* d_b,
                              uint64_t* d_out, int64_t count, int flags, int64_t act_c2, int64_t act_c1, void* d_workspace,
                              size_t workspace_bytes, void* stream) {
+  uint64_t* outs[1] = {d_out};
+  return fcn_mul_ct_multi(x, keys, lane, d_a, d_b, outs, 1, count, flags, act_c2, act_c1, d_workspace, workspace_bytes,
+                          stream);
+}
+
+extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane, const uint64_t* d_a, const uint64_t* d_b,
+                                uint64_t* const* d_outs, int n_dst, int64_t count, int flags, int64_t act_c2,
+                                int64_t act_c1, void* d_workspace, size_t workspace_bytes, void* stream) {
+  if (n_dst < 1 || n_dst > kMaxFanout || !d_outs) return set_error(FCN_ERR_ARG, "1..%d destinations", kMaxFanout);
+  for (int d = 0; d < n_dst; ++d)
+    if (!d_outs[d]) return set_error(FCN_ERR_ARG, "null destination %d", d);
   if (!x || !keys) return set_error(FCN_ERR_ARG, "null context or keys");
   if (lane < 0 || lane >= x->n_lanes) return set_error(FCN_ERR_ARG, "lane %d out of range", lane);
   if (count <= 0) return FCN_OK;
   if (x->ell + 1 > 32) return set_error(FCN_ERR_PARAM, "more than 32 decomposition digits");
-  if (!d_a || !d_out || !d_workspace) return set_error(FCN_ERR_ARG, "null buffer");
+  if (!d_a || !d_workspace) return set_error(FCN_ERR_ARG, "null buffer");
   if (keys->k != x->k || keys->n != x->n || keys->D != x->ell + 1) return set_error(FCN_ERR_ARG, "keys do not match context");
   const int64_t per = mulct_words_per_ct(x);
   const int64_t chunk_max = (int64_t)(workspace_bytes / 8) / per;
@@ -1773,7 +1801,8 @@ extern "C" int fcn_mul_ct_ex(const fcn_ctx* x, const fcn_keys* keys, int lane, c
     //      [ * c2 + c1 * a  when FCN_MUL_ACT: the a2 x^2 + a1 x activation]
     epi.add = R01;
     epi.lin = a;
-    epi.out = d_out + off * ct_words;
+    epi.out.n = n_dst;
+    for (int d = 0; d < n_dst; ++d) epi.out.dst[d] = d_outs[d] + off * ct_words;
     rc = launch_ntt(x->ext, ACC, C * 2 * k, k, 0, false, st, nullptr, 1, &epi);
     if (rc) return rc;
   }

@@ -770,14 +770,14 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     }
     inv_ctf<5, LOGN - 5>(x, tid, tw, q, qi);
     cp_async_wait_all();
-    uint64_t* po = E.out + row * N;
     const double c2 = E.fc2[limb], c2q = E.fc2q[limb];
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const double2 w = ld_ftw(twist + tid + j * T);
       double y = fredq(fmulq(x[j], w.x, w.y, q), qi, q);  // |y| <= q/2 + 1
       if (SCALE) y = fmulq(y, c2, c2q, q);              // |y| < 0.7 q
-      po[tid + j * T] = f2u_canon(fredq(y + u2f(sm[phys(tid + j * T)]), qi, q), q);
+      const uint64_t v = f2u_canon(fredq(y + u2f(sm[phys(tid + j * T)]), qi, q), q);
+      for (int d = 0; d < E.out.n; ++d) E.out.dst[d][row * N + tid + j * T] = v;
     }
     const int64_t nxt = row + gridDim.x;
     if (nxt < n_rows) {
@@ -802,7 +802,7 @@ __global__ void ntt_epi_kernel(const uint64_t* __restrict__ data, int64_t n_rows
       v = addmod(v, E.add[e], c.q);
       if (E.mode == 2) v = addmod(mulmod(v, E.c2[limb], c), mulmod(E.lin[e], E.c1[limb], c), c.q);
     }
-    E.out[e] = v;
+    for (int d = 0; d < E.out.n; ++d) E.out.dst[d][e] = v;
   }
 }
 

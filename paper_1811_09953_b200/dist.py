@@ -95,15 +95,9 @@ def _torch_gather(local, count: int, block: int, group=None):
     return full[:count].contiguous()
 
 
-def eval_encrypted_sharded(net, tensor, ek, cfg, encoding: str = "integer", group=None, mul_chunk=None):
-    """Same result as engine.eval_encrypted, computed across the ranks of `group`."""
-    import torch
-    import torch.distributed as dist
-
+def _prepare(net, tensor, cfg, encoding):
     from . import engine
 
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
     params, lane = tensor.params, tensor.lane
     t = int(params.t_lanes[lane])
     compiled = engine._compiled(net, cfg)
@@ -112,33 +106,145 @@ def eval_encrypted_sharded(net, tensor, ek, cfg, encoding: str = "integer", grou
     prec = cfg.precision_bits
     depths, scales = tensor.depths.copy(), tensor.scales.copy()
     scale, factor = tensor.scale_exponent, tensor.scale_factor
-    plans = compiled.plans
-    for p, lw in zip(plans, low):
+    for p, lw in zip(compiled.plans, low):
         depths, scales, scale, factor = engine._meta_step(p, lw, depths, scales, scale, factor, prec)
+    return compiled, counter, low, (depths, scales, scale, factor)
 
+
+def _stage(params, lane, ek, plans, low, st, cur, lo, hi, encoding, mul_chunk, out=None, fanout=()):
+    """Rows [lo, hi) of one stage; its last layer writes `out` (+ fan-out)."""
+    from . import engine
+
+    res = cur
+    for j, idx in enumerate(st):
+        last = j == len(st) - 1
+        res = engine._layer_range(params, lane, ek, plans[idx], low[idx], res if j else cur, lo, hi, encoding, mul_chunk,
+                                  out=out if last else None, fanout=fanout if last else ())
+    return res
+
+
+def _result(net, tensor, cfg, encoding, compiled, counter, meta, out, events):
+    from . import engine
+    from .netplan import TimedLayerCounts
+
+    for st, a, b in events:
+        for idx in st:
+            counter.layer_counts[idx] = TimedLayerCounts(counter.layer_counts[idx], (a, b, 1.0 / len(st)))
+    depths, scales, scale, factor = meta
+    res = engine.CipherTensor(compiled.out_shape, scale_exponent=scale, scale_factor=factor, buf=out,
+                              params=tensor.params, lane=tensor.lane, depths=depths, scales=scales)
+    return res, counter
+
+
+def eval_encrypted_sharded(net, tensor, ek, cfg, encoding: str = "integer", group=None, mul_chunk=None,
+                           transport: str = "nccl"):
+    """Same result as engine.eval_encrypted, computed across the ranks of `group`.
+
+    transport="nccl": each stage's block is all-gathered with NCCL.
+    transport="p2p": each stage's last kernel writes its block straight into
+    every rank's copy of the next layer's input (torch symmetric memory
+    mapped over NVLink; fcn_*_multi fan-out stores), followed by a
+    device-side barrier -- no separate collective on the data path."""
+    import torch
+    import torch.distributed as dist
+
+    if transport == "p2p":
+        return _eval_p2p(net, tensor, ek, cfg, encoding, group, mul_chunk)
+    if transport != "nccl":
+        raise ValueError(f"unknown transport {transport!r}")
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    params, lane = tensor.params, tensor.lane
+    compiled, counter, low, meta = _prepare(net, tensor, cfg, encoding)
+    plans = compiled.plans
     events = []
 
     def compute(st, cur, lo, hi):
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()
-        out = cur
-        for j, idx in enumerate(st):
-            plan, lw = plans[idx], low[idx]
-            if j == 0:
-                out = engine._layer_range(params, lane, ek, plan, lw, cur, lo, hi, encoding, mul_chunk)
-            else:  # activation on the rank's own block
-                out = engine._layer_range(params, lane, ek, plan, lw, out, lo, hi, encoding, mul_chunk)
+        out = _stage(params, lane, ek, plans, low, st, cur, lo, hi, encoding, mul_chunk)
         ev1.record()
         events.append((st, ev0, ev1))
         return out
 
     out = run_stages(plans, tensor.buf, rank, world, compute, lambda loc, c, b: _torch_gather(loc, c, b, group))
-    from .netplan import TimedLayerCounts
+    return _result(net, tensor, cfg, encoding, compiled, counter, meta, out, events)
 
-    for st, a, b in events:
-        for idx in st:
-            counter.layer_counts[idx] = TimedLayerCounts(counter.layer_counts[idx], (a, b, 1.0 / len(st)))
-    res = engine.CipherTensor(compiled.out_shape, scale_exponent=scale, scale_factor=factor, buf=out, params=params,
-                              lane=lane, depths=depths, scales=scales)
-    return res, counter
+
+def _max_rows(plans, world: int) -> int:
+    rows = 0
+    for st in stages(plans):
+        count = stage_outputs(plans[st[-1]])
+        block = partition(count, world)[0][1] - partition(count, world)[0][0]
+        rows = max(rows, block * world)
+    return max(rows, 1)
+
+
+def _eval_p2p(net, tensor, ek, cfg, encoding, group, mul_chunk):
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm
+
+    from . import device as dev
+    from . import engine
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if world > 8:
+        raise ValueError("fan-out transport supports up to 8 ranks (FCN_MAX_FANOUT)")
+    params, lane = tensor.params, tensor.lane
+    compiled, counter, low, meta = _prepare(net, tensor, cfg, encoding)
+    plans = compiled.plans
+    shape = (_max_rows(plans, world), 2, len(params.limb_primes), params.n)
+    gname = group.group_name if group is not None else dist.group.WORLD.group_name
+    bufs = [symm.empty(shape, dtype=torch.int64, device=torch.device("cuda", dev.current_device())) for _ in range(2)]
+    hdls = [symm.rendezvous(b, gname) for b in bufs]
+    rb = engine._row_bytes(params)
+    events = []
+    cur = tensor.buf
+    for s_i, st in enumerate(stages(plans)):
+        count = stage_outputs(plans[st[-1]])
+        lo, hi = partition(count, world)[rank]
+        dst, h = bufs[s_i % 2], hdls[s_i % 2]
+        peers = [int(h.buffer_ptrs[r]) + lo * rb for r in range(world) if r != rank]
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        if hi > lo:
+            _stage(params, lane, ek, plans, low, st, cur, lo, hi, encoding, mul_chunk, out=dst[lo:hi], fanout=peers)
+        h.barrier(channel=0)  # every rank's block has landed in every buffer
+        ev1.record()
+        events.append((st, ev0, ev1))
+        cur = dst[:count]
+    out = cur.clone()
+    torch.cuda.current_stream().synchronize()
+    return _result(net, tensor, cfg, encoding, compiled, counter, meta, out, events)
+
+
+def simulate_fanout(net, tensor, ek, cfg, encoding: str, world: int, mul_chunk=None):
+    """Single-GPU check of the fan-out schedule: the `world` ranks' stage
+    blocks are computed one after another (no rank ever waits on another)
+    and each writes its block into all `world` full buffers, exactly as
+    _eval_p2p does over NVLink.  Returns the per-rank final buffers."""
+    from . import device as dev
+    from . import engine
+
+    params, lane = tensor.params, tensor.lane
+    compiled, counter, low, meta = _prepare(net, tensor, cfg, encoding)
+    plans = compiled.plans
+    shape = (_max_rows(plans, world), 2, len(params.limb_primes), params.n)
+    bufs = [[dev.empty(shape) for _ in range(world)] for _ in range(2)]
+    rb = engine._row_bytes(params)
+    cur = [tensor.buf] * world
+    for s_i, st in enumerate(stages(plans)):
+        count = stage_outputs(plans[st[-1]])
+        dst = bufs[s_i % 2]
+        for rank in range(world):
+            lo, hi = partition(count, world)[rank]
+            if hi > lo:
+                peers = [dst[r].data_ptr() + lo * rb for r in range(world) if r != rank]
+                _stage(params, lane, ek, plans, low, st, cur[rank], lo, hi, encoding, mul_chunk, out=dst[rank][lo:hi],
+                       fanout=peers)
+        cur = [dst[r][:count] for r in range(world)]
+    return [c.clone() for c in cur]

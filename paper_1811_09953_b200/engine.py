@@ -11,9 +11,13 @@ HOP it issues one fused kernel per layer:
     becomes a signed monomial term c * x^r applied to an input ciphertext
     and accumulated exactly (mul_pt + add_ct chain, engine.py:698-743),
     then `fcn_add_plain_terms` for the bias (add_pt, engine.py:713-715);
-  * activation: `fcn_mul_ct` on all nodes (square + relinearisation), then
-    one `fcn_linear_mac` over [sq ; x] for a2*sq + a1*x, then add_pt(a0)
-    (engine.py:747-768).
+  * activation: `fcn_mul_ct_ex` on all nodes (square + relinearisation)
+    with a2*sq + a1*x fused into its last kernels when the multipliers are
+    constant plaintexts (batched encoding), else `fcn_mul_ct` followed by
+    one `fcn_linear_mac` over [sq ; x]; then add_pt(a0) (engine.py:744-770).
+
+Sharded evaluation (`dist.py`) passes extra destinations (`fanout`): the
+final kernel of a layer stores its rows into every rank's buffer.
 
 Plaintext constants are encoded as in the reference (`encoding="integer"`:
 base-2 encoder, a +-1 term per set bit at x^bit) or, for the SIMD-batched
@@ -26,6 +30,8 @@ from __future__ import annotations
 
 import time
 from dataclasses import dataclass, field
+
+import ctypes as C
 
 import numpy as np
 
@@ -463,41 +469,50 @@ def _lowered(compiled: CompiledNet, t: int, n: int, encoding: str):
 # ------------------------------------------------------------------ kernels
 
 
-def _run_mac(params, in0, in1, mac: _Mac, out):
+def _row_bytes(params) -> int:
+    return 2 * len(params.limb_primes) * params.n * 8
+
+
+def _run_mac(params, in0, in1, mac: _Mac, out, fanout=()):
+    """out rows (and the same rows at every fan-out pointer) = the MAC."""
     h = params.native()
     n_in0 = in0.shape[0]
     n_in1 = in1.shape[0] if in1 is not None else 0
+    ptrs = _lib.ptr_array([out.data_ptr()] + [int(p) for p in fanout])
     _lib.check(
-        _lib.lib().fcn_linear_mac_ex(
+        _lib.lib().fcn_linear_mac_multi(
             h.ptr, in0.data_ptr(), n_in0, in1.data_ptr() if in1 is not None else None, n_in1, mac.rowptr.data_ptr(),
-            mac.col.data_ptr(), mac.rot.data_ptr(), mac.coef.data_ptr(), out.data_ptr(), mac.n_out,
-            int(mac.no_rot), min(mac.max_abs_coef, (1 << 64) - 1), dev.stream_ptr(),
+            mac.col.data_ptr(), mac.rot.data_ptr(), mac.coef.data_ptr(), C.cast(ptrs, C.c_void_p), 1 + len(fanout),
+            mac.n_out, int(mac.no_rot), min(mac.max_abs_coef, (1 << 64) - 1), dev.stream_ptr(),
         ),
         FVError,
     )
 
 
-def _run_bias(params, lane, buf, bias: _Bias | None):
+def _run_bias(params, lane, buf, bias: _Bias | None, fanout=()):
     if bias is None:
         return
-    _lib.check(
-        _lib.lib().fcn_add_plain_terms(
-            params.native().ptr, lane, buf.data_ptr(), bias.n_terms, bias.ct_index.data_ptr(), bias.pos.data_ptr(),
-            bias.coef.data_ptr(), dev.stream_ptr(),
-        ),
-        FVError,
-    )
+    for ptr in [buf.data_ptr()] + [int(p) for p in fanout]:
+        _lib.check(
+            _lib.lib().fcn_add_plain_terms(
+                params.native().ptr, lane, ptr, bias.n_terms, bias.ct_index.data_ptr(), bias.pos.data_ptr(),
+                bias.coef.data_ptr(), dev.stream_ptr(),
+            ),
+            FVError,
+        )
 
 
-def _mac_out(params, mac: _Mac, in0, in1):
-    out = dev.empty((mac.n_out, 2, len(params.limb_primes), params.n))
+def _mac_out(params, mac: _Mac, in0, in1, out=None, fanout=()):
+    if out is None:
+        out = dev.empty((mac.n_out, 2, len(params.limb_primes), params.n))
+    rb = _row_bytes(params)
     for lo in range(0, mac.n_out, 65535):
         hi = min(mac.n_out, lo + 65535)
         if lo == 0 and hi == mac.n_out:
-            _run_mac(params, in0, in1, mac, out)
+            _run_mac(params, in0, in1, mac, out, fanout)
         else:  # split launches over output rows (grid.y limit)
             sub = _Mac(mac.rowptr[lo : hi + 1], mac.col, mac.rot, mac.coef, hi - lo, mac.n_terms, mac.no_rot, mac.max_abs_coef)
-            _run_mac(params, in0, in1, sub, out[lo:hi])
+            _run_mac(params, in0, in1, sub, out[lo:hi], [int(p) + lo * rb for p in fanout])
     return out
 
 
@@ -506,22 +521,26 @@ def _mac_out(params, mac: _Mac, in0, in1):
 _range_cache: dict = {}
 
 
-def _bias_range(bias: _Bias | None, lo: int, hi: int, key):
-    """Bias terms of outputs [lo, hi), re-indexed from 0 (cached per range)."""
+def _bias_range(bias: _Bias | None, lo: int, hi: int):
+    """Bias terms of outputs [lo, hi), re-indexed from 0 (cached per range).
+
+    Keyed by the lowered bias object itself (one per plan, encoding, t, n and
+    device), which the cache entry keeps alive so its id cannot be reused."""
     import torch
 
     if bias is None:
         return None
-    ck = ("bias", key, lo, hi)
+    ck = ("bias", id(bias), lo, hi)
     hit = _range_cache.get(ck)
-    if hit is None:
+    if hit is None or hit[0] is not bias:
         idx = bias.ct_index.cpu().numpy()
         sel = (idx >= lo) & (idx < hi)
         if not sel.any():
-            hit = (None,)
+            hit = (bias, None)
         else:
             d = bias.ct_index.device
             hit = (
+                bias,
                 _Bias(
                     torch.as_tensor(idx[sel] - lo, dtype=torch.int32, device=d),
                     bias.pos[torch.as_tensor(sel, device=d)].contiguous(),
@@ -530,7 +549,7 @@ def _bias_range(bias: _Bias | None, lo: int, hi: int, key):
                 ),
             )
         _range_cache[ck] = hit
-    return hit[0]
+    return hit[1]
 
 
 def _act_lowered(plan, t, n, encoding, m):
@@ -542,33 +561,38 @@ def _act_lowered(plan, t, n, encoding, m):
     return hit[1]
 
 
-def _layer_range(params, lane, ek, plan, lw, cur, lo: int, hi: int, encoding: str, mul_chunk=None):
+def _layer_range(params, lane, ek, plan, lw, cur, lo: int, hi: int, encoding: str, mul_chunk=None, out=None,
+                 fanout=()):
     """Outputs [lo, hi) of one compiled layer as a [hi-lo][2][k][n] buffer.
 
     `cur` holds every input of the layer (for an activation, its inputs
-    are the same rows as its outputs, so cur may also be just [lo, hi))."""
+    are the same rows as its outputs, so cur may also be just [lo, hi)).
+    `out` (optional) receives the rows; every pointer in `fanout` (device
+    addresses of row lo of other buffers, e.g. peers' buffers over NVLink)
+    receives the same rows from the layer's final kernel."""
     t = int(params.t_lanes[lane])
     kind = lw[0]
     if kind in ("linear", "pool"):
         mac, bias = lw[1], lw[2]
         if lo == 0 and hi == mac.n_out:
-            out = _mac_out(params, mac, cur, None)
-            _run_bias(params, lane, out, bias)
+            out = _mac_out(params, mac, cur, None, out, fanout)
+            _run_bias(params, lane, out, bias, fanout)
             return out
         sub = _Mac(mac.rowptr[lo : hi + 1], mac.col, mac.rot, mac.coef, hi - lo, mac.n_terms, mac.no_rot, mac.max_abs_coef)
-        out = _mac_out(params, sub, cur, None)
-        _run_bias(params, lane, out, _bias_range(bias, lo, hi, id(plan)))
+        out = _mac_out(params, sub, cur, None, out, fanout)
+        _run_bias(params, lane, out, _bias_range(bias, lo, hi), fanout)
         return out
     x = cur if cur.shape[0] == hi - lo else cur[lo:hi]
     mac, bias, identity = _act_lowered(plan, t, params.n, encoding, hi - lo)
     fused = _act_scalars(plan, t, params.n, encoding)
-    if fused is not None and not identity:
-        # a2 x^2 + a1 x with constant plaintexts: one fused product epilogue
-        out = fv.mul_ct_batch(params, ek, lane, x, None, chunk=mul_chunk, act=fused)
+    if identity or fused is not None:
+        # a2 x^2 + a1 x with constant plaintexts (or x^2): one fused product epilogue
+        out = fv.mul_ct_batch(params, ek, lane, x, None, out=out, chunk=mul_chunk, act=None if identity else fused,
+                              fanout=fanout)
     else:
         sq = fv.mul_ct_batch(params, ek, lane, x, None, chunk=mul_chunk)
-        out = sq if identity else _mac_out(params, mac, sq, x)
-    _run_bias(params, lane, out, bias)
+        out = _mac_out(params, mac, sq, x, out, fanout)
+    _run_bias(params, lane, out, bias, fanout)
     return out
 
 

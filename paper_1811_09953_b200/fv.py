@@ -496,11 +496,13 @@ MUL_CT_WORKSPACE_CAP = 12 << 30  # default scratch cap per call (bytes)
 
 
 def mul_ct_batch(params: EncryptionParams, ek: EvalKeys, lane: int, a, b=None, out=None, chunk: int | None = None,
-                 workspace=None, act: tuple | None = None):
+                 workspace=None, act: tuple | None = None, fanout=()):
     """Relinearised products of [B][2][k][n] buffers (b=None: squares).
 
     act=(c2, c1): fused activation epilogue, out = c2*a^2 + c1*a (mod q)
-    (squares only; fcn_mul_ct_ex, include/fcn.h)."""
+    (squares only; fcn_mul_ct_ex, include/fcn.h).  fanout: device addresses
+    that receive the same output rows from the final kernel
+    (fcn_mul_ct_multi)."""
     B = a.shape[0]
     if out is None:
         out = dev.empty(a.shape)
@@ -517,10 +519,11 @@ def mul_ct_batch(params: EncryptionParams, ek: EvalKeys, lane: int, a, b=None, o
         workspace = mul_ct_workspace(params, chunk)
     nbytes = workspace.numel() * 8
     flags, c2, c1 = (0, 1, 0) if act is None else (1, int(act[0]), int(act[1]))
+    ptrs = _lib.ptr_array([out.data_ptr()] + [int(p) for p in fanout])
     _lib.check(
-        _lib.lib().fcn_mul_ct_ex(
-            h.ptr, kh.ptr, lane, a.data_ptr(), b.data_ptr() if b is not None else None, out.data_ptr(), B, flags, c2, c1,
-            workspace.data_ptr(), nbytes, dev.stream_ptr(),
+        _lib.lib().fcn_mul_ct_multi(
+            h.ptr, kh.ptr, lane, a.data_ptr(), b.data_ptr() if b is not None else None, C.cast(ptrs, C.c_void_p),
+            1 + len(fanout), B, flags, c2, c1, workspace.data_ptr(), nbytes, dev.stream_ptr(),
         ),
         FVError,
     )

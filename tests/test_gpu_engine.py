@@ -231,11 +231,42 @@ def test_sharded_evaluator_single_rank_nccl(E):
     dist.init_process_group("nccl", rank=0, world_size=1)
     try:
         got, gc = fdist.eval_encrypted_sharded(net, tensor, ek, cfg, encoding="batched")
+        got_p, gc_p = fdist.eval_encrypted_sharded(net, tensor, ek, cfg, encoding="batched", transport="p2p")
     finally:
         dist.destroy_process_group()
-    assert np.array_equal(got.host_bodies(), want.host_bodies())
-    assert list(got.depths) == list(want.depths) and list(got.scales) == list(want.scales)
-    assert gc.same_ops(wc)
+    for g, c in ((got, gc), (got_p, gc_p)):
+        assert np.array_equal(g.host_bodies(), want.host_bodies())
+        assert list(g.depths) == list(want.depths) and list(g.scales) == list(want.scales)
+        assert c.same_ops(wc)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("encoding", ["batched", "integer"])
+def test_fanout_schedule_simulated(E, world, encoding):
+    """The fused layer + all-gather (fan-out stores of every stage's last
+    kernel into all ranks' buffers) reproduces the single-GPU evaluator in
+    every rank's buffer.  The ranks' blocks run one after another on this
+    GPU (no rank waits on another); only the NVLink mapping of the peer
+    buffers differs on a multi-GPU box."""
+    from paper_1811_09953_b200 import dist as fdist
+    from paper_1811_09953_b200 import device as dev
+    from paper_1811_09953_b200 import fv
+    from paper_1811_09953_b200.encode import FixedPointConfig
+
+    P, OP, net = _small_batched_setup(E, fv)
+    cfg = FixedPointConfig((65537,), 4)
+    sk, pk, ek = fv.keygen(P, 2)
+    if encoding == "batched":
+        x = np.random.default_rng(1).integers(0, 16, (16, P.n))
+        tensor = E.encrypt_tensor_batched(pk, P, x.reshape(1, 4, 4, P.n), cfg, 0, 3)
+    else:
+        x = np.random.default_rng(1).integers(0, 16, (1, 4, 4))
+        tensor = E.encrypt_tensor(pk, P, x, cfg, 0, 3)
+    want, _ = E.eval_encrypted(net, tensor, ek, cfg, encoding=encoding)
+    outs = fdist.simulate_fanout(net, tensor, ek, cfg, encoding, world)
+    ref = want.host_bodies()
+    for r, o in enumerate(outs):
+        assert np.array_equal(dev.to_host(o).reshape(ref.shape), ref), r
 
 
 def _sampled_first_stage(E, name, n_check, seed=5):
