@@ -19,9 +19,12 @@ one synthetic image per slot (8,192 images per pass).  A step is one
 restated in numpy + Python big ints) with all host cores instead.
 
 Multi-GPU (torchrun, one rank per GPU): `--shard outputs` (default) splits
-every layer's outputs across ranks and all-gathers them over NCCL
-(strong scaling of one batch); `--shard replicas` runs an independent batch
-per rank (weak scaling, no collective).
+every layer's outputs across ranks (strong scaling of one batch); with
+`--transport p2p` (default) each stage's last kernel stores its block into
+every rank's buffer over NVLink (symmetric memory, no collective on the data
+path), with `--transport nccl` the blocks are all-gathered with NCCL.
+`--shard replicas` runs an independent batch per rank (weak scaling, no
+collective).
 """
 
 from __future__ import annotations
@@ -48,6 +51,7 @@ def _args():
     ap.add_argument("--impl", choices=["fcn", "reference"], default="fcn")
     ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
     ap.add_argument("--shard", choices=["outputs", "replicas"], default="outputs")
+    ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
@@ -366,7 +370,22 @@ def run_gpu(args, ws, rank, local):
     if sharded:
         from paper_1811_09953_b200 import dist as fdist
 
-        evaluate = lambda t: fdist.eval_encrypted_sharded(net, t, ek, cfg, encoding="batched")[0]  # noqa: E731
+        transport = args.transport
+        if transport == "p2p":
+            # pre-flight: every rank must be able to map the symmetric buffers
+            ok = 1
+            try:
+                fdist.eval_encrypted_sharded(net, tensor, ek, cfg, encoding="batched", transport="p2p")
+            except Exception as exc:  # noqa: BLE001 - reported in config
+                ok = 0
+                args.transport_note = f"p2p unavailable ({type(exc).__name__}: {exc})"[:200]
+            flag = torch.tensor([ok], device="cuda", dtype=torch.int32)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0:
+                transport = "nccl"
+        args.transport_used = transport
+        evaluate = lambda t: fdist.eval_encrypted_sharded(net, t, ek, cfg, encoding="batched",  # noqa: E731
+                                                          transport=transport)[0]
     else:
         evaluate = lambda t: engine.eval_encrypted(net, t, ek, cfg, encoding="batched")[0]  # noqa: E731
 
@@ -494,8 +513,10 @@ def run_gpu(args, ws, rank, local):
         "vs_baseline": None,
         "dtype": "u64",
         "data": "synthetic (seeded uint8 images, one per slot; random-init pruned pow2 weights)",
-        "config": _config(W, args.workload, ws, args.shard, hops,
-                          "inputs larger than L2 (%d MB of input ciphertexts per step)" % (tensor.buf.numel() * 8 >> 20)),
+        "config": dict(_config(W, args.workload, ws, args.shard, hops,
+                               "inputs larger than L2 (%d MB of input ciphertexts per step)" % (tensor.buf.numel() * 8 >> 20)),
+                       **({"transport": getattr(args, "transport_used", args.transport)} if sharded else {}),
+                       **({"transport_note": args.transport_note} if getattr(args, "transport_note", None) else {})),
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
         "decrypt_check": check,

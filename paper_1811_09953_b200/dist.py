@@ -181,6 +181,9 @@ def _max_rows(plans, world: int) -> int:
     return max(rows, 1)
 
 
+_P2P_BUFFERS: dict = {}  # (shape, group, device) -> (two symmetric buffers, their handles)
+
+
 def _eval_p2p(net, tensor, ek, cfg, encoding, group, mul_chunk):
     import torch
     import torch.distributed as dist
@@ -198,8 +201,16 @@ def _eval_p2p(net, tensor, ek, cfg, encoding, group, mul_chunk):
     plans = compiled.plans
     shape = (_max_rows(plans, world), 2, len(params.limb_primes), params.n)
     gname = group.group_name if group is not None else dist.group.WORLD.group_name
-    bufs = [symm.empty(shape, dtype=torch.int64, device=torch.device("cuda", dev.current_device())) for _ in range(2)]
-    hdls = [symm.rendezvous(b, gname) for b in bufs]
+    key = (shape, gname, dev.current_device())
+    ws = _P2P_BUFFERS.get(key)
+    if ws is None:
+        bufs = [symm.empty(shape, dtype=torch.int64, device=torch.device("cuda", dev.current_device())) for _ in range(2)]
+        ws = (bufs, [symm.rendezvous(b, gname) for b in bufs])
+        _P2P_BUFFERS[key] = ws
+    bufs, hdls = ws
+    # no rank may overwrite a peer's buffers while that peer still reads the
+    # previous call's result out of them
+    hdls[0].barrier(channel=1)
     rb = engine._row_bytes(params)
     events = []
     cur = tensor.buf
@@ -218,7 +229,6 @@ def _eval_p2p(net, tensor, ek, cfg, encoding, group, mul_chunk):
         events.append((st, ev0, ev1))
         cur = dst[:count]
     out = cur.clone()
-    torch.cuda.current_stream().synchronize()
     return _result(net, tensor, cfg, encoding, compiled, counter, meta, out, events)
 
 
