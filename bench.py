@@ -225,6 +225,36 @@ def _ntt_roofline(P, iters: int = 20):
     return {"rows": rows, "n": n, "bytes": bytes_per_launch, "t_fwd_s": t_f, "t_inv_s": t_i}
 
 
+def _keyswitch_roofline(P, ek, count: int = 256, iters: int = 20):
+    """Average duration of the key-switching inner product (fcn_key_mac) over
+    `count` ciphertexts of NTT-domain digits (> L2): bytes = digits read +
+    accumulators written (keys excluded, SURVEY 8(d) convention)."""
+    import torch
+
+    from paper_1811_09953_b200 import _lib
+    from paper_1811_09953_b200 import device as dev
+
+    h = P.native()
+    kh = ek.native(P)
+    k, n, D = len(P.limb_primes), P.n, P.ell + 1
+    g = torch.Generator(device="cuda").manual_seed(1)
+    dig = torch.randint(0, 1 << 50, (count, D, k, n), device="cuda", dtype=torch.int64, generator=g)
+    acc = torch.empty((count, 2, k, n), device="cuda", dtype=torch.int64)
+    st = dev.stream_ptr()
+    L = _lib.lib()
+    for _ in range(3):
+        _lib.check(L.fcn_key_mac(h.ptr, kh.ptr, dig.data_ptr(), acc.data_ptr(), count, st))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        _lib.check(L.fcn_key_mac(h.ptr, kh.ptr, dig.data_ptr(), acc.data_ptr(), count, st))
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / iters / 1e3
+    return {"count": count, "digits": D, "bytes": count * (D * k + 2 * k) * n * 8, "t_s": t}
+
+
 # ----------------------------------------------------------------- CPU leg
 
 
@@ -490,6 +520,20 @@ def run_gpu(args, ws, rank, local):
         "note": "the NTT is FP64-pipe bound on B200 (one exact signed modmul = 5 DP ops + FRND per butterfly): "
                 "the register-resident butterfly ceiling is ~60% of the HBM roofline at n=8192",
     }
+    ks = _keyswitch_roofline(P, ek)
+    ks_ach = ks["bytes"] / ks["t_s"] / 1e9
+    keyswitch = {
+        "kernel": "keymac_f64_kernel (fcn_key_mac: sum_d key_d * digit_d, NTT domain)",
+        "bound": "hbm",
+        "achieved": ks_ach,
+        "peak": peak,
+        "unit": "GB/s",
+        "frac": ks_ach / peak,
+        "algorithmic_bytes_per_launch": ks["bytes"],
+        "ciphertexts_per_launch": ks["count"],
+        "digits": ks["digits"],
+        "ms": ks["t_s"] * 1e3,
+    }
     hops = engine.plan_hops(comp, "batched", W.t).totals
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
@@ -521,6 +565,7 @@ def run_gpu(args, ws, rank, local):
         "gpu_launches": int(launches),
         "decrypt_check": check,
         "roofline": roofline,
+        "keyswitch_roofline": keyswitch,
         "cpu_baseline": cpu,
         "e2e": e2e,
     }

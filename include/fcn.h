@@ -185,6 +185,14 @@ int fcn_mul_ct_multi(const fcn_ctx* ctx, const fcn_keys* keys, int lane, const u
                      const uint64_t* d_b, uint64_t* const* d_outs, int n_dst, int64_t count, int flags,
                      int64_t act_c2, int64_t act_c1, void* d_workspace, size_t workspace_bytes, void* stream);
 
+/* Key-switching inner product of fv.mul_ct (fv.py:533-537) on NTT-domain
+ * rows: acc[c][0] = sum_d g_d * D[c][d], acc[c][1] = sum_d a_d * D[c][d]
+ * (mod q_l, pointwise), for digits [count][D][k][n] already forward-NTT'd
+ * per limb; acc [count][2][k][n].  The kernel fcn_mul_ct runs between its
+ * digit NTT and its final inverse NTT, exported for measurement.          */
+int fcn_key_mac(const fcn_ctx* ctx, const fcn_keys* keys, const uint64_t* d_digits, uint64_t* d_acc,
+                int64_t count, void* stream);
+
 /* fv.decrypt core (fv.py:337-353): given w = [c0 + c1 s]_q as RNS rows
  * [count][k][n], write m = floor((w t + q>>1)/q) mod t as [count][n].     */
 int fcn_decrypt_round(const fcn_ctx* ctx, int lane, const uint64_t* d_w, uint64_t* d_m, int64_t count,

@@ -1809,6 +1809,16 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
   return FCN_OK;
 }
 
+extern "C" int fcn_key_mac(const fcn_ctx* x, const fcn_keys* keys, const uint64_t* d_digits, uint64_t* d_acc,
+                           int64_t count, void* stream) {
+  if (!x || !keys) return set_error(FCN_ERR_ARG, "null context or keys");
+  if (count <= 0) return FCN_OK;
+  if (!d_digits || !d_acc) return set_error(FCN_ERR_ARG, "null buffer");
+  if (keys->k != x->k || keys->n != x->n || keys->D != x->ell + 1) return set_error(FCN_ERR_ARG, "keys do not match context");
+  DeviceGuard gd(x->device);
+  return launch_keymac(d_digits, keys, d_acc, count, keys->D, x->k, x, (cudaStream_t)stream);
+}
+
 extern "C" int fcn_decrypt_round(const fcn_ctx* x, int lane, const uint64_t* d_w, uint64_t* d_m, int64_t count, void* stream) {
   if (!x || lane < 0 || lane >= x->n_lanes) return set_error(FCN_ERR_ARG, "bad context or lane");
   if (count <= 0) return FCN_OK;
