@@ -357,10 +357,12 @@ __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restric
     const uint64_t b = csub(csub(mulw(neg[v], 1, one_s, nq), 2 * q), q);
     res[v] = submod(a, b, q);
   }
-  for (int d = 0; d < F.n; ++d) {
-    uint64_t* dst = F.dst[d] + (int64_t)o * ct_words + (int64_t)r * n + j0;
-    *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(res[0], res[1]);
-    *reinterpret_cast<ulonglong2*>(dst + 2) = make_ulonglong2(res[2], res[3]);
+  const int64_t off = (int64_t)o * ct_words + (int64_t)r * n + j0;
+  *reinterpret_cast<ulonglong2*>(F.dst[0] + off) = make_ulonglong2(res[0], res[1]);
+  *reinterpret_cast<ulonglong2*>(F.dst[0] + off + 2) = make_ulonglong2(res[2], res[3]);
+  for (int d = 1; d < F.n; ++d) {  // fan-out to the peers' buffers
+    *reinterpret_cast<ulonglong2*>(F.dst[d] + off) = make_ulonglong2(res[0], res[1]);
+    *reinterpret_cast<ulonglong2*>(F.dst[d] + off + 2) = make_ulonglong2(res[2], res[3]);
   }
 }
 
@@ -616,7 +618,12 @@ __device__ __forceinline__ void emit_digits(const uint64_t* out, const RescaleP<
   }
   mw_reduce_q<NW>(a, cc, (int64_t)floor(fu));
   const int D = P.D, w = P.w;
-  if (P.direct) {
+  if (P.direct && w == 32) {
+    // beta = 2^32 (the configs): digit d is half d&1 of word d>>1 (compile-time indices)
+#pragma unroll
+    for (int d = 0; d < 2 * NW; ++d)
+      if (d < D) DG[(ct * D + d) * n + coef] = (a[d >> 1] >> (32 * (d & 1))) & 0xFFFFFFFFull;
+  } else if (P.direct) {
     // every digit < 2^w <= min q_i: one row per digit, broadcast to the limbs by the NTT
     const uint64_t mask = (w >= 64) ? ~0ull : ((1ull << w) - 1);
     for (int d = 0; d < D; ++d) {

@@ -707,7 +707,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 // during the last pass (each thread fetches exactly the residues it will
 // combine, so no barrier is needed); the next input row is prefetched into
 // registers instead (coalesced, as in the forward kernel).
-template <int LOGN, bool SCALE>
+template <int LOGN, bool SCALE, bool FAN>
 __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     ntt_f64_inv_epi(const uint64_t* __restrict__ data, int64_t n_rows, int period, int offset,
                     const LimbConst* __restrict__ lcs, const double2* __restrict__ tws,
@@ -771,13 +771,18 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     inv_ctf<5, LOGN - 5>(x, tid, tw, q, qi);
     cp_async_wait_all();
     const double c2 = E.fc2[limb], c2q = E.fc2q[limb];
+    uint64_t* po = E.out.dst[0] + row * N;
+    const int nd = E.out.n;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const double2 w = ld_ftw(twist + tid + j * T);
       double y = fredq(fmulq(x[j], w.x, w.y, q), qi, q);  // |y| <= q/2 + 1
       if (SCALE) y = fmulq(y, c2, c2q, q);              // |y| < 0.7 q
       const uint64_t v = f2u_canon(fredq(y + u2f(sm[phys(tid + j * T)]), qi, q), q);
-      for (int d = 0; d < E.out.n; ++d) E.out.dst[d][row * N + tid + j * T] = v;
+      po[tid + j * T] = v;
+      if (FAN) {  // fan-out to the peers' buffers
+        for (int d = 1; d < nd; ++d) E.out.dst[d][row * N + tid + j * T] = v;
+      }
     }
     const int64_t nxt = row + gridDim.x;
     if (nxt < n_rows) {
@@ -824,7 +829,10 @@ template <int LOGN, bool FWD, int EPI = 0>
 static const void* f64_ptr() {
   return FWD ? (const void*)ntt_f64_fwd<LOGN>
              : (EPI == 0 ? (const void*)ntt_f64_inv<LOGN>
-                         : (EPI == 1 ? (const void*)ntt_f64_inv_epi<LOGN, false> : (const void*)ntt_f64_inv_epi<LOGN, true>));
+                : EPI == 1 ? (const void*)ntt_f64_inv_epi<LOGN, false, false>
+                : EPI == 2 ? (const void*)ntt_f64_inv_epi<LOGN, true, false>
+                : EPI == 3 ? (const void*)ntt_f64_inv_epi<LOGN, false, true>
+                           : (const void*)ntt_f64_inv_epi<LOGN, true, true>);
 }
 
 static int g_sms = 0;
@@ -880,11 +888,11 @@ static void init_tables() {
     }
   }
   {
-    const void* epis[10] = {f64_ptr<10, false, 1>(), f64_ptr<11, false, 1>(), f64_ptr<12, false, 1>(),
-                            f64_ptr<13, false, 1>(), f64_ptr<14, false, 1>(), f64_ptr<10, false, 2>(),
-                            f64_ptr<11, false, 2>(), f64_ptr<12, false, 2>(), f64_ptr<13, false, 2>(),
-                            f64_ptr<14, false, 2>()};
-    for (int i = 0; i < 10; ++i) {
+#define FCN_EPIS(E) f64_ptr<10, false, E>(), f64_ptr<11, false, E>(), f64_ptr<12, false, E>(), \
+                    f64_ptr<13, false, E>(), f64_ptr<14, false, E>()
+    const void* epis[20] = {FCN_EPIS(1), FCN_EPIS(2), FCN_EPIS(3), FCN_EPIS(4)};
+#undef FCN_EPIS
+    for (int i = 0; i < 20; ++i) {
       cudaError_t e = cudaFuncSetAttribute(epis[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v2_smem(10 + i % 5));
       if (e != cudaSuccess) g_init_err = e;
     }
@@ -955,12 +963,18 @@ static void launch_f64_t(bool fwd, int grid, uint64_t* d, int64_t n_rows, int pe
                                                           src_div);
   else if (!epi || epi->mode == 0)
     ntt_f64_inv<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict, r->d_ftwist);
+  else if (epi->out.n == 1 && epi->mode == 1)
+    ntt_f64_inv_epi<LOGN, false, false><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc,
+                                                                           r->d_fict, r->d_ftwist, *epi);
+  else if (epi->out.n == 1)
+    ntt_f64_inv_epi<LOGN, true, false><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc,
+                                                                          r->d_fict, r->d_ftwist, *epi);
   else if (epi->mode == 1)
-    ntt_f64_inv_epi<LOGN, false><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict,
-                                                                     r->d_ftwist, *epi);
+    ntt_f64_inv_epi<LOGN, false, true><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc,
+                                                                          r->d_fict, r->d_ftwist, *epi);
   else
-    ntt_f64_inv_epi<LOGN, true><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict,
-                                                                    r->d_ftwist, *epi);
+    ntt_f64_inv_epi<LOGN, true, true><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc,
+                                                                         r->d_fict, r->d_ftwist, *epi);
 }
 
 static int launch_epi_int(const fcn_ring* r, const uint64_t* d, int64_t n_rows, int period, int offset, cudaStream_t st,
