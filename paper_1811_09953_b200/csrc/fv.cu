@@ -299,6 +299,9 @@ __global__ void __launch_bounds__(256) mac_kernel(const uint64_t* __restrict__ i
   for (int d = 0; d < F.n; ++d) *reinterpret_cast<ulonglong2*>(F.dst[d] + (int64_t)o * ct_words + (int64_t)r * n + j0) = res;
 }
 
+#ifndef MAC_WAVES
+#define MAC_WAVES 8
+#endif
 // Fast path: all rotations 0 (constant plaintexts) and max|coef| * q small
 // enough that `fold` consecutive products fit one 64-bit accumulator.  Each
 // term is then one IMAD.WIDE + one IMAD per residue (acc += x * |c|),
@@ -309,15 +312,17 @@ __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restric
                                                        const int32_t* __restrict__ rowptr,
                                                        const int32_t* __restrict__ col,
                                                        const int64_t* __restrict__ coef, const __grid_constant__ Fanout F,
-                                                       int logn, int k, const LimbConst* __restrict__ lcs, int fold) {
+                                                       int logn, int k, const LimbConst* __restrict__ lcs, int fold,
+                                                       int n_out) {
   const int n = 1 << logn;
-  const int o = blockIdx.y;
   const int r = blockIdx.z;
   const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (j0 >= n) return;
   const LimbConst& c = lcs[r % k];
   const uint64_t q = c.q, nq = c.nq, one_s = c.one_s;
   const int64_t ct_words = (int64_t)2 * k * n;
+  // outputs o = blockIdx.y + i * gridDim.y: per-CTA setup amortised over several outputs
+  for (int o = blockIdx.y; o < n_out; o += gridDim.y) {
   uint64_t pos[4] = {0, 0, 0, 0}, neg[4] = {0, 0, 0, 0};
   const int e0 = rowptr[o], e1 = rowptr[o + 1];
   int cnt = 0;
@@ -363,6 +368,7 @@ __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restric
   for (int d = 1; d < F.n; ++d) {  // fan-out to the peers' buffers
     *reinterpret_cast<ulonglong2*>(F.dst[d] + off) = make_ulonglong2(res[0], res[1]);
     *reinterpret_cast<ulonglong2*>(F.dst[d] + off + 2) = make_ulonglong2(res[2], res[3]);
+  }
   }
 }
 
@@ -1479,9 +1485,14 @@ extern "C" int fcn_linear_mac_multi(const fcn_ctx* x, const uint64_t* d_in0, int
   }
   if (fold >= 2 && x->n >= 4) {
     const int per_cta = threads * 4;
-    dim3 grid((x->n + per_cta - 1) / per_cta, (unsigned)n_out, 2 * x->k);
+    const int gx = (x->n + per_cta - 1) / per_cta, gz = 2 * x->k;
+    // ~8 resident CTAs x 148 SMs x a few waves; each CTA walks several outputs
+    int64_t gy = (148LL * 8 * MAC_WAVES + gx * gz - 1) / (gx * gz);
+    if (gy > n_out) gy = n_out;
+    if (gy < 1) gy = 1;
+    dim3 grid(gx, (unsigned)gy, gz);
     mac_fast_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_coef, F,
-                                                               x->logn, x->k, x->ext->d_lc, fold);
+                                                               x->logn, x->k, x->ext->d_lc, fold, (int)n_out);
     FCN_LAUNCH_CHECK("mac_fast_kernel");
     return FCN_OK;
   }
