@@ -148,6 +148,34 @@ def test_config_shape_square_vs_oracle(F, cfg):
         assert np.array_equal(out[b], np.stack([want.c0, want.c1]))
 
 
+def test_square_extreme_ciphertexts_cfg2(F):
+    """mul_ct (FP64 lift / tensor / rescale / key MAC over the cfg2 base with
+    auxiliary primes just below 2^51) on ciphertexts whose coefficients sit
+    at the extremes of the centred lift: q-1, (q-1)/2, (q+1)/2, 0."""
+    from paper_1811_09953_b200 import configs
+    from paper_1811_09953_b200 import device as dev
+
+    W = configs.WORKLOADS["cfg2"]
+    P = F.EncryptionParams(W.n, W.primes, (W.t,), W.beta)
+    OP = ob.Params(W.n, W.primes, (W.t,), W.beta)
+    sk, pk, ek = F.keygen(P, 2)
+    K = ob.Keys(sk.s.host(), pk.p0.host(), pk.p1.host(), [x.host() for x in ek.a], [x.host() for x in ek.g])
+    q = math.prod(W.primes)
+    n = W.n
+
+    def rows(v):
+        return np.stack([np.full(n, v % p, dtype=np.uint64) for p in W.primes])
+
+    mix = np.stack([np.array([(q - 1, (q - 1) // 2, (q + 1) // 2, 0)[j % 4] % p for j in range(n)], dtype=np.uint64)
+                    for p in W.primes])
+    cts = [(rows(q - 1), rows(q - 1)), (rows((q - 1) // 2), rows((q + 1) // 2)), (mix, mix[:, ::-1].copy())]
+    x = np.stack([np.stack([a, b]) for a, b in cts])
+    out = dev.to_host(F.mul_ct_batch(P, ek, 0, dev.to_device(x)))
+    for i, (a, b) in enumerate(cts):
+        want = ob.mul_ct(OP, ob.Ct(a, b), ob.Ct(a, b), K)
+        assert np.array_equal(out[i], np.stack([want.c0, want.c1])), i
+
+
 @pytest.mark.parametrize("primes", [(36028797018972161, 36028797018990593), (1125899906826241, 1125899906820097)],
                          ids=["int64-55bit", "fp64-50bit"])
 @pytest.mark.parametrize("c2,c1", [(1, 0), (-3, 5), (64, -1), (12345, -32768)])

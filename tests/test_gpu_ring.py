@@ -59,6 +59,41 @@ def test_ntt_extreme_values(R):
     assert np.array_equal(R.ntt_inverse(R.RingPoly(ctx, x, R.NTT)).host(), orn.intt(x, primes))
 
 
+def _primes_below_2_51(n, count):
+    """NTT primes just below 2^51 (the auxiliary-base rule of libfcn):
+    the tightest case of the FP64 kernels' |x| < 3.86 q < 2^53 bound."""
+    from oracle import nt
+
+    step = 2 * n
+    p = ((1 << 51) // step) * step + 1
+    out = []
+    while len(out) < count:
+        p -= step
+        if nt.is_prime(p):
+            out.append(p)
+    return tuple(out)
+
+
+@pytest.mark.parametrize("n", [1024, 8192, 16384])
+def test_ntt_fp64_extreme_values_near_2_51(R, n):
+    """FP64 NTT (q < 2^51) on rows that maximise every intermediate:
+    all q-1, all (q-1)/2, all (q+1)/2, alternating 0 / q-1, and random."""
+    primes = _primes_below_2_51(n, 2)
+    ctx = R.RingContext.create(n, primes)
+    rng = np.random.default_rng(n)
+    cases = [
+        [np.full(n, q - 1, dtype=np.uint64) for q in primes],
+        [np.full(n, (q - 1) // 2, dtype=np.uint64) for q in primes],
+        [np.full(n, (q + 1) // 2, dtype=np.uint64) for q in primes],
+        [np.where(np.arange(n) % 2 == 0, 0, q - 1).astype(np.uint64) for q in primes],
+        [rng.integers(0, q, n, dtype=np.uint64) for q in primes],
+    ]
+    for rows in cases:
+        x = np.stack(rows)
+        assert np.array_equal(R.ntt_forward(R.RingPoly(ctx, x)).host(), orn.ntt(x, primes))
+        assert np.array_equal(R.ntt_inverse(R.RingPoly(ctx, x, R.NTT)).host(), orn.intt(x, primes))
+
+
 def test_ring_ops_match_reference(R, golden_meta, golden_npz):
     d = golden_npz("ringops")
     m = golden_meta["ringops"]
