@@ -467,8 +467,13 @@ def run_gpu(args, ws, rank, local):
                                                buf=hb.to("cuda", non_blocking=True), params=P, lane=0)
                     yield evaluate(t_in).buf.to("cpu")
         else:
+            # result ring allocated once, like a server would (pinned allocation is slow)
+            out_shape = (int(np.prod(comp.out_shape)), 2, len(P.limb_primes), P.n)
+            ring = [torch.empty(out_shape, dtype=torch.int64, pin_memory=True) for _ in range(3)]
+
             def stream(batches):
-                return engine.evaluate_stream(net, batches, ek, cfg, P, tensor.shape, tensor.scale_exponent)
+                return engine.evaluate_stream(net, batches, ek, cfg, P, tensor.shape, tensor.scale_exponent,
+                                              host_out=ring)
         for _ in stream(host_in[i % 2] for i in range(2)):
             pass
         barrier()
