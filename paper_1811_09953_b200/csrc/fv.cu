@@ -316,13 +316,13 @@ __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restric
                                                        int n_out) {
   const int n = 1 << logn;
   const int r = blockIdx.z;
-  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const int j0 = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
   if (j0 >= n) return;
   const LimbConst& c = lcs[r % k];
   const uint64_t q = c.q, nq = c.nq, one_s = c.one_s;
   const int64_t ct_words = (int64_t)2 * k * n;
   // outputs o = blockIdx.y + i * gridDim.y: per-CTA setup amortised over several outputs
-  for (int o = blockIdx.y; o < n_out; o += gridDim.y) {
+  for (int o = blockIdx.x; o < n_out; o += gridDim.x) {
   uint64_t pos[4] = {0, 0, 0, 0}, neg[4] = {0, 0, 0, 0};
   const int e0 = rowptr[o], e1 = rowptr[o + 1];
   int cnt = 0;
@@ -1485,12 +1485,14 @@ extern "C" int fcn_linear_mac_multi(const fcn_ctx* x, const uint64_t* d_in0, int
   }
   if (fold >= 2 && x->n >= 4) {
     const int per_cta = threads * 4;
-    const int gx = (x->n + per_cta - 1) / per_cta, gz = 2 * x->k;
-    // ~8 resident CTAs x 148 SMs x a few waves; each CTA walks several outputs
-    int64_t gy = (148LL * 8 * MAC_WAVES + gx * gz - 1) / (gx * gz);
-    if (gy > n_out) gy = n_out;
-    if (gy < 1) gy = 1;
-    dim3 grid(gx, (unsigned)gy, gz);
+    const int gy = (x->n + per_cta - 1) / per_cta, gz = 2 * x->k;
+    // blockIdx.x (fastest) walks outputs, so the CTAs resident at any time
+    // share one (row, coefficient tile): its slice of every input (n_in x
+    // 8 KB) stays in L2 while all outputs that reference it are summed.
+    int64_t gx = (148LL * 8 * MAC_WAVES + gy * gz - 1) / (gy * gz);
+    if (gx > n_out) gx = n_out;
+    if (gx < 1) gx = 1;
+    dim3 grid((unsigned)gx, gy, gz);
     mac_fast_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_coef, F,
                                                                x->logn, x->k, x->ext->d_lc, fold, (int)n_out);
     FCN_LAUNCH_CHECK("mac_fast_kernel");
