@@ -5,7 +5,8 @@ N=16384, 8 x ~50-bit limbs, 4096 random uniform ciphertexts (seed 0):
   * ciphertext square + relinearisation with a dnum=3 key (beta = 2^134),
   * 1024-term sparse power-of-two MAC: 4096 outputs over the 4096 inputs.
 Prints one JSON line (per-op times, GB/s vs the HBM copy peak, the NTT's
-butterflies/s vs the measured mulw peak); optionally writes it to a file.
+butterflies/s vs the measured FP64 butterfly peak, the key-switching inner
+product's GB/s); optionally writes it to a file.
 
 usage: python tools/sweep.py [--out profiles/sweep_r01.json] [--count 4096]
 """
@@ -55,7 +56,7 @@ def main():
     ct_bytes = 2 * k * n * 8
     peak = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(REPO, "MEASURED_PEAKS.json")) else 6650.0
-    ip = json.load(open(os.path.join(REPO, "profiles", "int_peak.json")))
+    fp = json.load(open(os.path.join(REPO, "profiles", "fp64_peak.json")))
     L = _lib.lib()
     st = dev.stream_ptr()
     res = {"workload": "cfg5", "n": n, "limbs": k, "ciphertexts": B, "beta_log2": 134, "dnum": P.ell + 1}
@@ -73,7 +74,7 @@ def main():
     res["ntt_fwd_inv_s"] = t
     res["ntt_gbs"] = byts / t / 1e9
     res["ntt_frac_hbm"] = byts / t / 1e9 / peak
-    res["ntt_frac_mulw_peak"] = bfly / t / ip["mulw_per_s"]
+    res["ntt_frac_fp64_butterfly_peak"] = bfly / t / fp["butterfly_per_s"]
     assert torch.equal(y, x)
 
     # square + relinearisation (dnum = 3)
@@ -89,6 +90,21 @@ def main():
     res["square_relin_gbs"] = byts / t / 1e9
     res["square_relin_frac_hbm"] = byts / t / 1e9 / peak
     res["square_relin_cts_per_s"] = B / t
+
+    # key-switching inner product alone (digits -> accumulators), 256 cts per launch
+    D = P.ell + 1
+    dig = (torch.randint(0, 1 << 62, (256, D, k, n), device="cuda", generator=g, dtype=torch.int64)
+           % qs.view(1, 1, k, 1)).contiguous()
+    acc = torch.empty((256, 2, k, n), device="cuda", dtype=torch.int64)
+    kh = ek.native(P)
+
+    def km():
+        _lib.check(L.fcn_key_mac(h.ptr, kh.ptr, dig.data_ptr(), acc.data_ptr(), 256, st))
+
+    t = timed(km, iters=10)
+    res["keymac_s_per_256"] = t
+    res["keymac_gbs"] = 256 * (D * k + 2 * k) * n * 8 / t / 1e9
+    res["keymac_frac_hbm"] = res["keymac_gbs"] / peak
 
     # 1024-term sparse pow2 MAC, 4096 outputs over the 4096 inputs
     plan = configs.mac_sweep_plan(n_out=B, n_in=B, terms=args.mac_terms, seed=1)
