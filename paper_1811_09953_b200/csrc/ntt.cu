@@ -773,6 +773,10 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     const double c2 = E.fc2[limb], c2q = E.fc2q[limb];
     uint64_t* po = E.out.dst[0] + row * N;
     const int nd = E.out.n;
+    // the next row's element j is requested as soon as x[j] is consumed, so
+    // its loads overlap the rest of this epilogue
+    const int64_t nxt = row + gridDim.x;
+    const uint64_t* pn = data + (nxt < n_rows ? nxt : row) * N;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const double2 w = ld_ftw(twist + tid + j * T);
@@ -783,12 +787,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
       if (FAN) {  // fan-out to the peers' buffers
         for (int d = 1; d < nd; ++d) E.out.dst[d][row * N + tid + j * T] = v;
       }
-    }
-    const int64_t nxt = row + gridDim.x;
-    if (nxt < n_rows) {
-      const uint64_t* p = data + nxt * N;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
+      x[j] = __longlong_as_double((long long)pn[tid + j * T]);
     }
   }
 }
