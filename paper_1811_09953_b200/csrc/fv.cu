@@ -1012,7 +1012,10 @@ __global__ void key_to_f64_kernel(const uint64_t* __restrict__ w, double2* __res
 // exact) and |.| < 0.75 q; sums are reduced after every 4 products (< 3.5 q).
 // Both outputs' 2D key words stay in registers across the ciphertexts the
 // thread walks; the next ciphertext's D digit loads are issued early.
-template <int DMAX>
+// LEAN (more than 8 digits): only the signed key words stay in registers and
+// each quotient factor is recomputed as w * (1/q) (relative error 3 2^-53:
+// products |.| < 0.875 q, so sums are reduced before every 3rd product).
+template <int DMAX, bool LEAN = false>
 __global__ void __launch_bounds__(256, 2) keymac_f64_kernel(const uint64_t* __restrict__ DG, const double2* __restrict__ kg,
                                                             const double2* __restrict__ ka, uint64_t* __restrict__ ACC,
                                                             int64_t C, int D, int k, int logn,
@@ -1023,11 +1026,19 @@ __global__ void __launch_bounds__(256, 2) keymac_f64_kernel(const uint64_t* __re
   const int l = (int)(lc >> logn);
   const int coef = (int)(lc & (n - 1));
   const double q = lcs[l].fq, qi = lcs[l].fqi;
-  double2 gk[DMAX], ak[DMAX];
+  double2 gk[LEAN ? 1 : DMAX], ak[LEAN ? 1 : DMAX];
+  double gw[LEAN ? DMAX : 1], aw[LEAN ? DMAX : 1];
 #pragma unroll
   for (int d = 0; d < DMAX; ++d) {
-    gk[d] = d < D ? kg[((int64_t)d * k + l) * n + coef] : make_double2(0.0, 0.0);
-    ak[d] = d < D ? ka[((int64_t)d * k + l) * n + coef] : make_double2(0.0, 0.0);
+    const double2 g2 = d < D ? kg[((int64_t)d * k + l) * n + coef] : make_double2(0.0, 0.0);
+    const double2 a2 = d < D ? ka[((int64_t)d * k + l) * n + coef] : make_double2(0.0, 0.0);
+    if (LEAN) {
+      gw[d] = g2.x;
+      aw[d] = a2.x;
+    } else {
+      gk[d] = g2;
+      ak[d] = a2;
+    }
   }
   const int64_t per = (C + gridDim.y - 1) / gridDim.y;
   const int64_t c0 = (int64_t)blockIdx.y * per;
@@ -1050,12 +1061,17 @@ __global__ void __launch_bounds__(256, 2) keymac_f64_kernel(const uint64_t* __re
 #pragma unroll
     for (int d = 0; d < DMAX; ++d) {
       if (d < D) {
-        if (d > 0 && (d & 3) == 0) {
+        if (d > 0 && (LEAN ? d % 3 == 0 : (d & 3) == 0)) {
           g = fredq(g, qi, q);
           a = fredq(a, qi, q);
         }
-        g += fmulq_m(xs[d], gk[d].x, gk[d].y, q);
-        a += fmulq_m(xs[d], ak[d].x, ak[d].y, q);
+        if (LEAN) {
+          g += fmulq_m(xs[d], gw[d], gw[d] * qi, q);
+          a += fmulq_m(xs[d], aw[d], aw[d] * qi, q);
+        } else {
+          g += fmulq_m(xs[d], gk[d].x, gk[d].y, q);
+          a += fmulq_m(xs[d], ak[d].x, ak[d].y, q);
+        }
       }
     }
     ACC[((ct * 2 + 0) * k + l) * n + coef] = f2u_canon(fredq(g, qi, q), q);
@@ -1389,7 +1405,7 @@ extern "C" int fcn_keys_create(const fcn_ctx* x, const uint64_t* a, const uint64
   }
   int rc = launch_ntt(x->ext, kk->d_g, (int64_t)kk->D * kk->k, kk->k, 0, true, 0);
   if (!rc) rc = launch_ntt(x->ext, kk->d_a, (int64_t)kk->D * kk->k, kk->k, 0, true, 0);
-  if (!rc && x->fp && kk->D <= 8) {
+  if (!rc && x->fp && kk->D <= 12) {
     e = cudaMalloc(&kk->d_fg, words * sizeof(double2));
     if (e == cudaSuccess) e = cudaMalloc(&kk->d_fa, words * sizeof(double2));
     if (e != cudaSuccess) {
@@ -1700,13 +1716,16 @@ static int launch_keymac(const uint64_t* DG, const fcn_keys* keys, uint64_t* ACC
   if (split > C) split = C;
   if (split < 1) split = 1;
   dim3 grid(bx, (unsigned)split);
-  if (keys->d_fg && D <= 8) {
-    // exact digit count as the template argument: key words of unused digits take no registers
-    // (beyond 8 digits the 4D key doubles no longer fit the register budget: integer kernel)
+  if (keys->d_fg && D <= 12) {
+    // exact digit count as the template argument: key words of unused digits take no registers;
+    // beyond 8 digits only the key words stay in registers (LEAN); beyond 12 they spill: integer kernel
     switch (D) {
-#define FCN_KM(DD) \
-  case DD: keymac_f64_kernel<DD><<<grid, 256, 0, st>>>(DG, keys->d_fg, keys->d_fa, ACC, C, DD, k, x->logn, x->ext->d_lc); break;
-      FCN_KM(1) FCN_KM(2) FCN_KM(3) FCN_KM(4) FCN_KM(5) FCN_KM(6) FCN_KM(7) FCN_KM(8)
+#define FCN_KM(DD, LN)                                                                                             \
+  case DD:                                                                                                         \
+    keymac_f64_kernel<DD, LN><<<grid, 256, 0, st>>>(DG, keys->d_fg, keys->d_fa, ACC, C, DD, k, x->logn, x->ext->d_lc); \
+    break;
+      FCN_KM(1, false) FCN_KM(2, false) FCN_KM(3, false) FCN_KM(4, false) FCN_KM(5, false) FCN_KM(6, false)
+      FCN_KM(7, false) FCN_KM(8, false) FCN_KM(9, true) FCN_KM(10, true) FCN_KM(11, true) FCN_KM(12, true)
 #undef FCN_KM
     }
     FCN_LAUNCH_CHECK("keymac_f64_kernel");
