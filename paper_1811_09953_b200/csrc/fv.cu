@@ -1500,17 +1500,21 @@ extern "C" int fcn_linear_mac_multi(const fcn_ctx* x, const uint64_t* d_in0, int
     fold = f > 1024 ? 1024 : (int)f;
   }
   if (fold >= 2 && x->n >= 4) {
-    const int per_cta = threads * 4;
-    const int gy = (x->n + per_cta - 1) / per_cta, gz = 2 * x->k;
     // blockIdx.x (fastest) walks outputs, so the CTAs resident at any time
-    // share one (row, coefficient tile): its slice of every input (n_in x
-    // 8 KB) stays in L2 while all outputs that reference it are summed.
-    int64_t gx = (148LL * 8 * MAC_WAVES + gy * gz - 1) / (gy * gz);
+    // (~148 x 8) share one (row, coefficient tile): that tile's slice of
+    // every input stays in L2 while all outputs referencing it are summed.
+    // The tile (4 residues per thread) shrinks so n_in slices fit in ~48 MB.
+    const int64_t n_in_all = n_in0 + n_in1;
+    int th = threads;
+    while (th > 32 && n_in_all * th * 4 * 8 > (48ll << 20)) th >>= 1;
+    const int per_cta = th * 4;
+    const int gy = (x->n + per_cta - 1) / per_cta, gz = 2 * x->k;
+    int64_t gx = 148LL * 8 * MAC_WAVES / 4;
     if (gx > n_out) gx = n_out;
     if (gx < 1) gx = 1;
     dim3 grid((unsigned)gx, gy, gz);
-    mac_fast_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_coef, F,
-                                                               x->logn, x->k, x->ext->d_lc, fold, (int)n_out);
+    mac_fast_kernel<<<grid, th, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_coef, F,
+                                                           x->logn, x->k, x->ext->d_lc, fold, (int)n_out);
     FCN_LAUNCH_CHECK("mac_fast_kernel");
     return FCN_OK;
   }
