@@ -1079,16 +1079,6 @@ __global__ void __launch_bounds__(256, 2) keymac_f64_kernel(const uint64_t* __re
   }
 }
 
-__global__ void add_rows_kernel(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, uint64_t* __restrict__ out,
-                                int64_t total, int logn, int k, const LimbConst* __restrict__ lcs) {
-  const int64_t pairs = total >> 1;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pairs; e += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t q = lcs[(int)(((e << 1) >> logn) % k)].q;
-    const ulonglong2 x = reinterpret_cast<const ulonglong2*>(a)[e], y = reinterpret_cast<const ulonglong2*>(b)[e];
-    reinterpret_cast<ulonglong2*>(out)[e] = make_ulonglong2(addmod(x.x, y.x, q), addmod(x.y, y.y, q));
-  }
-}
-
 // Decrypt rounding m = floor((w t + (q-1)/2)/q) mod t  (fv.py:344-349).
 template <int KQ, int NW>
 __global__ void decrypt_round_kernel(const uint64_t* __restrict__ W, uint64_t* __restrict__ M, int64_t count, int logn,

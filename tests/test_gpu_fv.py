@@ -327,3 +327,40 @@ def test_errors(F):
     with pytest.raises(F.FVError):
         F.EncryptionParams(1000, (17,), (2,))
     assert F.add_pt(ct, F.PlainPoly.zero(P.t_lanes[0])) is ct
+
+
+def test_integer_kernel_family_subprocess():
+    """The integer kernels (used for limbs >= 2^51) on the cfg1/cfg2 shapes:
+    FCN_NTT_INT=1 forces them for every limb in a fresh process (the switch
+    is read once per process); squares and NTTs must match the oracle."""
+    import os
+    import subprocess
+    import sys
+
+    code = r"""
+import numpy as np
+from oracle import bfv as ob, rns as orn
+from paper_1811_09953_b200 import configs, fv, ring
+from paper_1811_09953_b200 import device as dev
+for name in ("cfg1", "cfg2"):
+    W = configs.WORKLOADS[name]
+    P = fv.EncryptionParams(W.n, W.primes, (W.t,), W.beta)
+    OP = ob.Params(W.n, W.primes, (W.t,), W.beta)
+    sk, pk, ek = fv.keygen(P, 2)
+    K = ob.Keys(sk.s.host(), pk.p0.host(), pk.p1.host(), [x.host() for x in ek.a], [x.host() for x in ek.g])
+    rng = np.random.default_rng(1)
+    x = np.stack([np.stack([orn.random_uniform(W.primes, W.n, rng) for _ in range(2)]) for _ in range(2)])
+    out = dev.to_host(fv.mul_ct_batch(P, ek, 0, dev.to_device(x)))
+    for b in range(2):
+        c = ob.Ct(x[b, 0], x[b, 1])
+        w = ob.mul_ct(OP, c, c, K)
+        assert np.array_equal(out[b], np.stack([w.c0, w.c1])), (name, b)
+    ctx = ring.RingContext.create(W.n, W.primes)
+    r = x[0, 0]
+    assert np.array_equal(ring.ntt_forward(ring.RingPoly(ctx, r)).host(), orn.ntt(r, W.primes))
+print("ok")
+"""
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FCN_NTT_INT="1", PYTHONPATH=repo)
+    res = subprocess.run([sys.executable, "-c", code], cwd=repo, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0 and res.stdout.strip().endswith("ok"), res.stdout[-2000:] + res.stderr[-2000:]
