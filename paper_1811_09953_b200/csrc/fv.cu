@@ -307,6 +307,7 @@ __global__ void __launch_bounds__(256) mac_kernel(const uint64_t* __restrict__ i
 // term is then one IMAD.WIDE + one IMAD per residue (acc += x * |c|),
 // accumulators are folded back below 4q every `fold` terms.  Four residues
 // per thread (two 16-byte loads) amortise the term metadata.
+template <bool SMALL>
 __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restrict__ in0, int64_t n_in0,
                                                        const uint64_t* __restrict__ in1,
                                                        const int32_t* __restrict__ rowptr,
@@ -320,6 +321,7 @@ __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restric
   if (j0 >= n) return;
   const LimbConst& c = lcs[r % k];
   const uint64_t q = c.q, nq = c.nq, one_s = c.one_s;
+  const uint32_t m32 = c.m32;
   const int64_t ct_words = (int64_t)2 * k * n;
   // outputs o = blockIdx.y + i * gridDim.y: per-CTA setup amortised over several outputs
   for (int o = blockIdx.x; o < n_out; o += gridDim.x) {
@@ -350,16 +352,22 @@ __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restric
       cnt = 0;
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
-        pos[v] = mulw(pos[v], 1, one_s, nq);
-        neg[v] = mulw(neg[v], 1, one_s, nq);
+        if (SMALL) {
+          pos[v] = reduce_small(pos[v], m32, q);
+          neg[v] = reduce_small(neg[v], m32, q);
+        } else {
+          pos[v] = mulw(pos[v], 1, one_s, nq);
+          neg[v] = mulw(neg[v], 1, one_s, nq);
+        }
       }
     }
   }
   uint64_t res[4];
 #pragma unroll
   for (int v = 0; v < 4; ++v) {
-    const uint64_t a = csub(csub(mulw(pos[v], 1, one_s, nq), 2 * q), q);
-    const uint64_t b = csub(csub(mulw(neg[v], 1, one_s, nq), 2 * q), q);
+    // SMALL: sums kept below 2^62 (fold), reduced by the high-word quotient
+    const uint64_t a = SMALL ? reduce_small(pos[v], m32, q) : csub(csub(mulw(pos[v], 1, one_s, nq), 2 * q), q);
+    const uint64_t b = SMALL ? reduce_small(neg[v], m32, q) : csub(csub(mulw(neg[v], 1, one_s, nq), 2 * q), q);
     res[v] = submod(a, b, q);
   }
   const int64_t off = (int64_t)o * ct_words + (int64_t)r * n + j0;
@@ -1489,6 +1497,16 @@ extern "C" int fcn_linear_mac_multi(const fcn_ctx* x, const uint64_t* d_in0, int
     const unsigned __int128 f = room / per;
     fold = f > 1024 ? 1024 : (int)f;
   }
+  // SMALL variant (every limb in [2^34, 2^56)): sums bounded by 2^62 so one
+  // high-word quotient reduces them (reduce_small) instead of a Shoup product
+  bool small = fold >= 2;
+  for (uint64_t q : x->primes) small &= q >= (1ull << 34) && q < (1ull << 56);
+  int fold_small = 0;
+  if (small) {
+    const unsigned __int128 f = (((unsigned __int128)1 << 62) - qmax) / ((unsigned __int128)qmax * max_abs_coef);
+    fold_small = f > 1024 ? 1024 : (int)f;
+    small = fold_small >= 2;
+  }
   if (fold >= 2 && x->n >= 4) {
     // blockIdx.x (fastest) walks outputs, so the CTAs resident at any time
     // (~148 x 8) share one (row, coefficient tile): that tile's slice of
@@ -1503,8 +1521,12 @@ extern "C" int fcn_linear_mac_multi(const fcn_ctx* x, const uint64_t* d_in0, int
     if (gx > n_out) gx = n_out;
     if (gx < 1) gx = 1;
     dim3 grid((unsigned)gx, gy, gz);
-    mac_fast_kernel<<<grid, th, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_coef, F,
-                                                           x->logn, x->k, x->ext->d_lc, fold, (int)n_out);
+    if (small)
+      mac_fast_kernel<true><<<grid, th, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_coef, F,
+                                                                 x->logn, x->k, x->ext->d_lc, fold_small, (int)n_out);
+    else
+      mac_fast_kernel<false><<<grid, th, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_coef, F,
+                                                                  x->logn, x->k, x->ext->d_lc, fold, (int)n_out);
     FCN_LAUNCH_CHECK("mac_fast_kernel");
     return FCN_OK;
   }
