@@ -825,7 +825,10 @@ __global__ void __launch_bounds__(256, (KQ <= 4 ? 3 : 2)) rescale_kernel(const u
 //     so all partial sums stay below 3.6 q_i < 2^53.
 // Instantiated for exact limb counts (k = KQ, K = KE) only.
 template <int KQ, int KE, int NW>
-__global__ void __launch_bounds__(256, (KQ <= 4 ? 3 : 2))
+#ifndef FCN_RS_MINB
+#define FCN_RS_MINB(KQ) ((KQ) <= 4 ? 3 : 2)
+#endif
+__global__ void __launch_bounds__(256, FCN_RS_MINB(KQ))
     rescale_f64_kernel(const uint64_t* __restrict__ T_in, uint64_t* __restrict__ R01, uint64_t* __restrict__ DG, int64_t C,
                        int logn, const __grid_constant__ RescaleP<KQ, KE> P, const MulCtConst* __restrict__ cc,
                        unsigned long long* __restrict__ fallbacks, const uint64_t* __restrict__ lin) {
