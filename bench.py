@@ -479,19 +479,23 @@ def run_gpu(args, ws, rank, local):
         barrier()
         torch.cuda.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # at least 20 batches so the pipeline fill (one upload not overlapped
+        # with compute) is amortised as in a serving loop
+        n_e2e = max(args.steps, 20)
         s0.record()
-        for res in stream(host_in[i % 2] for i in range(args.steps)):
+        for res in stream(host_in[i % 2] for i in range(n_e2e)):
             d2h = res.numel() * 8
         s1.record()
         torch.cuda.synchronize()
         barrier()
-        t_e2e = s0.elapsed_time(s1) / 1e3 / args.steps
+        t_e2e = s0.elapsed_time(s1) / 1e3 / n_e2e
         if ws > 1:
             tt = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_e2e = float(tt.item())
         e2e = {"value": images / t_e2e, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": t_e2e * 1e3}
+               "ms_per_step": t_e2e * 1e3, "batches": n_e2e,
+               "api": "engine.evaluate_stream (pinned host batches in, host result bodies out)"}
 
     if rank != 0:
         return
