@@ -45,6 +45,10 @@ const char* fcn_last_error(void);
 int fcn_version(void);
 /* Number of kernels this library has launched in the process (bench evidence). */
 long long fcn_launch_count(void);
+/* Reduction schedule the FP64 NTT uses for a transform of size 2^logn whose
+ * largest limb is qmax: 0 = reduce every third stage (any q < 2^51), 1 = once
+ * per transform, 2 = never (host-only diagnostic; no reference counterpart). */
+int fcn_ntt_f64_schedule(int logn, uint64_t qmax);
 
 /* ---------------------------------------------------------------- rings */
 

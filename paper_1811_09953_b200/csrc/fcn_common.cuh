@@ -244,6 +244,12 @@ __device__ __forceinline__ double fredq(double x, double qi, double q) {
   const double qt = fma(x, qi, M) - M;
   return fma(-qt, q, x);
 }
+// Reduction schedules of the FP64 NTT (ntt_f64.cuh): reduce every value
+// before stage s?  RS 0: s = 3, 6, 9, 12 (any q < 2^51); RS 1: once, before
+// stage logn/2; RS 2: never.  ntt.cu f64_schedule checks the bound.
+__host__ __device__ constexpr bool f64_red_before(int logn, int rs, int s) {
+  return rs == 0 ? (s > 0 && s % 3 == 0) : rs == 1 ? (s == logn / 2) : false;
+}
 // u64 residue (< 2^52) <-> double, bit tricks instead of the slow I2F/F2I.
 __device__ __forceinline__ double u2f(uint64_t x) {
   return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - 4503599627370496.0;

@@ -1281,18 +1281,19 @@ extern "C" int fcn_ctx_create(int device, int n, int k, const uint64_t* primes, 
   // Auxiliary base.  The reference scans find_ntt_primes(n, need//54 + 1,
   // bits=55, exclude=q) (fv.py:99-107); the base only has to make the
   // extended-base CRT of the tensor exact, which needs P > 2nq.  We take
-  // NTT primes just below 2^51 (descending scan, limb primes excluded) so
-  // every extended-base limb runs the FP64 NTT (q < 2^51), with the
-  // smallest count giving P >= 8nq (each prime > 2^50), so |T|/B <= 1/16
-  // (section 5 of DESIGN.md); outputs do not depend on the choice.
+  // the first NTT primes above 2^50 (ascending scan, limb primes excluded),
+  // the smallest count giving P >= 8nq, so |T|/B <= 1/16 (section 5 of
+  // DESIGN.md); outputs do not depend on the choice.  Primes just above 2^50
+  // keep every extended-base limb on the FP64 kernels (q < 2^51) and let the
+  // FP64 NTT reduce once per transform instead of four times (ntt_f64.cuh).
   int nb = 0;
   while ((1 << nb) <= n) ++nb;
   const int need = nb + q.bits() + 3;
   const int count = (need + 49) / 50;
   const uint64_t step = 2ull * (uint64_t)n;
-  uint64_t p = ((1ull << 51) / step) * step + 1;
-  while ((int)x->aux.size() < count && p > (1ull << 50) + step) {
-    p -= step;
+  uint64_t p = ((1ull << 50) / step) * step + 1;
+  while ((int)x->aux.size() < count && p < (1ull << 51) - step) {
+    p += step;
     bool skip = false;
     for (uint64_t qq : x->primes) skip |= qq == p;
     if (!skip && h_is_prime(p)) x->aux.push_back(p);

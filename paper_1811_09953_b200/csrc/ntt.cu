@@ -473,324 +473,6 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
   cp_async_wait_all();
 }
 
-// ================================================================= f64
-// Same three-pass structure as v2, butterflies on the FP64 pipe with signed
-// integer-valued doubles (fcn_common.cuh fmulq/fredq) for limbs q < 2^51.
-// Bounds (q < 2^51): for |Y| <= Bq the quotient rint(Y w/q) is within
-// 1/2 + B/4 of the exact one (|w| <= q/2, two roundings of 2^-53), so a
-// butterfly adds |t| <= (1/2 + B/4) q.  From canonical inputs (B = 1) three
-// stages reach B = 3.86; from a reduced |x| <= q/2 + 1, three stages reach
-// 2.88.  Every value is therefore reduced before stages 3, 6, 9, 12 and
-// nothing ever exceeds 3.86 q < 2^53: all arithmetic is exact.
-
-__device__ __forceinline__ double2 ld_ftw(const double2* p) { return __ldg(p); }
-
-__device__ __forceinline__ void fbfly(double& X, double& Y, const double2& w, double q) {
-  const double t = fmulq(Y, w.x, w.y, q);
-  const double x = X;
-  X = x + t;
-  Y = x - t;
-}
-
-template <int G>
-__device__ __forceinline__ void fred_all(double* x, double q, double qi) {
-#pragma unroll
-  for (int j = 0; j < G; ++j) x[j] = fredq(x[j], qi, q);
-}
-
-template <int R, int S0>
-__device__ __forceinline__ void fwd_ctf(double* x, int b, const double2* __restrict__ tw, double q, double qi) {
-  constexpr int G = 1 << R;
-#pragma unroll
-  for (int u = 0; u < R; ++u) {
-    if (S0 + u > 0 && (S0 + u) % 3 == 0) fred_all<G>(x, q, qi);
-    const int tb = (1 << (S0 + u)) + (b << u);
-    const int h = G >> (u + 1);
-#pragma unroll
-    for (int blk = 0; blk < (1 << u); ++blk) {
-      const double2 w = ld_ftw(tw + tb + blk);
-#pragma unroll
-      for (int jj = 0; jj < h; ++jj) {
-        const int j = blk * 2 * h + jj;
-        fbfly(x[j], x[j + h], w, q);
-      }
-    }
-  }
-}
-
-template <int S0>
-__device__ __forceinline__ void fwd_ctf_last(double* x, int t, int T, const double2* __restrict__ tl, double q,
-                                             double qi) {
-  int off = 0;
-#pragma unroll
-  for (int u = 0; u < 5; ++u) {
-    if (S0 + u > 0 && (S0 + u) % 3 == 0) fred_all<32>(x, q, qi);
-    const int h = 32 >> (u + 1);
-#pragma unroll
-    for (int blk = 0; blk < (1 << u); ++blk) {
-      const double2 w = ld_ftw(tl + off + blk * T + t);
-#pragma unroll
-      for (int jj = 0; jj < h; ++jj) {
-        const int j = blk * 2 * h + jj;
-        fbfly(x[j], x[j + h], w, q);
-      }
-    }
-    off += (1 << u) * T;
-  }
-}
-
-template <int R, int S0>
-__device__ __forceinline__ void inv_ctf(double* x, int o, const double2* __restrict__ tw, double q, double qi) {
-  constexpr int G = 1 << R;
-#pragma unroll
-  for (int u = 0; u < R; ++u) {
-    if (S0 + u > 0 && (S0 + u) % 3 == 0) fred_all<G>(x, q, qi);
-    const int hd = 1 << u;
-    const int tb = (1 << (S0 + u)) + o;
-#pragma unroll
-    for (int jj = 0; jj < hd; ++jj) {
-      const double2 w = ld_ftw(tw + tb + (jj << S0));
-#pragma unroll
-      for (int blk = 0; blk < (G >> (u + 1)); ++blk) {
-        const int j = blk * 2 * hd + jj;
-        fbfly(x[j], x[j + hd], w, q);
-      }
-    }
-  }
-}
-
-template <int LOGN>
-__global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
-    ntt_f64_fwd(uint64_t* __restrict__ data, int64_t n_rows, int period, int offset, const LimbConst* __restrict__ lcs,
-                const double2* __restrict__ tws, const double2* __restrict__ twl, const uint64_t* __restrict__ src,
-                int src_div) {
-  constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
-  extern __shared__ uint64_t sm[];
-  double* fs = reinterpret_cast<double*>(sm);
-  const int tid = threadIdx.x;
-  int64_t row = blockIdx.x;
-  if (row >= n_rows) return;
-  double x[32];  // raw u64 bits of the next row between iterations
-  {
-    const uint64_t* p = src + (row / src_div) * N;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
-  }
-  for (; row < n_rows; row += gridDim.x) {
-    const int limb = offset + (int)(row % period);
-    const LimbConst& c = lcs[limb];
-    const double q = c.fq, qi = c.fqi;
-    const double2* tw = tws + (int64_t)limb * N;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = u2f((uint64_t)__double_as_longlong(x[j]));
-    // pass 1: stages 0..4 on t + j*T (twiddles uniform across the CTA)
-    fwd_ctf<5, 0>(x, 0, tw, q, qi);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) fs[phys(tid + j * T)] = x[j];
-    __syncthreads();
-    if (RM > 0) {
-#pragma unroll
-      for (int i = 0; i < 32 / GM; ++i) {
-        const int g = tid + i * T;
-        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
-#pragma unroll
-        for (int j = 0; j < GM; ++j) x[i * GM + j] = fs[phys(base + j * 32)];
-      }
-#pragma unroll
-      for (int i = 0; i < 32 / GM; ++i) fwd_ctf<(RM > 0 ? RM : 1), 5>(x + i * GM, (tid + i * T) >> 5, tw, q, qi);
-#pragma unroll
-      for (int i = 0; i < 32 / GM; ++i) {
-        const int g = tid + i * T;
-        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
-#pragma unroll
-        for (int j = 0; j < GM; ++j) fs[phys(base + j * 32)] = x[i * GM + j];
-      }
-      __syncthreads();
-    }
-    // pass 3: the last 5 stages on 32 contiguous residues, canonical out
-#pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = fs[tid * 33 + j];
-    fwd_ctf_last<LOGN - 5>(x, tid, T, twl + (int64_t)limb * N, q, qi);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) sm[tid * 33 + j] = f2u_canon(fredq(x[j], qi, q), q);
-    __syncthreads();
-    const int64_t nxt = row + gridDim.x;
-    if (nxt < n_rows) {
-      const uint64_t* p = src + (nxt / src_div) * N;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
-    }
-    ulonglong2* o2 = reinterpret_cast<ulonglong2*>(data + row * N);
-#pragma unroll 4
-    for (int i = tid; i < N / 2; i += T) {
-      ulonglong2 v;
-      v.x = sm[phys(2 * i)];
-      v.y = sm[phys(2 * i + 1)];
-      o2[i] = v;
-    }
-    __syncthreads();
-  }
-}
-
-template <int LOGN>
-__global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
-    ntt_f64_inv(uint64_t* __restrict__ data, int64_t n_rows, int period, int offset, const LimbConst* __restrict__ lcs,
-                const double2* __restrict__ tws, const double2* __restrict__ twists) {
-  constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
-  extern __shared__ uint64_t sm[];
-  double* fs = reinterpret_cast<double*>(sm);
-  const int tid = threadIdx.x;
-  int64_t row = blockIdx.x;
-  if (row >= n_rows) return;
-  {
-    const uint64_t* p = data + row * N;
-    for (int i = tid; i < N; i += T) cp_async8(&sm[phys(i)], p + i);
-    cp_async_commit();
-  }
-  double x[32];
-  for (; row < n_rows; row += gridDim.x) {
-    const int limb = offset + (int)(row % period);
-    const LimbConst& c = lcs[limb];
-    const double q = c.fq, qi = c.fqi;
-    const double2* tw = tws + (int64_t)limb * N;
-    const double2* twist = twists + (int64_t)limb * N;
-    cp_async_wait_all();
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = u2f(sm[tid * 33 + j]);
-    inv_ctf<5, 0>(x, 0, tw, q, qi);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) fs[tid * 33 + j] = x[j];
-    __syncthreads();
-    if (RM > 0) {
-#pragma unroll
-      for (int i = 0; i < 32 / GM; ++i) {
-        const int g = tid + i * T;
-        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
-#pragma unroll
-        for (int j = 0; j < GM; ++j) x[i * GM + j] = fs[phys(base + j * 32)];
-      }
-#pragma unroll
-      for (int i = 0; i < 32 / GM; ++i) inv_ctf<(RM > 0 ? RM : 1), 5>(x + i * GM, (tid + i * T) & 31, tw, q, qi);
-#pragma unroll
-      for (int i = 0; i < 32 / GM; ++i) {
-        const int g = tid + i * T;
-        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
-#pragma unroll
-        for (int j = 0; j < GM; ++j) fs[phys(base + j * 32)] = x[i * GM + j];
-      }
-      __syncthreads();
-    }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = fs[phys(tid + j * T)];
-    __syncthreads();
-    const int64_t nxt = row + gridDim.x;
-    if (nxt < n_rows) {
-      const uint64_t* p = data + nxt * N;
-      for (int i = tid; i < N; i += T) cp_async8(&sm[phys(i)], p + i);
-      cp_async_commit();
-    }
-    inv_ctf<5, LOGN - 5>(x, tid, tw, q, qi);
-    // twist by n^-1 psi^-j, canonicalise, store coalesced
-    uint64_t* p = data + row * N;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const double2 w = ld_ftw(twist + tid + j * T);
-      p[tid + j * T] = f2u_canon(fredq(fmulq(x[j], w.x, w.y, q), qi, q), q);
-    }
-  }
-  cp_async_wait_all();
-}
-
-// Inverse with a fused epilogue out = add + v (SCALE: add + c2 v), out of
-// place.  The epilogue row `add` streams into shared memory with cp.async
-// during the last pass (each thread fetches exactly the residues it will
-// combine, so no barrier is needed); the next input row is prefetched into
-// registers instead (coalesced, as in the forward kernel).
-template <int LOGN, bool SCALE, bool FAN>
-__global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
-    ntt_f64_inv_epi(const uint64_t* __restrict__ data, int64_t n_rows, int period, int offset,
-                    const LimbConst* __restrict__ lcs, const double2* __restrict__ tws,
-                    const double2* __restrict__ twists, const __grid_constant__ NttEpi E) {
-  constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
-  extern __shared__ uint64_t sm[];
-  double* fs = reinterpret_cast<double*>(sm);
-  const int tid = threadIdx.x;
-  int64_t row = blockIdx.x;
-  if (row >= n_rows) return;
-  double x[32];  // raw u64 bits of the next row between iterations
-  {
-    const uint64_t* p = data + row * N;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
-  }
-  for (; row < n_rows; row += gridDim.x) {
-    const int limb = offset + (int)(row % period);
-    const LimbConst& c = lcs[limb];
-    const double q = c.fq, qi = c.fqi;
-    const double2* tw = tws + (int64_t)limb * N;
-    const double2* twist = twists + (int64_t)limb * N;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) sm[phys(tid + j * T)] = (uint64_t)__double_as_longlong(x[j]);
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = u2f(sm[tid * 33 + j]);
-    inv_ctf<5, 0>(x, 0, tw, q, qi);
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < 32; ++j) fs[tid * 33 + j] = x[j];
-    __syncthreads();
-    if (RM > 0) {
-#pragma unroll
-      for (int i = 0; i < 32 / GM; ++i) {
-        const int g = tid + i * T;
-        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
-#pragma unroll
-        for (int j = 0; j < GM; ++j) x[i * GM + j] = fs[phys(base + j * 32)];
-      }
-#pragma unroll
-      for (int i = 0; i < 32 / GM; ++i) inv_ctf<(RM > 0 ? RM : 1), 5>(x + i * GM, (tid + i * T) & 31, tw, q, qi);
-#pragma unroll
-      for (int i = 0; i < 32 / GM; ++i) {
-        const int g = tid + i * T;
-        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
-#pragma unroll
-        for (int j = 0; j < GM; ++j) fs[phys(base + j * 32)] = x[i * GM + j];
-      }
-      __syncthreads();
-    }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = fs[phys(tid + j * T)];
-    {
-      // own slots only: no barrier between these reads and the cp.async writes
-      const uint64_t* pa = E.add + row * N;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) cp_async8(&sm[phys(tid + j * T)], pa + tid + j * T);
-      cp_async_commit();
-    }
-    inv_ctf<5, LOGN - 5>(x, tid, tw, q, qi);
-    cp_async_wait_all();
-    const double c2 = E.fc2[limb], c2q = E.fc2q[limb];
-    uint64_t* po = E.out.dst[0] + row * N;
-    const int nd = E.out.n;
-    // the next row's element j is requested as soon as x[j] is consumed, so
-    // its loads overlap the rest of this epilogue
-    const int64_t nxt = row + gridDim.x;
-    const uint64_t* pn = data + (nxt < n_rows ? nxt : row) * N;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const double2 w = ld_ftw(twist + tid + j * T);
-      double y = fredq(fmulq(x[j], w.x, w.y, q), qi, q);  // |y| <= q/2 + 1
-      if (SCALE) y = fmulq(y, c2, c2q, q);              // |y| < 0.7 q
-      const uint64_t v = f2u_canon(fredq(y + u2f(sm[phys(tid + j * T)]), qi, q), q);
-      po[tid + j * T] = v;
-      if (FAN) {  // fan-out to the peers' buffers
-        for (int d = 1; d < nd; ++d) E.out.dst[d][row * N + tid + j * T] = v;
-      }
-      x[j] = __longlong_as_double((long long)pn[tid + j * T]);
-    }
-  }
-}
 
 // Integer epilogue for the non-FP64 kernels, applied after the transform.
 __global__ void ntt_epi_kernel(const uint64_t* __restrict__ data, int64_t n_rows, int logn, int period, int offset,
@@ -824,19 +506,8 @@ template <int LOGN, bool FWD>
 static const void* v2_ptr() {
   return FWD ? (const void*)ntt_v2_fwd<LOGN> : (const void*)ntt_v2_inv<LOGN>;
 }
-template <int LOGN, bool FWD, int EPI = 0>
-static const void* f64_ptr() {
-  return FWD ? (const void*)ntt_f64_fwd<LOGN>
-             : (EPI == 0 ? (const void*)ntt_f64_inv<LOGN>
-                : EPI == 1 ? (const void*)ntt_f64_inv_epi<LOGN, false, false>
-                : EPI == 2 ? (const void*)ntt_f64_inv_epi<LOGN, true, false>
-                : EPI == 3 ? (const void*)ntt_f64_inv_epi<LOGN, false, true>
-                           : (const void*)ntt_f64_inv_epi<LOGN, true, true>);
-}
-
 static int g_sms = 0;
 static V2Entry g_v2[2][15];
-static V2Entry g_f64[2][15];
 static std::once_flag g_init;
 static cudaError_t g_init_err = cudaSuccess;
 
@@ -863,37 +534,6 @@ static void init_tables() {
       if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fns[f][lg], (1 << lg) / 32, sm);
       if (e != cudaSuccess) g_init_err = e;
       g_v2[f][lg] = {fns[f][lg], occ > 0 ? occ : 1};
-    }
-  }
-  const void* ffns[2][15] = {};
-  ffns[1][10] = f64_ptr<10, true>();
-  ffns[1][11] = f64_ptr<11, true>();
-  ffns[1][12] = f64_ptr<12, true>();
-  ffns[1][13] = f64_ptr<13, true>();
-  ffns[1][14] = f64_ptr<14, true>();
-  ffns[0][10] = f64_ptr<10, false>();
-  ffns[0][11] = f64_ptr<11, false>();
-  ffns[0][12] = f64_ptr<12, false>();
-  ffns[0][13] = f64_ptr<13, false>();
-  ffns[0][14] = f64_ptr<14, false>();
-  for (int f = 0; f < 2; ++f) {
-    for (int lg = 10; lg <= 14; ++lg) {
-      const size_t sm = v2_smem(lg);
-      cudaError_t e = cudaFuncSetAttribute(ffns[f][lg], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      int occ = 0;
-      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ffns[f][lg], (1 << lg) / 32, sm);
-      if (e != cudaSuccess) g_init_err = e;
-      g_f64[f][lg] = {ffns[f][lg], occ > 0 ? occ : 1};
-    }
-  }
-  {
-#define FCN_EPIS(E) f64_ptr<10, false, E>(), f64_ptr<11, false, E>(), f64_ptr<12, false, E>(), \
-                    f64_ptr<13, false, E>(), f64_ptr<14, false, E>()
-    const void* epis[20] = {FCN_EPIS(1), FCN_EPIS(2), FCN_EPIS(3), FCN_EPIS(4)};
-#undef FCN_EPIS
-    for (int i = 0; i < 20; ++i) {
-      cudaError_t e = cudaFuncSetAttribute(epis[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v2_smem(10 + i % 5));
-      if (e != cudaSuccess) g_init_err = e;
     }
   }
   const size_t mx = v1_smem(14);
@@ -953,29 +593,6 @@ static void launch_v2_t(bool fwd, int grid, uint64_t* d, int64_t n_rows, int per
     ntt_v2_inv<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_ict, r->d_twist);
 }
 
-template <int LOGN>
-static void launch_f64_t(bool fwd, int grid, uint64_t* d, int64_t n_rows, int period, int offset, const fcn_ring* r,
-                         cudaStream_t st, const uint64_t* src, int src_div, const NttEpi* epi) {
-  const size_t sm = v2_smem(LOGN);
-  if (fwd)
-    ntt_f64_fwd<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_ffwd, r->d_ffl, src,
-                                                          src_div);
-  else if (!epi || epi->mode == 0)
-    ntt_f64_inv<LOGN><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict, r->d_ftwist);
-  else if (epi->out.n == 1 && epi->mode == 1)
-    ntt_f64_inv_epi<LOGN, false, false><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc,
-                                                                           r->d_fict, r->d_ftwist, *epi);
-  else if (epi->out.n == 1)
-    ntt_f64_inv_epi<LOGN, true, false><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc,
-                                                                          r->d_fict, r->d_ftwist, *epi);
-  else if (epi->mode == 1)
-    ntt_f64_inv_epi<LOGN, false, true><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc,
-                                                                          r->d_fict, r->d_ftwist, *epi);
-  else
-    ntt_f64_inv_epi<LOGN, true, true><<<grid, (1 << LOGN) / 32, sm, st>>>(d, n_rows, period, offset, r->d_lc,
-                                                                         r->d_fict, r->d_ftwist, *epi);
-}
-
 static int launch_epi_int(const fcn_ring* r, const uint64_t* d, int64_t n_rows, int period, int offset, cudaStream_t st,
                           const NttEpi* epi) {
   if (!epi || epi->mode == 0) return FCN_OK;
@@ -983,6 +600,41 @@ static int launch_epi_int(const fcn_ring* r, const uint64_t* d, int64_t n_rows, 
   FCN_LAUNCH_CHECK("ntt_epi_kernel");
   return FCN_OK;
 }
+
+template <int RS>
+int launch_ntt_f64(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st,
+                   const uint64_t* src, int src_div, const NttEpi* epi, int sms);  // ntt_f64.cuh
+
+// The FP64 kernels' value bound (ntt_f64.cuh): a butterfly on |Y| <= B q
+// adds |t| <= (1/2 + B q 2^-53) q, a reduction leaves |x| <= q/2 + 2^-40 q,
+// inputs are canonical (B = 1), and every value must stay below 2^53.
+// Returns the cheapest schedule (2, then 1) whose bound holds for limbs up
+// to qmax, else 0 (proved for every q < 2^51).  FCN_NTT_RS=0/1/2 caps it.
+static int g_rs_cap = -1;
+int f64_schedule(int logn, uint64_t qmax) {
+  if (g_rs_cap < 0) {
+    const char* ev = getenv("FCN_NTT_RS");
+    g_rs_cap = (ev && ev[0] >= '0' && ev[0] <= '2') ? ev[0] - '0' : 2;
+  }
+  const double e = ((double)qmax + 1.0) * 0x1p-53 * (1.0 + 1e-12);
+  for (int rs = g_rs_cap; rs >= 1; --rs) {
+    double B = 1.0;
+    bool ok = true;
+    for (int s = 0; s < logn && ok; ++s) {
+      if (f64_red_before(logn, rs, s)) B = 0.5 + 1e-9;
+      B = B + 0.5 + B * e + 1e-9;
+      ok = B * e < 1.0;
+    }
+    if (ok) return rs;
+  }
+  return 0;
+}
+
+}  // namespace fcn
+
+extern "C" int fcn_ntt_f64_schedule(int logn, uint64_t qmax) { return fcn::f64_schedule(logn, qmax); }
+
+namespace fcn {
 
 static int g_force_int = -1;  // FCN_NTT_INT=1 selects the integer kernels (A/B tests)
 
@@ -1018,18 +670,13 @@ int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int o
     return rc ? rc : launch_epi_int(r, d, n_rows, period, offset, st, epi);
   }
   if (f64) {
-    const V2Entry& e = g_f64[fwd ? 1 : 0][logn];
-    int64_t grid = (int64_t)g_sms * e.ctas_per_sm;
-    if (grid > n_rows) grid = n_rows;
-    switch (logn) {
-      case 10: launch_f64_t<10>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div, epi); break;
-      case 11: launch_f64_t<11>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div, epi); break;
-      case 12: launch_f64_t<12>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div, epi); break;
-      case 13: launch_f64_t<13>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div, epi); break;
-      default: launch_f64_t<14>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div, epi); break;
+    uint64_t qmax = 0;
+    for (int l = 0; l < period; ++l) qmax = r->primes[offset + l] > qmax ? r->primes[offset + l] : qmax;
+    switch (f64_schedule(logn, qmax)) {
+      case 2: return launch_ntt_f64<2>(r, d, n_rows, period, offset, fwd, st, src, src_div, epi, g_sms);
+      case 1: return launch_ntt_f64<1>(r, d, n_rows, period, offset, fwd, st, src, src_div, epi, g_sms);
+      default: return launch_ntt_f64<0>(r, d, n_rows, period, offset, fwd, st, src, src_div, epi, g_sms);
     }
-    FCN_LAUNCH_CHECK(fwd ? "ntt_f64_fwd" : "ntt_f64_inv");
-    return FCN_OK;
   }
   const V2Entry& e = g_v2[fwd ? 1 : 0][logn];
   int64_t grid = (int64_t)g_sms * e.ctas_per_sm;

@@ -1,0 +1,418 @@
+// libfcn: FP64-pipe batched negacyclic NTT kernels (replace reference
+// ring.py:199-255 for limbs q < 2^51), templated on the transform size and on
+// the reduction schedule RS.  Each schedule is instantiated in its own
+// translation unit (ntt_f64_s{0,1,2}.cu) so the three compile in parallel.
+#pragma once
+
+#include <mutex>
+
+#include "fcn_common.cuh"
+
+#ifndef FCN_NTT_MINB
+#define FCN_NTT_MINB(LOGN) (16384 / (1 << (LOGN)))
+#endif
+
+namespace fcn {
+
+__device__ __forceinline__ int phys(int i) { return i + (i >> 5); }
+
+// ================================================================= f64
+// Same three-pass structure as v2, butterflies on the FP64 pipe with signed
+// integer-valued doubles (fcn_common.cuh fmulq/fredq) for limbs q < 2^51.
+// Bounds (q < 2^51): for |Y| <= Bq the quotient rint(Y w/q) is within
+// 1/2 + B/4 of the exact one (|w| <= q/2, two roundings of 2^-53), so a
+// butterfly adds |t| <= (1/2 + B/4) q.  From canonical inputs (B = 1) three
+// stages reach B = 3.86; from a reduced |x| <= q/2 + 1, three stages reach
+// 2.88.  Every value is therefore reduced before stages 3, 6, 9, 12 and
+// nothing ever exceeds 3.86 q < 2^53: all arithmetic is exact (schedule
+// RS = 0).  The quotient error is really 1/2 + B q 2^-53, so smaller limbs
+// allow fewer reductions: RS = 1 reduces once, before stage LOGN/2, and
+// RS = 2 never; launch_ntt (ntt.cu f64_schedule) proves the bound for the
+// launch's largest limb before picking either (q just above 2^50: RS = 1,
+// one reduction per transform instead of four).
+
+__device__ __forceinline__ double2 ld_ftw(const double2* p) { return __ldg(p); }
+
+__device__ __forceinline__ void fbfly(double& X, double& Y, const double2& w, double q) {
+  const double t = fmulq(Y, w.x, w.y, q);
+  const double x = X;
+  X = x + t;
+  Y = x - t;
+}
+
+template <int G>
+__device__ __forceinline__ void fred_all(double* x, double q, double qi) {
+#pragma unroll
+  for (int j = 0; j < G; ++j) x[j] = fredq(x[j], qi, q);
+}
+
+template <int LOGN, int RS, int R, int S0>
+__device__ __forceinline__ void fwd_ctf(double* x, int b, const double2* __restrict__ tw, double q, double qi) {
+  constexpr int G = 1 << R;
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    if (f64_red_before(LOGN, RS, S0 + u)) fred_all<G>(x, q, qi);
+    const int tb = (1 << (S0 + u)) + (b << u);
+    const int h = G >> (u + 1);
+#pragma unroll
+    for (int blk = 0; blk < (1 << u); ++blk) {
+      const double2 w = ld_ftw(tw + tb + blk);
+#pragma unroll
+      for (int jj = 0; jj < h; ++jj) {
+        const int j = blk * 2 * h + jj;
+        fbfly(x[j], x[j + h], w, q);
+      }
+    }
+  }
+}
+
+template <int LOGN, int RS, int S0>
+__device__ __forceinline__ void fwd_ctf_last(double* x, int t, int T, const double2* __restrict__ tl, double q,
+                                             double qi) {
+  int off = 0;
+#pragma unroll
+  for (int u = 0; u < 5; ++u) {
+    if (f64_red_before(LOGN, RS, S0 + u)) fred_all<32>(x, q, qi);
+    const int h = 32 >> (u + 1);
+#pragma unroll
+    for (int blk = 0; blk < (1 << u); ++blk) {
+      const double2 w = ld_ftw(tl + off + blk * T + t);
+#pragma unroll
+      for (int jj = 0; jj < h; ++jj) {
+        const int j = blk * 2 * h + jj;
+        fbfly(x[j], x[j + h], w, q);
+      }
+    }
+    off += (1 << u) * T;
+  }
+}
+
+template <int LOGN, int RS, int R, int S0>
+__device__ __forceinline__ void inv_ctf(double* x, int o, const double2* __restrict__ tw, double q, double qi) {
+  constexpr int G = 1 << R;
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    if (f64_red_before(LOGN, RS, S0 + u)) fred_all<G>(x, q, qi);
+    const int hd = 1 << u;
+    const int tb = (1 << (S0 + u)) + o;
+#pragma unroll
+    for (int jj = 0; jj < hd; ++jj) {
+      const double2 w = ld_ftw(tw + tb + (jj << S0));
+#pragma unroll
+      for (int blk = 0; blk < (G >> (u + 1)); ++blk) {
+        const int j = blk * 2 * hd + jj;
+        fbfly(x[j], x[j + hd], w, q);
+      }
+    }
+  }
+}
+
+template <int LOGN, int RS>
+__global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
+    ntt_f64_fwd(uint64_t* __restrict__ data, int64_t n_rows, int period, int offset, const LimbConst* __restrict__ lcs,
+                const double2* __restrict__ tws, const double2* __restrict__ twl, const uint64_t* __restrict__ src,
+                int src_div) {
+  constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
+  extern __shared__ uint64_t sm[];
+  double* fs = reinterpret_cast<double*>(sm);
+  const int tid = threadIdx.x;
+  int64_t row = blockIdx.x;
+  if (row >= n_rows) return;
+  double x[32];  // raw u64 bits of the next row between iterations
+  {
+    const uint64_t* p = src + (row / src_div) * N;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
+  }
+  for (; row < n_rows; row += gridDim.x) {
+    const int limb = offset + (int)(row % period);
+    const LimbConst& c = lcs[limb];
+    const double q = c.fq, qi = c.fqi;
+    const double2* tw = tws + (int64_t)limb * N;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = u2f((uint64_t)__double_as_longlong(x[j]));
+    // pass 1: stages 0..4 on t + j*T (twiddles uniform across the CTA)
+    fwd_ctf<LOGN, RS, 5, 0>(x, 0, tw, q, qi);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) fs[phys(tid + j * T)] = x[j];
+    __syncthreads();
+    if (RM > 0) {
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) {
+        const int g = tid + i * T;
+        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
+#pragma unroll
+        for (int j = 0; j < GM; ++j) x[i * GM + j] = fs[phys(base + j * 32)];
+      }
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) fwd_ctf<LOGN, RS, (RM > 0 ? RM : 1), 5>(x + i * GM, (tid + i * T) >> 5, tw, q, qi);
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) {
+        const int g = tid + i * T;
+        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
+#pragma unroll
+        for (int j = 0; j < GM; ++j) fs[phys(base + j * 32)] = x[i * GM + j];
+      }
+      __syncthreads();
+    }
+    // pass 3: the last 5 stages on 32 contiguous residues, canonical out
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = fs[tid * 33 + j];
+    fwd_ctf_last<LOGN, RS, LOGN - 5>(x, tid, T, twl + (int64_t)limb * N, q, qi);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) sm[tid * 33 + j] = f2u_canon(fredq(x[j], qi, q), q);
+    __syncthreads();
+    const int64_t nxt = row + gridDim.x;
+    if (nxt < n_rows) {
+      const uint64_t* p = src + (nxt / src_div) * N;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
+    }
+    ulonglong2* o2 = reinterpret_cast<ulonglong2*>(data + row * N);
+#pragma unroll 4
+    for (int i = tid; i < N / 2; i += T) {
+      ulonglong2 v;
+      v.x = sm[phys(2 * i)];
+      v.y = sm[phys(2 * i + 1)];
+      o2[i] = v;
+    }
+    __syncthreads();
+  }
+}
+
+template <int LOGN, int RS>
+__global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
+    ntt_f64_inv(uint64_t* __restrict__ data, int64_t n_rows, int period, int offset, const LimbConst* __restrict__ lcs,
+                const double2* __restrict__ tws, const double2* __restrict__ twists) {
+  constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
+  extern __shared__ uint64_t sm[];
+  double* fs = reinterpret_cast<double*>(sm);
+  const int tid = threadIdx.x;
+  int64_t row = blockIdx.x;
+  if (row >= n_rows) return;
+  {
+    const uint64_t* p = data + row * N;
+    for (int i = tid; i < N; i += T) cp_async8(&sm[phys(i)], p + i);
+    cp_async_commit();
+  }
+  double x[32];
+  for (; row < n_rows; row += gridDim.x) {
+    const int limb = offset + (int)(row % period);
+    const LimbConst& c = lcs[limb];
+    const double q = c.fq, qi = c.fqi;
+    const double2* tw = tws + (int64_t)limb * N;
+    const double2* twist = twists + (int64_t)limb * N;
+    cp_async_wait_all();
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = u2f(sm[tid * 33 + j]);
+    inv_ctf<LOGN, RS, 5, 0>(x, 0, tw, q, qi);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) fs[tid * 33 + j] = x[j];
+    __syncthreads();
+    if (RM > 0) {
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) {
+        const int g = tid + i * T;
+        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
+#pragma unroll
+        for (int j = 0; j < GM; ++j) x[i * GM + j] = fs[phys(base + j * 32)];
+      }
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) inv_ctf<LOGN, RS, (RM > 0 ? RM : 1), 5>(x + i * GM, (tid + i * T) & 31, tw, q, qi);
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) {
+        const int g = tid + i * T;
+        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
+#pragma unroll
+        for (int j = 0; j < GM; ++j) fs[phys(base + j * 32)] = x[i * GM + j];
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = fs[phys(tid + j * T)];
+    __syncthreads();
+    const int64_t nxt = row + gridDim.x;
+    if (nxt < n_rows) {
+      const uint64_t* p = data + nxt * N;
+      for (int i = tid; i < N; i += T) cp_async8(&sm[phys(i)], p + i);
+      cp_async_commit();
+    }
+    inv_ctf<LOGN, RS, 5, LOGN - 5>(x, tid, tw, q, qi);
+    // twist by n^-1 psi^-j, canonicalise, store coalesced
+    uint64_t* p = data + row * N;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double2 w = ld_ftw(twist + tid + j * T);
+      p[tid + j * T] = f2u_canon(fredq(fmulq(x[j], w.x, w.y, q), qi, q), q);
+    }
+  }
+  cp_async_wait_all();
+}
+
+// Inverse with a fused epilogue out = add + v (SCALE: add + c2 v), out of
+// place.  The epilogue row `add` streams into shared memory with cp.async
+// during the last pass (each thread fetches exactly the residues it will
+// combine, so no barrier is needed); the next input row is prefetched into
+// registers instead (coalesced, as in the forward kernel).
+template <int LOGN, int RS, bool SCALE, bool FAN>
+__global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
+    ntt_f64_inv_epi(const uint64_t* __restrict__ data, int64_t n_rows, int period, int offset,
+                    const LimbConst* __restrict__ lcs, const double2* __restrict__ tws,
+                    const double2* __restrict__ twists, const __grid_constant__ NttEpi E) {
+  constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
+  extern __shared__ uint64_t sm[];
+  double* fs = reinterpret_cast<double*>(sm);
+  const int tid = threadIdx.x;
+  int64_t row = blockIdx.x;
+  if (row >= n_rows) return;
+  double x[32];  // raw u64 bits of the next row between iterations
+  {
+    const uint64_t* p = data + row * N;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
+  }
+  for (; row < n_rows; row += gridDim.x) {
+    const int limb = offset + (int)(row % period);
+    const LimbConst& c = lcs[limb];
+    const double q = c.fq, qi = c.fqi;
+    const double2* tw = tws + (int64_t)limb * N;
+    const double2* twist = twists + (int64_t)limb * N;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) sm[phys(tid + j * T)] = (uint64_t)__double_as_longlong(x[j]);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = u2f(sm[tid * 33 + j]);
+    inv_ctf<LOGN, RS, 5, 0>(x, 0, tw, q, qi);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) fs[tid * 33 + j] = x[j];
+    __syncthreads();
+    if (RM > 0) {
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) {
+        const int g = tid + i * T;
+        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
+#pragma unroll
+        for (int j = 0; j < GM; ++j) x[i * GM + j] = fs[phys(base + j * 32)];
+      }
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) inv_ctf<LOGN, RS, (RM > 0 ? RM : 1), 5>(x + i * GM, (tid + i * T) & 31, tw, q, qi);
+#pragma unroll
+      for (int i = 0; i < 32 / GM; ++i) {
+        const int g = tid + i * T;
+        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
+#pragma unroll
+        for (int j = 0; j < GM; ++j) fs[phys(base + j * 32)] = x[i * GM + j];
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = fs[phys(tid + j * T)];
+    {
+      // own slots only: no barrier between these reads and the cp.async writes
+      const uint64_t* pa = E.add + row * N;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) cp_async8(&sm[phys(tid + j * T)], pa + tid + j * T);
+      cp_async_commit();
+    }
+    inv_ctf<LOGN, RS, 5, LOGN - 5>(x, tid, tw, q, qi);
+    cp_async_wait_all();
+    const double c2 = E.fc2[limb], c2q = E.fc2q[limb];
+    uint64_t* po = E.out.dst[0] + row * N;
+    const int nd = E.out.n;
+    // the next row's element j is requested as soon as x[j] is consumed, so
+    // its loads overlap the rest of this epilogue
+    const int64_t nxt = row + gridDim.x;
+    const uint64_t* pn = data + (nxt < n_rows ? nxt : row) * N;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double2 w = ld_ftw(twist + tid + j * T);
+      double y = fredq(fmulq(x[j], w.x, w.y, q), qi, q);  // |y| <= q/2 + 1
+      if (SCALE) y = fmulq(y, c2, c2q, q);              // |y| < 0.7 q
+      const uint64_t v = f2u_canon(fredq(y + u2f(sm[phys(tid + j * T)]), qi, q), q);
+      po[tid + j * T] = v;
+      if (FAN) {  // fan-out to the peers' buffers
+        for (int d = 1; d < nd; ++d) E.out.dst[d][row * N + tid + j * T] = v;
+      }
+      x[j] = __longlong_as_double((long long)pn[tid + j * T]);
+    }
+  }
+}
+
+// ============================================================== dispatch
+
+// Resident CTAs per SM of one kernel (dynamic smem attribute set once).
+template <int LOGN, int RS, int V>
+struct F64Occ {
+  static int get(const void* fn, size_t smem, cudaError_t* err) {
+    static cudaError_t e0 = cudaSuccess;
+    static const int occ = [&] {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int o = 0;
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, (1 << LOGN) / 32, smem);
+      e0 = e;
+      return o > 0 ? o : 1;
+    }();
+    *err = e0;
+    return occ;
+  }
+};
+
+template <int LOGN, int RS>
+static int f64_launch_t(bool fwd, int sms, uint64_t* d, int64_t n_rows, int period, int offset, const fcn_ring* r,
+                        cudaStream_t st, const uint64_t* src, int src_div, const NttEpi* epi) {
+  constexpr int threads = (1 << LOGN) / 32;
+  const size_t sm = (size_t)((1 << LOGN) + (1 << LOGN) / 32 + 2) * sizeof(uint64_t);
+  cudaError_t err = cudaSuccess;
+  auto grid_of = [&](int occ) {
+    int64_t g = (int64_t)sms * occ;
+    return (int)(g > n_rows ? n_rows : g);
+  };
+  if (fwd) {
+    const int g = grid_of(F64Occ<LOGN, RS, 0>::get((const void*)ntt_f64_fwd<LOGN, RS>, sm, &err));
+    if (err != cudaSuccess) return check_cuda(err, "ntt_f64_fwd attributes");
+    ntt_f64_fwd<LOGN, RS><<<g, threads, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_ffwd, r->d_ffl, src, src_div);
+  } else if (!epi || epi->mode == 0) {
+    const int g = grid_of(F64Occ<LOGN, RS, 1>::get((const void*)ntt_f64_inv<LOGN, RS>, sm, &err));
+    if (err != cudaSuccess) return check_cuda(err, "ntt_f64_inv attributes");
+    ntt_f64_inv<LOGN, RS><<<g, threads, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict, r->d_ftwist);
+  } else if (epi->out.n == 1 && epi->mode == 1) {
+    const int g = grid_of(F64Occ<LOGN, RS, 2>::get((const void*)ntt_f64_inv_epi<LOGN, RS, false, false>, sm, &err));
+    if (err != cudaSuccess) return check_cuda(err, "ntt_f64_inv_epi attributes");
+    ntt_f64_inv_epi<LOGN, RS, false, false><<<g, threads, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict,
+                                                                    r->d_ftwist, *epi);
+  } else if (epi->out.n == 1) {
+    const int g = grid_of(F64Occ<LOGN, RS, 3>::get((const void*)ntt_f64_inv_epi<LOGN, RS, true, false>, sm, &err));
+    if (err != cudaSuccess) return check_cuda(err, "ntt_f64_inv_epi attributes");
+    ntt_f64_inv_epi<LOGN, RS, true, false><<<g, threads, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict,
+                                                                   r->d_ftwist, *epi);
+  } else if (epi->mode == 1) {
+    const int g = grid_of(F64Occ<LOGN, RS, 4>::get((const void*)ntt_f64_inv_epi<LOGN, RS, false, true>, sm, &err));
+    if (err != cudaSuccess) return check_cuda(err, "ntt_f64_inv_epi attributes");
+    ntt_f64_inv_epi<LOGN, RS, false, true><<<g, threads, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict,
+                                                                   r->d_ftwist, *epi);
+  } else {
+    const int g = grid_of(F64Occ<LOGN, RS, 5>::get((const void*)ntt_f64_inv_epi<LOGN, RS, true, true>, sm, &err));
+    if (err != cudaSuccess) return check_cuda(err, "ntt_f64_inv_epi attributes");
+    ntt_f64_inv_epi<LOGN, RS, true, true><<<g, threads, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict,
+                                                                  r->d_ftwist, *epi);
+  }
+  FCN_LAUNCH_CHECK(fwd ? "ntt_f64_fwd" : "ntt_f64_inv");
+  return FCN_OK;
+}
+
+template <int RS>
+int launch_ntt_f64(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st,
+                   const uint64_t* src, int src_div, const NttEpi* epi, int sms) {
+  switch (r->logn) {
+    case 10: return f64_launch_t<10, RS>(fwd, sms, d, n_rows, period, offset, r, st, src, src_div, epi);
+    case 11: return f64_launch_t<11, RS>(fwd, sms, d, n_rows, period, offset, r, st, src, src_div, epi);
+    case 12: return f64_launch_t<12, RS>(fwd, sms, d, n_rows, period, offset, r, st, src, src_div, epi);
+    case 13: return f64_launch_t<13, RS>(fwd, sms, d, n_rows, period, offset, r, st, src, src_div, epi);
+    case 14: return f64_launch_t<14, RS>(fwd, sms, d, n_rows, period, offset, r, st, src, src_div, epi);
+    default: return set_error(FCN_ERR_ARG, "FP64 NTT: unsupported log n %d", r->logn);
+  }
+}
+
+}  // namespace fcn

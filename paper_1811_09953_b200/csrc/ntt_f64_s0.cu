@@ -1,0 +1,7 @@
+// libfcn: FP64 NTT kernels, reduction schedule RS = 0 (see ntt_f64.cuh).
+#include "ntt_f64.cuh"
+
+namespace fcn {
+template int launch_ntt_f64<0>(const fcn_ring*, uint64_t*, int64_t, int, int, bool, cudaStream_t, const uint64_t*, int,
+                                 const NttEpi*, int);
+}  // namespace fcn

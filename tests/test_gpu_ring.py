@@ -74,21 +74,63 @@ def _primes_below_2_51(n, count):
     return tuple(out)
 
 
-@pytest.mark.parametrize("n", [1024, 8192, 16384])
-def test_ntt_fp64_extreme_values_near_2_51(R, n):
-    """FP64 NTT (q < 2^51) on rows that maximise every intermediate:
-    all q-1, all (q-1)/2, all (q+1)/2, alternating 0 / q-1, and random."""
-    primes = _primes_below_2_51(n, 2)
-    ctx = R.RingContext.create(n, primes)
+def _largest_primes_with_schedule(n, rs, count):
+    """The largest NTT primes for which the FP64 NTT picks reduction
+    schedule rs (ntt.cu f64_schedule): the tightest case of its bound."""
+    from oracle import nt
+    from paper_1811_09953_b200 import _lib
+
+    L = _lib.load()
+    logn = n.bit_length() - 1
+    lo, hi = 1 << 30, (1 << 51) - 1
+    while hi - lo > 1:  # largest q with schedule >= rs
+        mid = (lo + hi) // 2
+        if L.fcn_ntt_f64_schedule(logn, mid) >= rs:
+            lo = mid
+        else:
+            hi = mid
+    step = 2 * n
+    p = (lo // step) * step + 1
+    out = []
+    while len(out) < count:
+        if p <= lo and nt.is_prime(p) and L.fcn_ntt_f64_schedule(logn, p) == rs:
+            out.append(p)
+        p -= step
+    return tuple(out)
+
+
+def _extreme_rows(n, primes):
     rng = np.random.default_rng(n)
-    cases = [
+    return [
         [np.full(n, q - 1, dtype=np.uint64) for q in primes],
         [np.full(n, (q - 1) // 2, dtype=np.uint64) for q in primes],
         [np.full(n, (q + 1) // 2, dtype=np.uint64) for q in primes],
         [np.where(np.arange(n) % 2 == 0, 0, q - 1).astype(np.uint64) for q in primes],
         [rng.integers(0, q, n, dtype=np.uint64) for q in primes],
     ]
-    for rows in cases:
+
+
+@pytest.mark.parametrize("n", [1024, 8192, 16384])
+def test_ntt_fp64_extreme_values_near_2_51(R, n):
+    """FP64 NTT (q < 2^51) on rows that maximise every intermediate:
+    all q-1, all (q-1)/2, all (q+1)/2, alternating 0 / q-1, and random."""
+    primes = _primes_below_2_51(n, 2)
+    ctx = R.RingContext.create(n, primes)
+    for rows in _extreme_rows(n, primes):
+        x = np.stack(rows)
+        assert np.array_equal(R.ntt_forward(R.RingPoly(ctx, x)).host(), orn.ntt(x, primes))
+        assert np.array_equal(R.ntt_inverse(R.RingPoly(ctx, x, R.NTT)).host(), orn.intt(x, primes))
+
+
+@pytest.mark.parametrize("rs", [1, 2])
+@pytest.mark.parametrize("n", [1024, 2048, 4096, 8192, 16384])
+def test_ntt_fp64_reduced_schedules_at_their_limit(R, n, rs):
+    """The cheaper FP64 reduction schedules (one reduction per transform,
+    none) on the largest primes that select them, with extreme rows; also
+    the epilogue inverse through mul_ct is covered by the cfg tests."""
+    primes = _largest_primes_with_schedule(n, rs, 2)
+    ctx = R.RingContext.create(n, primes)
+    for rows in _extreme_rows(n, primes):
         x = np.stack(rows)
         assert np.array_equal(R.ntt_forward(R.RingPoly(ctx, x)).host(), orn.ntt(x, primes))
         assert np.array_equal(R.ntt_inverse(R.RingPoly(ctx, x, R.NTT)).host(), orn.intt(x, primes))
