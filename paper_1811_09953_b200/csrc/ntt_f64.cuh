@@ -68,7 +68,7 @@ __device__ __forceinline__ void fwd_ctf(double* x, int b, const double2* __restr
 
 template <int LOGN, int RS, int S0>
 __device__ __forceinline__ void fwd_ctf_last(double* x, int t, int T, const double2* __restrict__ tl, double q,
-                                             double qi) {
+                                             double qi, double2 w0) {
   int off = 0;
 #pragma unroll
   for (int u = 0; u < 5; ++u) {
@@ -76,7 +76,7 @@ __device__ __forceinline__ void fwd_ctf_last(double* x, int t, int T, const doub
     const int h = 32 >> (u + 1);
 #pragma unroll
     for (int blk = 0; blk < (1 << u); ++blk) {
-      const double2 w = ld_ftw(tl + off + blk * T + t);
+      const double2 w = u == 0 ? w0 : ld_ftw(tl + off + blk * T + t);
 #pragma unroll
       for (int jj = 0; jj < h; ++jj) {
         const int j = blk * 2 * h + jj;
@@ -87,8 +87,9 @@ __device__ __forceinline__ void fwd_ctf_last(double* x, int t, int T, const doub
   }
 }
 
-template <int LOGN, int RS, int R, int S0>
-__device__ __forceinline__ void inv_ctf(double* x, int o, const double2* __restrict__ tw, double q, double qi) {
+template <int LOGN, int RS, int R, int S0, bool PRE = false>
+__device__ __forceinline__ void inv_ctf(double* x, int o, const double2* __restrict__ tw, double q, double qi,
+                                        double2 w0 = double2{}) {
   constexpr int G = 1 << R;
 #pragma unroll
   for (int u = 0; u < R; ++u) {
@@ -97,7 +98,7 @@ __device__ __forceinline__ void inv_ctf(double* x, int o, const double2* __restr
     const int tb = (1 << (S0 + u)) + o;
 #pragma unroll
     for (int jj = 0; jj < hd; ++jj) {
-      const double2 w = ld_ftw(tw + tb + (jj << S0));
+      const double2 w = (PRE && u == 0) ? w0 : ld_ftw(tw + tb + (jj << S0));
 #pragma unroll
       for (int blk = 0; blk < (G >> (u + 1)); ++blk) {
         const int j = blk * 2 * hd + jj;
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
   if (row >= n_rows) return;
   double x[32];  // raw u64 bits of the next row between iterations
   {
-    const uint64_t* p = src + (row / src_div) * N;
+    const uint64_t* p = src + (src_div == 1 ? row : row / src_div) * N;
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
   }
@@ -133,6 +134,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     for (int j = 0; j < 32; ++j) x[j] = u2f((uint64_t)__double_as_longlong(x[j]));
     // pass 1: stages 0..4 on t + j*T (twiddles uniform across the CTA)
     fwd_ctf<LOGN, RS, 5, 0>(x, 0, tw, q, qi);
+    __syncthreads();  // every warp has copied out the previous row
 #pragma unroll
     for (int j = 0; j < 32; ++j) fs[phys(tid + j * T)] = x[j];
     __syncthreads();
@@ -153,30 +155,36 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 #pragma unroll
         for (int j = 0; j < GM; ++j) fs[phys(base + j * 32)] = x[i * GM + j];
       }
-      __syncthreads();
     }
+    // the first twiddle of pass 3 is requested before the barrier (its L2
+    // latency was exposed at the start of the pass)
+    const double2 w3 = ld_ftw(twl + (int64_t)limb * N + tid);
+    if (RM > 0) __syncthreads();
     // pass 3: the last 5 stages on 32 contiguous residues, canonical out
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = fs[tid * 33 + j];
-    fwd_ctf_last<LOGN, RS, LOGN - 5>(x, tid, T, twl + (int64_t)limb * N, q, qi);
+    fwd_ctf_last<LOGN, RS, LOGN - 5>(x, tid, T, twl + (int64_t)limb * N, q, qi, w3);
 #pragma unroll
     for (int j = 0; j < 32; ++j) sm[tid * 33 + j] = f2u_canon(fredq(x[j], qi, q), q);
-    __syncthreads();
+    // A warp's 32 threads own residues [1024 w, 1024 w + 1024): it copies
+    // them out coalesced on its own (no CTA barrier), while the next row's
+    // loads are in flight.
+    __syncwarp();
+    ulonglong2* o2 = reinterpret_cast<ulonglong2*>(data + row * N) + (tid & ~31) * 16 + (tid & 31);
+    const uint64_t* sw = sm + (tid & ~31) * 33 + 2 * (tid & 31) + ((tid & 31) >> 4);
     const int64_t nxt = row + gridDim.x;
     if (nxt < n_rows) {
-      const uint64_t* p = src + (nxt / src_div) * N;
+      const uint64_t* p = src + (src_div == 1 ? nxt : nxt / src_div) * N;
 #pragma unroll
       for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
     }
-    ulonglong2* o2 = reinterpret_cast<ulonglong2*>(data + row * N);
-#pragma unroll 4
-    for (int i = tid; i < N / 2; i += T) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {  // pair 32 i + lane of this warp's block: phys offset 66 i
       ulonglong2 v;
-      v.x = sm[phys(2 * i)];
-      v.y = sm[phys(2 * i + 1)];
-      o2[i] = v;
+      v.x = sw[66 * i];
+      v.y = sw[66 * i + 1];
+      o2[32 * i] = v;
     }
-    __syncthreads();
   }
 }
 
@@ -227,8 +235,9 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 #pragma unroll
         for (int j = 0; j < GM; ++j) fs[phys(base + j * 32)] = x[i * GM + j];
       }
-      __syncthreads();
     }
+    const double2 w3 = ld_ftw(tw + (1 << (LOGN - 5)) + tid);  // pass 3's first twiddle, before the barrier
+    if (RM > 0) __syncthreads();
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = fs[phys(tid + j * T)];
     __syncthreads();
@@ -238,7 +247,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
       for (int i = tid; i < N; i += T) cp_async8(&sm[phys(i)], p + i);
       cp_async_commit();
     }
-    inv_ctf<LOGN, RS, 5, LOGN - 5>(x, tid, tw, q, qi);
+    inv_ctf<LOGN, RS, 5, LOGN - 5, true>(x, tid, tw, q, qi, w3);
     // twist by n^-1 psi^-j, canonicalise, store coalesced
     uint64_t* p = data + row * N;
 #pragma unroll
@@ -305,8 +314,9 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 #pragma unroll
         for (int j = 0; j < GM; ++j) fs[phys(base + j * 32)] = x[i * GM + j];
       }
-      __syncthreads();
     }
+    const double2 w3 = ld_ftw(tw + (1 << (LOGN - 5)) + tid);  // pass 3's first twiddle, before the barrier
+    if (RM > 0) __syncthreads();
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = fs[phys(tid + j * T)];
     {
@@ -316,7 +326,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
       for (int j = 0; j < 32; ++j) cp_async8(&sm[phys(tid + j * T)], pa + tid + j * T);
       cp_async_commit();
     }
-    inv_ctf<LOGN, RS, 5, LOGN - 5>(x, tid, tw, q, qi);
+    inv_ctf<LOGN, RS, 5, LOGN - 5, true>(x, tid, tw, q, qi, w3);
     cp_async_wait_all();
     const double c2 = E.fc2[limb], c2q = E.fc2q[limb];
     uint64_t* po = E.out.dst[0] + row * N;
