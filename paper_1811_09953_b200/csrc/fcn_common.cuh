@@ -237,6 +237,15 @@ __device__ __forceinline__ double fmulq_m(double a, double w, double wq, double 
   const double qt = fma(a, wq, M) - M;
   return fma(-qt, q, h) + l;
 }
+// a b mod q for |a|, |b| <= q/2 + small (q < 2^51): |a b / q| < 2^49, so the
+// magic-constant quotient is exact to 1/2 and the result is |.| < 0.6 q.
+__device__ __forceinline__ double fprod(double a, double b, double q, double qi) {
+  const double M = 6755399441055744.0;
+  const double h = a * b;
+  const double l = fma(a, b, -h);
+  const double qt = fma(h, qi, M) - M;
+  return fma(-qt, q, h) + l;
+}
 // x mod q centred: |r| <= q/2 + 2^-40 q for |x| < 2^53 (magic-constant rint,
 // valid since |x / q| < 2^51).
 __device__ __forceinline__ double fredq(double x, double qi, double q) {
@@ -303,6 +312,11 @@ struct NttEpi {
 // src + (r / src_div) * n (broadcast of one source row to several limbs).
 int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st,
                const uint64_t* src = nullptr, int src_div = 1, const NttEpi* epi = nullptr);
+// Forward NTT of squared ciphertexts' lifted polys fused with the NTT-domain
+// tensor (ntt_f64.cuh ntt_f64_fwd_sq): FP64 rings with 2^10 <= n <= 2^14 only
+// (returns 1 when not applicable, nothing launched).
+int launch_ntt_square_tensor(const fcn_ring* r, const uint64_t* a, const uint64_t* aux, uint64_t* Tout, int64_t C,
+                             int k, int m, cudaStream_t st);
 
 inline int grid_for(int64_t work, int block, int max_blocks = 148 * 16) {
   int64_t g = (work + block - 1) / block;

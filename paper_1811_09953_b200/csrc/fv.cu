@@ -299,6 +299,20 @@ __global__ void __launch_bounds__(256) mac_kernel(const uint64_t* __restrict__ i
   for (int d = 0; d < F.n; ++d) *reinterpret_cast<ulonglong2*>(F.dst[d] + (int64_t)o * ct_words + (int64_t)r * n + j0) = res;
 }
 
+// acc + x m (mod 2^64) for a 32-bit multiplier
+__device__ __forceinline__ uint64_t mac32(uint64_t acc, uint64_t x, uint32_t m) {
+  uint64_t r;
+  asm("{\n\t.reg .u32 xl, xh, al, ah;\n\t.reg .u64 t;\n\t"
+      "mov.b64 {xl, xh}, %1;\n\t"
+      "mov.b64 {al, ah}, %2;\n\t"
+      "mad.lo.u32 ah, xh, %3, ah;\n\t"
+      "mov.b64 t, {al, ah};\n\t"
+      "mad.wide.u32 %0, xl, %3, t;\n\t}"
+      : "=l"(r)
+      : "l"(x), "l"(acc), "r"(m));
+  return r;
+}
+
 #ifndef MAC_WAVES
 #define MAC_WAVES 8
 #endif
@@ -335,18 +349,20 @@ __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restric
                           (int64_t)r * n + j0;
     const ulonglong2 va = *reinterpret_cast<const ulonglong2*>(src);
     const ulonglong2 vb = *reinterpret_cast<const ulonglong2*>(src + 2);
+    // |c| < 2^32 on this path (fold >= 2): acc += x |c| is one IMAD.WIDE.U32
+    // (low word, 64-bit addend) plus one IMAD (high word)
     if (cf >= 0) {
-      const uint64_t m = (uint64_t)cf;
-      pos[0] += va.x * m;
-      pos[1] += va.y * m;
-      pos[2] += vb.x * m;
-      pos[3] += vb.y * m;
+      const uint32_t m = (uint32_t)cf;
+      pos[0] = mac32(pos[0], va.x, m);
+      pos[1] = mac32(pos[1], va.y, m);
+      pos[2] = mac32(pos[2], vb.x, m);
+      pos[3] = mac32(pos[3], vb.y, m);
     } else {
-      const uint64_t m = (uint64_t)(-cf);
-      neg[0] += va.x * m;
-      neg[1] += va.y * m;
-      neg[2] += vb.x * m;
-      neg[3] += vb.y * m;
+      const uint32_t m = (uint32_t)(-cf);
+      neg[0] = mac32(neg[0], va.x, m);
+      neg[1] = mac32(neg[1], va.y, m);
+      neg[2] = mac32(neg[2], vb.x, m);
+      neg[3] = mac32(neg[3], vb.y, m);
     }
     if (++cnt == fold) {
       cnt = 0;
@@ -495,9 +511,11 @@ template <int KQ, int KA, int NW>
 __global__ void __launch_bounds__(256) lift_f64_kernel(const uint64_t* __restrict__ in, uint64_t* __restrict__ ext,
                                                        int64_t npoly, int logn, const __grid_constant__ LiftP<KQ, KA> P,
                                                        const MulCtConst* __restrict__ cc,
-                                                       unsigned long long* __restrict__ fallbacks) {
+                                                       unsigned long long* __restrict__ fallbacks, int compact) {
   const int n = 1 << logn;
   constexpr int k = KQ, m = KA, K = KQ + KA;  // exact-size instantiations only
+  // compact: only the m auxiliary rows are written, as [poly][m][n] (the
+  // q-limb rows of the lift are the input rows themselves)
   const int64_t total = npoly << logn;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   constexpr double M = 6755399441055744.0;
@@ -525,7 +543,7 @@ __global__ void __launch_bounds__(256) lift_f64_kernel(const uint64_t* __restric
     for (int i = 0; i < KQ; ++i) {
       y[i] = 0.0;
       if (i < k) {
-        ext[(poly * K + i) * n + coef] = cur[i];
+        if (!compact) ext[(poly * K + i) * n + coef] = cur[i];
         y[i] = fmulq_m(u2f(cur[i]), P.fqinv[i], P.fqinvq[i], P.fq[i]);
         f = fma(y[i], P.rq[i], f);
       }
@@ -571,7 +589,7 @@ __global__ void __launch_bounds__(256) lift_f64_kernel(const uint64_t* __restric
           if ((i & 3) == 3) acc = fredq(acc, pji, pj);
           acc += fmulq_m(y[i], P.flc[j][i], P.flcq[j][i], pj);
         }
-        ext[(poly * K + k + j) * n + coef] = f2u_canon(fredq(acc, pji, pj), pj);
+        ext[(compact ? poly * m + j : poly * K + k + j) * n + coef] = f2u_canon(fredq(acc, pji, pj), pj);
       }
     }
   }
@@ -683,13 +701,6 @@ __device__ __forceinline__ void emit_digits(const uint64_t* out, const RescaleP<
 __device__ __forceinline__ double fcentre(uint64_t x, uint64_t qh, double q) {
   const double d = u2f(x);
   return x > qh ? d - q : d;
-}
-__device__ __forceinline__ double fprod(double a, double b, double q, double qi) {
-  const double M = 6755399441055744.0;
-  const double h = a * b;
-  const double l = fma(a, b, -h);
-  const double qt = fma(h, qi, M) - M;
-  return fma(-qt, q, h) + l;
 }
 
 __global__ void tensor_f64_kernel(const uint64_t* __restrict__ A, const uint64_t* __restrict__ B, uint64_t* __restrict__ T,
@@ -1661,16 +1672,17 @@ struct ActArgs {
 
 template <int KQ, int KE>
 static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t* in, uint64_t* out, int64_t cnt,
-                            uint64_t* R01, uint64_t* DG, cudaStream_t st, ActArgs* act) {
+                            uint64_t* R01, uint64_t* DG, cudaStream_t st, ActArgs* act, bool* compact) {
   const bool f64 = x->fp && x->k == KQ && x->k + x->m == KE;  // FP64 kernels: exact sizes
   const MulCtConst& mc = x->host_mc[lane];
   const MulCtConst* dmc = x->d_mc + lane;
   if (lift) {
     const LiftP<KQ, KE - KQ> P = make_lift_params<KQ, KE - KQ>(x, mc);
     const int64_t total = cnt << x->logn;  // cnt = polys
+    if (compact) *compact = *compact && f64;  // only the FP64 lift writes the compact layout
     if (f64)
-      lift_f64_kernel<KQ, KE - KQ, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, out, cnt, x->logn, P, dmc,
-                                                                                 x->d_fallbacks);
+      lift_f64_kernel<KQ, KE - KQ, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(
+          in, out, cnt, x->logn, P, dmc, x->d_fallbacks, compact && *compact ? 1 : 0);
     else
       lift_kernel<KQ, KE - KQ, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, out, cnt, x->logn, P, dmc,
                                                                              x->d_fallbacks);
@@ -1710,10 +1722,11 @@ static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_
 }
 
 static int lift_or_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t* in, uint64_t* out, int64_t cnt,
-                           uint64_t* R01, uint64_t* DG, cudaStream_t st, ActArgs* act = nullptr) {
+                           uint64_t* R01, uint64_t* DG, cudaStream_t st, ActArgs* act = nullptr,
+                           bool* compact = nullptr) {
   const int k = x->k, m = x->m;
 #define FCN_TRY(KQ, KE) \
-  if (k <= KQ && m <= KE - KQ) return run_lift_rescale<KQ, KE>(lift, x, lane, in, out, cnt, R01, DG, st, act);
+  if (k <= KQ && m <= KE - KQ) return run_lift_rescale<KQ, KE>(lift, x, lane, in, out, cnt, R01, DG, st, act, compact);
   FCN_TRY(2, 5)
   FCN_TRY(2, 6)
   FCN_TRY(3, 6)
@@ -1726,6 +1739,15 @@ static int lift_or_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t
   FCN_TRY(16, 32)
 #undef FCN_TRY
   return set_error(FCN_ERR_PARAM, "unsupported limb counts k=%d m=%d", k, m);
+}
+
+// FCN_SQ_FUSE=0 disables the fused forward-NTT + tensor kernel (A/B tests).
+static bool sq_fuse_enabled() {
+  static const bool on = [] {
+    const char* ev = getenv("FCN_SQ_FUSE");
+    return !(ev && ev[0] == '0');
+  }();
+  return on;
 }
 
 static int launch_keymac(const uint64_t* DG, const fcn_keys* keys, uint64_t* ACC, int64_t C, int D, int k, const fcn_ctx* x,
@@ -1821,22 +1843,39 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
     uint64_t* DGR = ACC + C * 2 * k * n;
     const uint64_t* a = d_a + off * ct_words;
     const uint64_t* b = d_b ? d_b + off * ct_words : nullptr;
-    // (i) lift + forward NTT over the extended base
-    for (int which = 0; which < (b ? 2 : 1); ++which) {
-      uint64_t* dst = which ? EB : EA;
-      int rc = lift_or_rescale(true, x, lane, which ? b : a, dst, C * 2, nullptr, nullptr, st);
+    // (i) lift + forward NTT over the extended base, (ii) tensor.  Squares on
+    // FP64 rings: compact lift (auxiliary rows only) and one fused
+    // forward-NTT + tensor kernel that reads the q-limb rows from a itself.
+    bool fused = !b && x->fp && sq_fuse_enabled() && logn >= 10 && logn <= 14;
+    if (fused) {
+      int rc = lift_or_rescale(true, x, lane, a, EA, C * 2, nullptr, nullptr, st, nullptr, &fused);
       if (rc) return rc;
-      rc = launch_ntt(x->ext, dst, C * 2 * K, K, 0, true, st);
-      if (rc) return rc;
+      if (fused) {
+        rc = launch_ntt_square_tensor(x->ext, a, EA, T, C, k, x->m, st);
+        if (rc) return rc < 0 ? rc : set_error(FCN_ERR_STATE, "fused square tensor unavailable");
+      } else {  // the lift wrote the full extended rows
+        rc = launch_ntt(x->ext, EA, C * 2 * K, K, 0, true, st);
+        if (rc) return rc;
+      }
+    } else {
+      for (int which = 0; which < (b ? 2 : 1); ++which) {
+        uint64_t* dst = which ? EB : EA;
+        int rc = lift_or_rescale(true, x, lane, which ? b : a, dst, C * 2, nullptr, nullptr, st);
+        if (rc) return rc;
+        rc = launch_ntt(x->ext, dst, C * 2 * K, K, 0, true, st);
+        if (rc) return rc;
+      }
     }
-    // (ii) tensor, (iii) inverse NTT
-    if (x->fp)
-      tensor_f64_kernel<<<grid_for((C * K) << (logn - 1), 256), 256, 0, st>>>(EA, b ? EB : nullptr, T, C, K, logn,
-                                                                              x->ext->d_lc);
-    else
-      tensor_kernel<<<grid_for((C * K) << (logn - 1), 256), 256, 0, st>>>(EA, b ? EB : nullptr, T, C, K, logn,
-                                                                          x->ext->d_lc);
-    FCN_LAUNCH_CHECK(x->fp ? "tensor_f64_kernel" : "tensor_kernel");
+    if (!fused) {
+      if (x->fp)
+        tensor_f64_kernel<<<grid_for((C * K) << (logn - 1), 256), 256, 0, st>>>(EA, b ? EB : nullptr, T, C, K, logn,
+                                                                                x->ext->d_lc);
+      else
+        tensor_kernel<<<grid_for((C * K) << (logn - 1), 256), 256, 0, st>>>(EA, b ? EB : nullptr, T, C, K, logn,
+                                                                            x->ext->d_lc);
+      FCN_LAUNCH_CHECK(x->fp ? "tensor_f64_kernel" : "tensor_kernel");
+    }
+    // (iii) inverse NTT
     int rc = launch_ntt(x->ext, T, C * 3 * K, K, 0, false, st);
     if (rc) return rc;
     // (iv) exact rescale + digit decomposition (FP64: R01 <- c2 R01 + c1 a for the activation)

@@ -636,6 +636,10 @@ extern "C" int fcn_ntt_f64_schedule(int logn, uint64_t qmax) { return fcn::f64_s
 
 namespace fcn {
 
+template <int RS>
+int launch_ntt_f64_sq(const fcn_ring* r, const uint64_t* a, const uint64_t* aux, uint64_t* Tout, int64_t units, int k,
+                      int m, cudaStream_t st, int sms);  // ntt_f64.cuh
+
 static int g_force_int = -1;  // FCN_NTT_INT=1 selects the integer kernels (A/B tests)
 
 int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st,
@@ -690,6 +694,25 @@ int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int o
   }
   FCN_LAUNCH_CHECK(fwd ? "ntt_v2_fwd" : "ntt_v2_inv");
   return launch_epi_int(r, d, n_rows, period, offset, st, epi);
+}
+
+int launch_ntt_square_tensor(const fcn_ring* r, const uint64_t* a, const uint64_t* aux, uint64_t* Tout, int64_t C,
+                             int k, int m, cudaStream_t st) {
+  if (C <= 0) return FCN_OK;
+  if (!r->d_ffwd || r->logn < 10 || r->logn > 14 || r->L != k + m) return 1;
+  uint64_t qmax = 0;
+  for (int l = 0; l < r->L; ++l) {
+    if (r->primes[l] >= (1ull << 51)) return 1;
+    qmax = r->primes[l] > qmax ? r->primes[l] : qmax;
+  }
+  std::call_once(g_init, init_tables);
+  if (g_init_err != cudaSuccess) return check_cuda(g_init_err, "ntt init");
+  const int64_t units = C * (k + m);
+  switch (f64_schedule(r->logn, qmax)) {
+    case 2: return launch_ntt_f64_sq<2>(r, a, aux, Tout, units, k, m, st, g_sms);
+    case 1: return launch_ntt_f64_sq<1>(r, a, aux, Tout, units, k, m, st, g_sms);
+    default: return launch_ntt_f64_sq<0>(r, a, aux, Tout, units, k, m, st, g_sms);
+  }
 }
 
 }  // namespace fcn

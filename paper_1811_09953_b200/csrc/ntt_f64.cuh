@@ -108,12 +108,57 @@ __device__ __forceinline__ void inv_ctf(double* x, int o, const double2* __restr
   }
 }
 
+// The forward transform of one row held as signed doubles x[j] = element
+// tid + j T: pass 1 (stages 0..4, CTA-uniform twiddles), exchange, pass 2,
+// exchange, pass 3 (last five stages; tl = the limb's transposed last-stage
+// table).  On return x[j] holds output element 32 tid + j (bit-reversed order),
+// not yet reduced.  Starts with a barrier, so the caller may still be reading
+// shared memory from the previous row when it calls this.
+template <int LOGN, int RS>
+__device__ __forceinline__ void fwd_body(double* x, int tid, double* fs, const double2* __restrict__ tw,
+                                         const double2* __restrict__ tl, double q, double qi) {
+  constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
+  (void)N;
+  // pass 1: stages 0..4 on t + j*T (twiddles uniform across the CTA)
+  fwd_ctf<LOGN, RS, 5, 0>(x, 0, tw, q, qi);
+  __syncthreads();  // every warp has copied out the previous row
+#pragma unroll
+  for (int j = 0; j < 32; ++j) fs[phys(tid + j * T)] = x[j];
+  __syncthreads();
+  if (RM > 0) {
+#pragma unroll
+    for (int i = 0; i < 32 / GM; ++i) {
+      const int g = tid + i * T;
+      const int base = ((g >> 5) << (5 + RM)) + (g & 31);
+#pragma unroll
+      for (int j = 0; j < GM; ++j) x[i * GM + j] = fs[phys(base + j * 32)];
+    }
+#pragma unroll
+    for (int i = 0; i < 32 / GM; ++i) fwd_ctf<LOGN, RS, (RM > 0 ? RM : 1), 5>(x + i * GM, (tid + i * T) >> 5, tw, q, qi);
+#pragma unroll
+    for (int i = 0; i < 32 / GM; ++i) {
+      const int g = tid + i * T;
+      const int base = ((g >> 5) << (5 + RM)) + (g & 31);
+#pragma unroll
+      for (int j = 0; j < GM; ++j) fs[phys(base + j * 32)] = x[i * GM + j];
+    }
+  }
+  // the first twiddle of pass 3 is requested before the barrier (its L2
+  // latency was exposed at the start of the pass)
+  const double2 w3 = ld_ftw(tl + tid);
+  if (RM > 0) __syncthreads();
+  // pass 3: the last 5 stages on 32 contiguous residues
+#pragma unroll
+  for (int j = 0; j < 32; ++j) x[j] = fs[tid * 33 + j];
+  fwd_ctf_last<LOGN, RS, LOGN - 5>(x, tid, T, tl, q, qi, w3);
+}
+
 template <int LOGN, int RS>
 __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     ntt_f64_fwd(uint64_t* __restrict__ data, int64_t n_rows, int period, int offset, const LimbConst* __restrict__ lcs,
                 const double2* __restrict__ tws, const double2* __restrict__ twl, const uint64_t* __restrict__ src,
                 int src_div) {
-  constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
+  constexpr int N = 1 << LOGN, T = N / 32;
   extern __shared__ uint64_t sm[];
   double* fs = reinterpret_cast<double*>(sm);
   const int tid = threadIdx.x;
@@ -132,38 +177,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     const double2* tw = tws + (int64_t)limb * N;
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = u2f((uint64_t)__double_as_longlong(x[j]));
-    // pass 1: stages 0..4 on t + j*T (twiddles uniform across the CTA)
-    fwd_ctf<LOGN, RS, 5, 0>(x, 0, tw, q, qi);
-    __syncthreads();  // every warp has copied out the previous row
-#pragma unroll
-    for (int j = 0; j < 32; ++j) fs[phys(tid + j * T)] = x[j];
-    __syncthreads();
-    if (RM > 0) {
-#pragma unroll
-      for (int i = 0; i < 32 / GM; ++i) {
-        const int g = tid + i * T;
-        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
-#pragma unroll
-        for (int j = 0; j < GM; ++j) x[i * GM + j] = fs[phys(base + j * 32)];
-      }
-#pragma unroll
-      for (int i = 0; i < 32 / GM; ++i) fwd_ctf<LOGN, RS, (RM > 0 ? RM : 1), 5>(x + i * GM, (tid + i * T) >> 5, tw, q, qi);
-#pragma unroll
-      for (int i = 0; i < 32 / GM; ++i) {
-        const int g = tid + i * T;
-        const int base = ((g >> 5) << (5 + RM)) + (g & 31);
-#pragma unroll
-        for (int j = 0; j < GM; ++j) fs[phys(base + j * 32)] = x[i * GM + j];
-      }
-    }
-    // the first twiddle of pass 3 is requested before the barrier (its L2
-    // latency was exposed at the start of the pass)
-    const double2 w3 = ld_ftw(twl + (int64_t)limb * N + tid);
-    if (RM > 0) __syncthreads();
-    // pass 3: the last 5 stages on 32 contiguous residues, canonical out
-#pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = fs[tid * 33 + j];
-    fwd_ctf_last<LOGN, RS, LOGN - 5>(x, tid, T, twl + (int64_t)limb * N, q, qi, w3);
+    fwd_body<LOGN, RS>(x, tid, fs, tw, twl + (int64_t)limb * N, q, qi);
 #pragma unroll
     for (int j = 0; j < 32; ++j) sm[tid * 33 + j] = f2u_canon(fredq(x[j], qi, q), q);
     // A warp's 32 threads own residues [1024 w, 1024 w + 1024): it copies
@@ -185,6 +199,108 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
       v.y = sw[66 * i + 1];
       o2[32 * i] = v;
     }
+  }
+}
+
+// Forward NTT of a squared ciphertext's lifted polys fused with the
+// NTT-domain tensor (reference fv.py:511-515 with a = b): a unit (ct, l)
+// transforms A0 = NTT(a0 mod b_l) and then A1 = NTT(a1 mod b_l) and writes
+// d0 = A0^2, d1 = 2 A0 A1, d2 = A1^2 to Tout[(ct*3 + p)*K + l] (canonical),
+// so neither A0 nor A1 makes an HBM round trip through a separate tensor
+// kernel.  A0 is parked (centred doubles) in the d2 row by the per-warp
+// copy-out and read back by the very thread that wrote it.  Input rows: limb
+// l < k from the ciphertexts a ([C][2][k][n]), l >= k from the lift's compact
+// auxiliary rows aux ([C][2][m][n]).
+template <int LOGN, int RS>
+__global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
+    ntt_f64_fwd_sq(const uint64_t* __restrict__ a, const uint64_t* __restrict__ aux, uint64_t* __restrict__ Tout,
+                   int64_t units, int k, int m, const LimbConst* __restrict__ lcs, const double2* __restrict__ tws,
+                   const double2* __restrict__ twl) {
+  constexpr int N = 1 << LOGN, T = N / 32;
+  const int K = k + m;
+  extern __shared__ uint64_t sm[];
+  double* fs = reinterpret_cast<double*>(sm);
+  const int tid = threadIdx.x;
+  int64_t u = blockIdx.x;
+  if (u >= units) return;
+  auto src_row = [&](int64_t uu, int ss) -> const uint64_t* {
+    const int64_t ct = uu / K;
+    const int l = (int)(uu - ct * K);
+    return l < k ? a + ((ct * 2 + ss) * k + l) * N : aux + ((ct * 2 + ss) * m + (l - k)) * N;
+  };
+  double x[32];  // raw u64 bits of the next row between iterations
+  {
+    const uint64_t* p = src_row(u, 0);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
+  }
+  const int wb = tid & ~31, ln = tid & 31;
+  const int pofs = wb * 33 + 2 * ln + (ln >> 4);  // this lane's first pair in its warp's block (phys)
+  int s = 0;
+  for (;;) {
+    const int64_t ct = u / K;
+    const int limb = (int)(u - ct * K);
+    const LimbConst& c = lcs[limb];
+    const double q = c.fq, qi = c.fqi;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = u2f((uint64_t)__double_as_longlong(x[j]));
+    fwd_body<LOGN, RS>(x, tid, fs, tws + (int64_t)limb * N, twl + (int64_t)limb * N, q, qi);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) fs[tid * 33 + j] = fredq(x[j], qi, q);  // |.| <= q/2 + 2^-40 q
+    __syncwarp();
+    const int64_t un = s == 0 ? u : u + gridDim.x;
+    const bool more = un < units;
+    const uint64_t* pn = more ? src_row(un, s ^ 1) : nullptr;
+    ulonglong2* o2 = reinterpret_cast<ulonglong2*>(Tout + ((ct * 3 + 2) * K + limb) * N) + wb * 16 + ln;
+    const double* fw = fs + pofs;
+    if (s == 0) {
+      // A0: park it in the d2 row (this warp's block, coalesced) while the A1 row loads
+      if (more) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)pn[tid + j * T]);
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        ulonglong2 v;
+        v.x = (uint64_t)__double_as_longlong(fw[66 * i]);
+        v.y = (uint64_t)__double_as_longlong(fw[66 * i + 1]);
+        o2[32 * i] = v;
+      }
+    } else {
+      // A1 in shared memory; this lane's parked A0 pairs come back from L2
+      // into x[] (free now), each pair replaced by the next row's elements
+      // once consumed
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const ulonglong2 v = o2[32 * i];
+        x[2 * i] = __longlong_as_double((long long)v.x);
+        x[2 * i + 1] = __longlong_as_double((long long)v.y);
+      }
+      ulonglong2* o0 = reinterpret_cast<ulonglong2*>(Tout + ((ct * 3 + 0) * K + limb) * N) + wb * 16 + ln;
+      ulonglong2* o1 = reinterpret_cast<ulonglong2*>(Tout + ((ct * 3 + 1) * K + limb) * N) + wb * 16 + ln;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        uint64_t t0[2], t1[2], t2[2];
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const double x0 = x[2 * i + v], x1 = fw[66 * i + v];
+          t0[v] = f2u_canon(fprod(x0, x0, q, qi), q);
+          const double mm = fprod(x0, x1, q, qi);
+          t1[v] = f2u_canon(fredq(mm + mm, qi, q), q);
+          t2[v] = f2u_canon(fprod(x1, x1, q, qi), q);
+        }
+        o0[32 * i] = make_ulonglong2(t0[0], t0[1]);
+        o1[32 * i] = make_ulonglong2(t1[0], t1[1]);
+        o2[32 * i] = make_ulonglong2(t2[0], t2[1]);
+        if (more) {
+          x[2 * i] = __longlong_as_double((long long)pn[tid + 2 * i * T]);
+          x[2 * i + 1] = __longlong_as_double((long long)pn[tid + (2 * i + 1) * T]);
+        }
+      }
+    }
+    if (!more) break;
+    u = un;
+    s ^= 1;
   }
 }
 
@@ -421,6 +537,34 @@ int launch_ntt_f64(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, i
     case 12: return f64_launch_t<12, RS>(fwd, sms, d, n_rows, period, offset, r, st, src, src_div, epi);
     case 13: return f64_launch_t<13, RS>(fwd, sms, d, n_rows, period, offset, r, st, src, src_div, epi);
     case 14: return f64_launch_t<14, RS>(fwd, sms, d, n_rows, period, offset, r, st, src, src_div, epi);
+    default: return set_error(FCN_ERR_ARG, "FP64 NTT: unsupported log n %d", r->logn);
+  }
+}
+
+template <int LOGN, int RS>
+static int f64_sq_launch_t(int sms, const fcn_ring* r, const uint64_t* a, const uint64_t* aux, uint64_t* Tout,
+                           int64_t units, int k, int m, cudaStream_t st) {
+  constexpr int threads = (1 << LOGN) / 32;
+  const size_t sm = (size_t)((1 << LOGN) + (1 << LOGN) / 32 + 2) * sizeof(uint64_t);
+  cudaError_t err = cudaSuccess;
+  const int occ = F64Occ<LOGN, RS, 6>::get((const void*)ntt_f64_fwd_sq<LOGN, RS>, sm, &err);
+  if (err != cudaSuccess) return check_cuda(err, "ntt_f64_fwd_sq attributes");
+  int64_t g = (int64_t)sms * occ;
+  if (g > units) g = units;
+  ntt_f64_fwd_sq<LOGN, RS><<<(int)g, threads, sm, st>>>(a, aux, Tout, units, k, m, r->d_lc, r->d_ffwd, r->d_ffl);
+  FCN_LAUNCH_CHECK("ntt_f64_fwd_sq");
+  return FCN_OK;
+}
+
+template <int RS>
+int launch_ntt_f64_sq(const fcn_ring* r, const uint64_t* a, const uint64_t* aux, uint64_t* Tout, int64_t units, int k,
+                      int m, cudaStream_t st, int sms) {
+  switch (r->logn) {
+    case 10: return f64_sq_launch_t<10, RS>(sms, r, a, aux, Tout, units, k, m, st);
+    case 11: return f64_sq_launch_t<11, RS>(sms, r, a, aux, Tout, units, k, m, st);
+    case 12: return f64_sq_launch_t<12, RS>(sms, r, a, aux, Tout, units, k, m, st);
+    case 13: return f64_sq_launch_t<13, RS>(sms, r, a, aux, Tout, units, k, m, st);
+    case 14: return f64_sq_launch_t<14, RS>(sms, r, a, aux, Tout, units, k, m, st);
     default: return set_error(FCN_ERR_ARG, "FP64 NTT: unsupported log n %d", r->logn);
   }
 }
