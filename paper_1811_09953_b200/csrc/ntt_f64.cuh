@@ -368,7 +368,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     if (RM > 0) __syncthreads();
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = fs[pst + j * (T + T / 32)];
-    __syncthreads();
+    // the next row lands in exactly the slots this thread just read: no barrier
     const int64_t nxt = row + gridDim.x;
     if (nxt < n_rows) {
       const uint64_t* p = data + nxt * N;
