@@ -316,12 +316,17 @@ __device__ __forceinline__ uint64_t mac32(uint64_t acc, uint64_t x, uint32_t m) 
 #ifndef MAC_WAVES
 #define MAC_WAVES 8
 #endif
+#ifndef MAC_ROWS
+#define MAC_ROWS 2
+#endif
 // Fast path: all rotations 0 (constant plaintexts) and max|coef| * q small
 // enough that `fold` consecutive products fit one 64-bit accumulator.  Each
-// term is then one IMAD.WIDE + one IMAD per residue (acc += x * |c|),
-// accumulators are folded back below 4q every `fold` terms.  Four residues
-// per thread (two 16-byte loads) amortise the term metadata.
-template <bool SMALL>
+// term is then acc += x |c| per residue (mac32: IMAD.WIDE.U32 + IMAD + carry),
+// accumulators are folded back below 4q every `fold` terms.  A thread owns
+// four residues of NR rows of the same limb (rows r, r + k: c0 and c1), so
+// the term metadata (column, coefficient, source address: uniform-datapath
+// work) is amortised over 4 NR residues.
+template <bool SMALL, int NR>
 __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restrict__ in0, int64_t n_in0,
                                                        const uint64_t* __restrict__ in1,
                                                        const int32_t* __restrict__ rowptr,
@@ -329,70 +334,85 @@ __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restric
                                                        const int64_t* __restrict__ coef, const __grid_constant__ Fanout F,
                                                        int logn, int k, const LimbConst* __restrict__ lcs, int fold,
                                                        int n_out) {
+  constexpr int V = 4 * NR;
   const int n = 1 << logn;
-  const int r = blockIdx.z;
+  const int r = blockIdx.z;  // first row; the others are r + k, r + 2k, ...
   const int j0 = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
   if (j0 >= n) return;
   const LimbConst& c = lcs[r % k];
   const uint64_t q = c.q, nq = c.nq, one_s = c.one_s;
   const uint32_t m32 = c.m32;
   const int64_t ct_words = (int64_t)2 * k * n;
+  const int64_t rstep = (int64_t)k * n;
   // outputs o = blockIdx.y + i * gridDim.y: per-CTA setup amortised over several outputs
   for (int o = blockIdx.x; o < n_out; o += gridDim.x) {
-  uint64_t pos[4] = {0, 0, 0, 0}, neg[4] = {0, 0, 0, 0};
-  const int e0 = rowptr[o], e1 = rowptr[o + 1];
-  int cnt = 0;
-  for (int e = e0; e < e1; ++e) {
-    const int cl = __ldg(col + e);
-    const int64_t cf = __ldg(coef + e);
-    const uint64_t* src = (cl < n_in0 ? in0 + (int64_t)cl * ct_words : in1 + (int64_t)(cl - n_in0) * ct_words) +
-                          (int64_t)r * n + j0;
-    const ulonglong2 va = *reinterpret_cast<const ulonglong2*>(src);
-    const ulonglong2 vb = *reinterpret_cast<const ulonglong2*>(src + 2);
-    // |c| < 2^32 on this path (fold >= 2): acc += x |c| is one IMAD.WIDE.U32
-    // (low word, 64-bit addend) plus one IMAD (high word)
-    if (cf >= 0) {
-      const uint32_t m = (uint32_t)cf;
-      pos[0] = mac32(pos[0], va.x, m);
-      pos[1] = mac32(pos[1], va.y, m);
-      pos[2] = mac32(pos[2], vb.x, m);
-      pos[3] = mac32(pos[3], vb.y, m);
-    } else {
-      const uint32_t m = (uint32_t)(-cf);
-      neg[0] = mac32(neg[0], va.x, m);
-      neg[1] = mac32(neg[1], va.y, m);
-      neg[2] = mac32(neg[2], vb.x, m);
-      neg[3] = mac32(neg[3], vb.y, m);
-    }
-    if (++cnt == fold) {
-      cnt = 0;
+    uint64_t pos[V], neg[V];
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        if (SMALL) {
-          pos[v] = reduce_small(pos[v], m32, q);
-          neg[v] = reduce_small(neg[v], m32, q);
-        } else {
-          pos[v] = mulw(pos[v], 1, one_s, nq);
-          neg[v] = mulw(neg[v], 1, one_s, nq);
+    for (int v = 0; v < V; ++v) pos[v] = neg[v] = 0;
+    const int e0 = rowptr[o], e1 = rowptr[o + 1];
+    int cnt = 0;
+    for (int e = e0; e < e1; ++e) {
+      const int cl = __ldg(col + e);
+      const int64_t cf = __ldg(coef + e);
+      const uint64_t* src = (cl < n_in0 ? in0 + (int64_t)cl * ct_words : in1 + (int64_t)(cl - n_in0) * ct_words) +
+                            (int64_t)r * n + j0;
+      ulonglong2 va[NR], vb[NR];
+#pragma unroll
+      for (int h = 0; h < NR; ++h) {
+        va[h] = *reinterpret_cast<const ulonglong2*>(src + h * rstep);
+        vb[h] = *reinterpret_cast<const ulonglong2*>(src + h * rstep + 2);
+      }
+      // |c| < 2^32 on this path (fold >= 2)
+      uint64_t* acc = cf >= 0 ? pos : neg;
+      const uint32_t m = (uint32_t)(cf >= 0 ? cf : -cf);
+      if (cf >= 0) {
+#pragma unroll
+        for (int h = 0; h < NR; ++h) {
+          pos[4 * h + 0] = mac32(pos[4 * h + 0], va[h].x, m);
+          pos[4 * h + 1] = mac32(pos[4 * h + 1], va[h].y, m);
+          pos[4 * h + 2] = mac32(pos[4 * h + 2], vb[h].x, m);
+          pos[4 * h + 3] = mac32(pos[4 * h + 3], vb[h].y, m);
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < NR; ++h) {
+          neg[4 * h + 0] = mac32(neg[4 * h + 0], va[h].x, m);
+          neg[4 * h + 1] = mac32(neg[4 * h + 1], va[h].y, m);
+          neg[4 * h + 2] = mac32(neg[4 * h + 2], vb[h].x, m);
+          neg[4 * h + 3] = mac32(neg[4 * h + 3], vb[h].y, m);
+        }
+      }
+      (void)acc;
+      if (++cnt == fold) {
+        cnt = 0;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          if (SMALL) {
+            pos[v] = reduce_small(pos[v], m32, q);
+            neg[v] = reduce_small(neg[v], m32, q);
+          } else {
+            pos[v] = mulw(pos[v], 1, one_s, nq);
+            neg[v] = mulw(neg[v], 1, one_s, nq);
+          }
         }
       }
     }
-  }
-  uint64_t res[4];
+    uint64_t res[V];
 #pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    // SMALL: sums kept below 2^62 (fold), reduced by the high-word quotient
-    const uint64_t a = SMALL ? reduce_small(pos[v], m32, q) : csub(csub(mulw(pos[v], 1, one_s, nq), 2 * q), q);
-    const uint64_t b = SMALL ? reduce_small(neg[v], m32, q) : csub(csub(mulw(neg[v], 1, one_s, nq), 2 * q), q);
-    res[v] = submod(a, b, q);
-  }
-  const int64_t off = (int64_t)o * ct_words + (int64_t)r * n + j0;
-  *reinterpret_cast<ulonglong2*>(F.dst[0] + off) = make_ulonglong2(res[0], res[1]);
-  *reinterpret_cast<ulonglong2*>(F.dst[0] + off + 2) = make_ulonglong2(res[2], res[3]);
-  for (int d = 1; d < F.n; ++d) {  // fan-out to the peers' buffers
-    *reinterpret_cast<ulonglong2*>(F.dst[d] + off) = make_ulonglong2(res[0], res[1]);
-    *reinterpret_cast<ulonglong2*>(F.dst[d] + off + 2) = make_ulonglong2(res[2], res[3]);
-  }
+    for (int v = 0; v < V; ++v) {
+      // SMALL: sums kept below 2^62 (fold), reduced by the high-word quotient
+      const uint64_t a = SMALL ? reduce_small(pos[v], m32, q) : csub(csub(mulw(pos[v], 1, one_s, nq), 2 * q), q);
+      const uint64_t b = SMALL ? reduce_small(neg[v], m32, q) : csub(csub(mulw(neg[v], 1, one_s, nq), 2 * q), q);
+      res[v] = submod(a, b, q);
+    }
+#pragma unroll
+    for (int h = 0; h < NR; ++h) {
+      const int64_t off = (int64_t)o * ct_words + (int64_t)r * n + h * rstep + j0;
+      for (int d = 0; d < F.n; ++d) {  // d > 0: fan-out to the peers' buffers
+        *reinterpret_cast<ulonglong2*>(F.dst[d] + off) = make_ulonglong2(res[4 * h], res[4 * h + 1]);
+        *reinterpret_cast<ulonglong2*>(F.dst[d] + off + 2) = make_ulonglong2(res[4 * h + 2], res[4 * h + 3]);
+      }
+    }
   }
 }
 
@@ -1528,20 +1548,21 @@ extern "C" int fcn_linear_mac_multi(const fcn_ctx* x, const uint64_t* d_in0, int
     // every input stays in L2 while all outputs referencing it are summed.
     // The tile (4 residues per thread) shrinks so n_in slices fit in ~48 MB.
     const int64_t n_in_all = n_in0 + n_in1;
+    constexpr int NR = MAC_ROWS;  // rows (c0, c1 of one limb) per thread
     int th = threads;
-    while (th > 32 && n_in_all * th * 4 * 8 > (48ll << 20)) th >>= 1;
+    while (th > 32 && n_in_all * th * 4 * 8 * NR > (48ll << 20)) th >>= 1;
     const int per_cta = th * 4;
-    const int gy = (x->n + per_cta - 1) / per_cta, gz = 2 * x->k;
+    const int gy = (x->n + per_cta - 1) / per_cta, gz = 2 * x->k / NR;
     int64_t gx = 148LL * 8 * MAC_WAVES / 4;
     if (gx > n_out) gx = n_out;
     if (gx < 1) gx = 1;
     dim3 grid((unsigned)gx, gy, gz);
     if (small)
-      mac_fast_kernel<true><<<grid, th, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_coef, F,
-                                                                 x->logn, x->k, x->ext->d_lc, fold_small, (int)n_out);
+      mac_fast_kernel<true, NR><<<grid, th, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_coef, F,
+                                                                     x->logn, x->k, x->ext->d_lc, fold_small, (int)n_out);
     else
-      mac_fast_kernel<false><<<grid, th, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_coef, F,
-                                                                  x->logn, x->k, x->ext->d_lc, fold, (int)n_out);
+      mac_fast_kernel<false, NR><<<grid, th, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_coef, F,
+                                                                      x->logn, x->k, x->ext->d_lc, fold, (int)n_out);
     FCN_LAUNCH_CHECK("mac_fast_kernel");
     return FCN_OK;
   }
