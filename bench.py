@@ -509,9 +509,17 @@ def run_gpu(args, ws, rank, local):
     fp_roof = None
     if fp:
         ach = bfly / t_avg
-        fp_roof = {"achieved_butterflies_per_s": ach, "peak_butterflies_per_s": fp["butterfly_per_s"],
-                   "frac": ach / fp["butterfly_per_s"],
-                   "peak_source": "profiles/fp64_peak.json (measured register-resident FP64 butterfly, tools/fp64bench.cu)"}
+        # the reduction schedule the launch used (one reduction per transform for limbs just above 2^50)
+        from paper_1811_09953_b200 import _lib
+
+        h = P.native()
+        qmax = max(tuple(P.limb_primes) + tuple(h.aux))
+        rs = _lib.load().fcn_ntt_f64_schedule(int(r["n"]).bit_length() - 1, qmax)
+        pk = fp.get("butterfly_rs1_per_s", fp["butterfly_per_s"]) if rs >= 1 else fp["butterfly_per_s"]
+        fp_roof = {"achieved_butterflies_per_s": ach, "peak_butterflies_per_s": pk, "frac": ach / pk,
+                   "schedule": rs, "ceiling_frac_of_hbm": pk * r["bytes"] / bfly / 1e9 / peak,
+                   "peak_source": "profiles/fp64_peak.json (measured register-resident FP64 butterfly with the "
+                                  "launch's reduction schedule, tools/fp64bench.cu)"}
     roofline = {
         "kernel": "ntt_f64_fwd / ntt_f64_inv (batched negacyclic NTT on the FP64 pipe, one CTA per row slot)",
         "bound": "hbm",
@@ -527,7 +535,7 @@ def run_gpu(args, ws, rank, local):
         "ms_inv": r["t_inv_s"] * 1e3,
         "fp64_roofline": fp_roof,
         "note": "the NTT is FP64-pipe bound on B200 (one exact signed modmul = 5 DP ops + FRND per butterfly): "
-                "the register-resident butterfly ceiling is ~60% of the HBM roofline at n=8192",
+                "fp64_roofline.ceiling_frac_of_hbm is the register-resident butterfly ceiling as a fraction of HBM",
     }
     ks = _keyswitch_roofline(P, ek)
     ks_ach = ks["bytes"] / ks["t_s"] / 1e9

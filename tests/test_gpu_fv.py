@@ -329,10 +329,15 @@ def test_errors(F):
     assert F.add_pt(ct, F.PlainPoly.zero(P.t_lanes[0])) is ct
 
 
-def test_integer_kernel_family_subprocess():
-    """The integer kernels (used for limbs >= 2^51) on the cfg1/cfg2 shapes:
-    FCN_NTT_INT=1 forces them for every limb in a fresh process (the switch
-    is read once per process); squares and NTTs must match the oracle."""
+@pytest.mark.parametrize("env", [{"FCN_NTT_INT": "1"}, {"FCN_SQ_FUSE": "0"}, {"FCN_NTT_RS": "0"}],
+                         ids=["integer-kernels", "unfused-square", "ntt-rs0"])
+def test_kernel_family_subprocess(env):
+    """Kernel families the default dispatch does not pick for these shapes,
+    each forced in a fresh process (the switches are read once per process):
+    FCN_NTT_INT=1 the integer kernels (used for limbs >= 2^51), FCN_SQ_FUSE=0
+    the separate forward NTT + tensor kernels for squares, FCN_NTT_RS=0 the
+    FP64 NTT's every-third-stage reduction schedule (limbs near 2^51).
+    Squares and NTTs on the cfg1/cfg2 shapes must match the oracle."""
     import os
     import subprocess
     import sys
@@ -361,6 +366,6 @@ for name in ("cfg1", "cfg2"):
 print("ok")
 """
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, FCN_NTT_INT="1", PYTHONPATH=repo)
+    env = dict(os.environ, PYTHONPATH=repo, **env)
     res = subprocess.run([sys.executable, "-c", code], cwd=repo, env=env, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0 and res.stdout.strip().endswith("ok"), res.stdout[-2000:] + res.stderr[-2000:]

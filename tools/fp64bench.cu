@@ -51,8 +51,9 @@ __device__ __forceinline__ double redq(double x, double qi, double q) {
 }
 
 // 15 stages per iteration (three 5-stage register passes), values reduced
-// before every third stage -- the NTT kernel's schedule (ntt.cu, f64 family)
-template <int MAGIC>
+// before every third stage (RS 0) or once, before stage 7 (RS 1) -- the NTT
+// kernels' schedules (ntt_f64.cuh; RS 1 is what limbs just above 2^50 get)
+template <int MAGIC, int RS>
 __global__ void __launch_bounds__(256, 2) k_bfly(double* out, const double2* __restrict__ tw, double q, int reps) {
   double x[32];
 #pragma unroll
@@ -62,7 +63,7 @@ __global__ void __launch_bounds__(256, 2) k_bfly(double* out, const double2* __r
 #pragma unroll
     for (int s = 0; s < 15; ++s) {
       const int u = s % 5;
-      if (s > 0 && s % 3 == 0) {
+      if (RS == 0 ? (s > 0 && s % 3 == 0) : s == 7) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) x[j] = redq(x[j], qi, q);
       }
@@ -128,11 +129,12 @@ int main() {
   double2* d;
   cudaMalloc(&d, sizeof(h));
   cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice);
-  for (int mg = 0; mg < 2; ++mg) {
+  for (int v = 0; v < 3; ++v) {  // rint RS0, magic RS0, rint RS1
     const int br = 86;
     auto launch = [&] {
-      if (mg) k_bfly<1><<<sms * 2, 256>>>(o, d, q, br);
-      else k_bfly<0><<<sms * 2, 256>>>(o, d, q, br);
+      if (v == 0) k_bfly<0, 0><<<sms * 2, 256>>>(o, d, q, br);
+      else if (v == 1) k_bfly<1, 0><<<sms * 2, 256>>>(o, d, q, br);
+      else k_bfly<0, 1><<<sms * 2, 256>>>(o, d, q / 2, br);  // RS 1 needs q ~ 2^50
     };
     launch();
     cudaDeviceSynchronize();
@@ -143,7 +145,8 @@ int main() {
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     const double bf = 5.0 * sms * 2 * 256.0 * br * 16 * 15;
-    printf("fp64 butterfly (%s): %.3f T/s (%.2f per SM per clk)  err=%s\n", mg ? "magic" : "rint", bf / (ms * 1e-3) / 1e12,
+    const char* nm[3] = {"rint, RS0", "magic, RS0", "rint, RS1"};
+    printf("fp64 butterfly (%s): %.3f T/s (%.2f per SM per clk)  err=%s\n", nm[v], bf / (ms * 1e-3) / 1e12,
            bf / (ms * 1e-3) / sms / 1.965e9, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
