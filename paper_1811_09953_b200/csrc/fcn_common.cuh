@@ -305,6 +305,9 @@ struct NttEpi {
   const uint64_t* add = nullptr;
   const uint64_t* lin = nullptr;
   Fanout out;  // destinations, row-aligned
+  // mode 0 on the FP64 inverse: replacement twist table (n^-1 psi^-j times a
+  // per-limb constant), e.g. the rescale's (B/b_l)^-1 folded into the tensor's INTT
+  const double2* ftwist = nullptr;
   uint64_t c2[kEpiLimbs], c1[kEpiLimbs];
   double fc2[kEpiLimbs], fc2q[kEpiLimbs], fc1[kEpiLimbs], fc1q[kEpiLimbs];
 };
@@ -312,6 +315,9 @@ struct NttEpi {
 // src + (r / src_div) * n (broadcast of one source row to several limbs).
 int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st,
                const uint64_t* src = nullptr, int src_div = 1, const NttEpi* epi = nullptr);
+// Which NTT kernels launch_ntt runs for rows of limbs offset .. offset+period-1:
+// 0 generic (ntt_v1), 1 integer register passes (ntt_v2), 2 FP64 (ntt_f64.cuh).
+int ntt_family(const fcn_ring* r, int period, int offset);
 // Forward NTT of squared ciphertexts' lifted polys fused with the NTT-domain
 // tensor (ntt_f64.cuh ntt_f64_fwd_sq): FP64 rings with 2^10 <= n <= 2^14 only
 // (returns 1 when not applicable, nothing launched).

@@ -70,6 +70,9 @@ struct fcn_ctx {
   std::vector<fcn::MulCtConst> host_mc;
   unsigned long long* d_fallbacks = nullptr;
   bool fp = false;  // every ext prime < 2^51: FP64-pipe lift / rescale kernels
+  // FP64 inverse twist of the tensor INTT with the rescale's first factor
+  // folded in: {w, w/b_l}, w = n^-1 psi_l^-j (B/b_l)^-1 mod b_l signed
+  double2* d_ftwist_binv = nullptr;
 };
 
 struct fcn_keys {
@@ -453,6 +456,8 @@ struct RescaleP {
   double fntp[KQ], fntpq[KQ];
   // fused activation (FP64 path): R01 rows become c2 R + c1 lin (mod q_i)
   int act;
+  // FP64 path: the inputs are already y_j = T_j (B/b_j)^-1 (folded into the INTT's twist)
+  int prescaled;
   double fc2[KQ], fc2q[KQ], fc1[KQ], fc1q[KQ];
 };
 
@@ -911,7 +916,10 @@ __global__ void __launch_bounds__(256, FCN_RS_MINB(KQ))
       y[j] = 0.0;
       if (j < K) {
         const double x = u2f(cur[j]);
-        y[j] = fmulq_m(x, P.fbinv[j], P.fbinvq[j], P.fb[j]);
+        if (P.prescaled)
+          y[j] = x > 0.5 * P.fb[j] ? x - P.fb[j] : x;  // centred: |y_j| <= b_j / 2
+        else
+          y[j] = fmulq_m(x, P.fbinv[j], P.fbinvq[j], P.fb[j]);
         fv = fma(y[j], P.rb[j], fv);
       }
     }
@@ -1364,6 +1372,26 @@ extern "C" int fcn_ctx_create(int device, int n, int k, const uint64_t* primes, 
   if (e == cudaSuccess) e = cudaMemcpy(x->d_mc, host.data(), sizeof(MulCtConst) * n_lanes, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&x->d_fallbacks, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(x->d_fallbacks, 0, sizeof(unsigned long long));
+  if (e == cudaSuccess && x->fp) {
+    // twist_l[j] (B/b_l)^-1 for the tensor's inverse NTT (the rescale then
+    // starts from y_j = T_j (B/b_l)^-1 directly, fv.py:473-490)
+    const int K = (int)ext.size();
+    std::vector<double2> tw((size_t)K * n);
+    for (int l = 0; l < K; ++l) {
+      const uint64_t b = ext[l];
+      const uint64_t iroot = h_powmod(x->ext->roots[l], b - 2, b);
+      const uint64_t ninv = h_powmod((uint64_t)n % b, b - 2, b);
+      uint64_t w = h_mulmod(ninv, host[0].binv[l], b);
+      for (int j = 0; j < n; ++j) {
+        const double ws = w > b / 2 ? -(double)(b - w) : (double)w;
+        tw[(size_t)l * n + j] = make_double2(ws, ws / (double)b);
+        w = h_mulmod(w, iroot, b);
+      }
+    }
+    e = cudaMalloc(&x->d_ftwist_binv, sizeof(double2) * tw.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(x->d_ftwist_binv, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice);
+  }
   if (e != cudaSuccess) {
     fcn_ctx_destroy(x);
     return check_cuda(e, "fcn_ctx_create upload");
@@ -1378,6 +1406,7 @@ extern "C" int fcn_ctx_destroy(fcn_ctx* x) {
     DeviceGuard g(x->device);
     cudaFree(x->d_mc);
     cudaFree(x->d_fallbacks);
+    cudaFree(x->d_ftwist_binv);
   }
   fcn_ring_destroy(x->ext);
   delete x;
@@ -1689,6 +1718,7 @@ struct ActArgs {
   int64_t c2 = 1, c1 = 0;
   const uint64_t* lin = nullptr;
   bool applied = false;  // set when the rescale kernel folded it into R01
+  bool prescaled = false;  // the tensor INTT already multiplied by (B/b_j)^-1 (FP64 rescale only)
 };
 
 template <int KQ, int KE>
@@ -1710,6 +1740,10 @@ static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_
     FCN_LAUNCH_CHECK(f64 ? "lift_f64_kernel" : "lift_kernel");
   } else {
     RescaleP<KQ, KE> P = make_rescale_params<KQ, KE>(x, mc);
+    if (act && act->prescaled) {
+      if (!f64) return set_error(FCN_ERR_STATE, "prescaled rescale inputs need the FP64 rescale kernel");
+      P.prescaled = 1;
+    }
     if (f64 && act && act->on) {
       P.act = 1;
       for (int i = 0; i < x->k; ++i) {
@@ -1742,6 +1776,15 @@ static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_
   return FCN_OK;
 }
 
+// The (KQ, KE) instantiation lift_or_rescale picks for a context, and
+// whether its FP64 (exact-size) kernels run.
+static bool f64_lift_rescale(const fcn_ctx* x) {
+  static const int sizes[][2] = {{2, 5}, {2, 6}, {3, 6}, {4, 8}, {4, 9}, {6, 12}, {6, 13}, {8, 16}, {8, 17}, {16, 32}};
+  for (const auto& sz : sizes)
+    if (x->k <= sz[0] && x->m <= sz[1] - sz[0]) return x->fp && x->k == sz[0] && x->k + x->m == sz[1];
+  return false;
+}
+
 static int lift_or_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t* in, uint64_t* out, int64_t cnt,
                            uint64_t* R01, uint64_t* DG, cudaStream_t st, ActArgs* act = nullptr,
                            bool* compact = nullptr) {
@@ -1760,6 +1803,15 @@ static int lift_or_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t
   FCN_TRY(16, 32)
 #undef FCN_TRY
   return set_error(FCN_ERR_PARAM, "unsupported limb counts k=%d m=%d", k, m);
+}
+
+// FCN_PRESCALE=0 keeps (B/b_j)^-1 in the rescale kernel instead of the INTT twist (A/B tests).
+static bool prescale_enabled() {
+  static const bool on = [] {
+    const char* ev = getenv("FCN_PRESCALE");
+    return !(ev && ev[0] == '0');
+  }();
+  return on;
 }
 
 // FCN_SQ_FUSE=0 disables the fused forward-NTT + tensor kernel (A/B tests).
@@ -1896,8 +1948,13 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
                                                                             x->ext->d_lc);
       FCN_LAUNCH_CHECK(x->fp ? "tensor_f64_kernel" : "tensor_kernel");
     }
-    // (iii) inverse NTT
-    int rc = launch_ntt(x->ext, T, C * 3 * K, K, 0, false, st);
+    // (iii) inverse NTT; on the FP64 path its twist also applies the
+    // rescale's first factor (B/b_j)^-1 (one multiply per residue saved)
+    const bool prescale = x->d_ftwist_binv && ntt_family(x->ext, K, 0) == 2 && f64_lift_rescale(x) && prescale_enabled();
+    NttEpi tw_epi;
+    tw_epi.mode = 0;
+    tw_epi.ftwist = x->d_ftwist_binv;
+    int rc = launch_ntt(x->ext, T, C * 3 * K, K, 0, false, st, nullptr, 1, prescale ? &tw_epi : nullptr);
     if (rc) return rc;
     // (iv) exact rescale + digit decomposition (FP64: R01 <- c2 R01 + c1 a for the activation)
     ActArgs aa;
@@ -1905,6 +1962,7 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
     aa.c2 = act_c2;
     aa.c1 = act_c1;
     aa.lin = a;
+    aa.prescaled = prescale;
     rc = lift_or_rescale(false, x, lane, T, nullptr, C, R01, direct ? DGR : DGN, st, &aa);
     if (rc) return rc;
     epi.mode = !act ? 1 : (aa.applied ? 3 : 2);

@@ -642,6 +642,23 @@ int launch_ntt_f64_sq(const fcn_ring* r, const uint64_t* a, const uint64_t* aux,
 
 static int g_force_int = -1;  // FCN_NTT_INT=1 selects the integer kernels (A/B tests)
 
+int ntt_family(const fcn_ring* r, int period, int offset) {
+  const int logn = r->logn;
+  bool v2 = logn >= 10 && logn <= 14;
+  for (int l = 0; v2 && l < period; ++l) {
+    const uint64_t q = r->primes[offset + l];
+    v2 = q >= (1ull << 34) && q < (1ull << 56);
+  }
+  if (!v2) return 0;
+  if (g_force_int < 0) {
+    const char* ev = getenv("FCN_NTT_INT");
+    g_force_int = (ev && ev[0] == '1') ? 1 : 0;
+  }
+  bool f64 = !g_force_int && r->d_ffwd;
+  for (int l = 0; f64 && l < period; ++l) f64 = r->primes[offset + l] < (1ull << 51);
+  return f64 ? 2 : 1;
+}
+
 int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st,
                const uint64_t* src, int src_div, const NttEpi* epi) {
   if (n_rows <= 0) return FCN_OK;
@@ -654,21 +671,14 @@ int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int o
   std::call_once(g_init, init_tables);
   if (g_init_err != cudaSuccess) return check_cuda(g_init_err, "ntt init");
   const int logn = r->logn;
-  bool v2 = logn >= 10 && logn <= 14;
-  for (int l = 0; v2 && l < period; ++l) {
-    const uint64_t q = r->primes[offset + l];
-    v2 = q >= (1ull << 34) && q < (1ull << 56);
-  }
-  if (!v2) {
+  const int family = ntt_family(r, period, offset);
+  if (epi && epi->ftwist && (family != 2 || epi->mode != 0))
+    return set_error(FCN_ERR_STATE, "a replacement twist needs the FP64 inverse without epilogue");
+  if (family == 0) {
     const int rc = launch_v1(r, d, n_rows, period, offset, fwd, st, src, src_div);
     return rc ? rc : launch_epi_int(r, d, n_rows, period, offset, st, epi);
   }
-  if (g_force_int < 0) {
-    const char* ev = getenv("FCN_NTT_INT");
-    g_force_int = (ev && ev[0] == '1') ? 1 : 0;
-  }
-  bool f64 = !g_force_int && r->d_ffwd;
-  for (int l = 0; f64 && l < period; ++l) f64 = r->primes[offset + l] < (1ull << 51);
+  const bool f64 = family == 2;
   if (f64 && epi && epi->mode == 2) {  // no fused FP64 form: plain inverse, then the integer epilogue
     const int rc = launch_ntt(r, d, n_rows, period, offset, false, st);
     return rc ? rc : launch_epi_int(r, d, n_rows, period, offset, st, epi);

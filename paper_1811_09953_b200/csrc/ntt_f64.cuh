@@ -514,7 +514,8 @@ static int f64_launch_t(bool fwd, int sms, uint64_t* d, int64_t n_rows, int peri
   } else if (!epi || epi->mode == 0) {
     const int g = grid_of(F64Occ<LOGN, RS, 1>::get((const void*)ntt_f64_inv<LOGN, RS>, sm, &err));
     if (err != cudaSuccess) return check_cuda(err, "ntt_f64_inv attributes");
-    ntt_f64_inv<LOGN, RS><<<g, threads, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict, r->d_ftwist);
+    ntt_f64_inv<LOGN, RS><<<g, threads, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict,
+                                                  epi && epi->ftwist ? epi->ftwist : r->d_ftwist);
   } else if (epi->out.n == 1 && epi->mode == 1) {
     const int g = grid_of(F64Occ<LOGN, RS, 2>::get((const void*)ntt_f64_inv_epi<LOGN, RS, false, false>, sm, &err));
     if (err != cudaSuccess) return check_cuda(err, "ntt_f64_inv_epi attributes");
