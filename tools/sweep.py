@@ -74,7 +74,10 @@ def main():
     res["ntt_fwd_inv_s"] = t
     res["ntt_gbs"] = byts / t / 1e9
     res["ntt_frac_hbm"] = byts / t / 1e9 / peak
-    res["ntt_frac_fp64_butterfly_peak"] = bfly / t / fp["butterfly_per_s"]
+    rs = L.fcn_ntt_f64_schedule(n.bit_length() - 1, max(W.primes))
+    res["ntt_fp64_schedule"] = rs
+    res["ntt_frac_fp64_butterfly_peak"] = bfly / t / (fp.get("butterfly_rs1_per_s", fp["butterfly_per_s"])
+                                                       if rs >= 1 else fp["butterfly_per_s"])
     assert torch.equal(y, x)
 
     # square + relinearisation (dnum = 3)
