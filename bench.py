@@ -403,9 +403,14 @@ def run_gpu(args, ws, rank, local):
         transport = args.transport
         if transport == "p2p":
             # pre-flight: every rank must be able to map the symmetric buffers
+            # and produce the same bytes as the NCCL all-gather schedule
             ok = 1
             try:
-                fdist.eval_encrypted_sharded(net, tensor, ek, cfg, encoding="batched", transport="p2p")
+                got = fdist.eval_encrypted_sharded(net, tensor, ek, cfg, encoding="batched", transport="p2p")[0]
+                want = fdist.eval_encrypted_sharded(net, tensor, ek, cfg, encoding="batched", transport="nccl")[0]
+                if not torch.equal(got.buf, want.buf):
+                    ok = 0
+                    args.transport_note = "p2p result differs from the NCCL schedule"
             except Exception as exc:  # noqa: BLE001 - reported in config
                 ok = 0
                 args.transport_note = f"p2p unavailable ({type(exc).__name__}: {exc})"[:200]
