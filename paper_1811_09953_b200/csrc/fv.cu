@@ -1062,11 +1062,18 @@ __global__ void key_to_f64_kernel(const uint64_t* __restrict__ w, double2* __res
 // exact) and |.| < 0.75 q; sums are reduced after every 4 products (< 3.5 q).
 // Both outputs' 2D key words stay in registers across the ciphertexts the
 // thread walks; the next ciphertext's D digit loads are issued early.
-// LEAN (more than 8 digits): only the signed key words stay in registers and
+// LEAN: only the signed key words stay in registers and
 // each quotient factor is recomputed as w * (1/q) (relative error 3 2^-53:
 // products |.| < 0.875 q, so sums are reduced before every 3rd product).
+// From 5 digits on the kernel runs LEAN: the key words take half the
+// registers, so up to 8 digits fit 3 CTAs per SM (24 warps): more loads in
+// flight, 74% -> 80% of the HBM copy peak at cfg2 (D = 7), against one extra
+// DMUL per product.
+#ifndef FCN_KM_LEAN_FROM
+#define FCN_KM_LEAN_FROM 5
+#endif
 template <int DMAX, bool LEAN = false>
-__global__ void __launch_bounds__(256, 2) keymac_f64_kernel(const uint64_t* __restrict__ DG, const double2* __restrict__ kg,
+__global__ void __launch_bounds__(256, DMAX <= 8 ? 3 : 2) keymac_f64_kernel(const uint64_t* __restrict__ DG, const double2* __restrict__ kg,
                                                             const double2* __restrict__ ka, uint64_t* __restrict__ ACC,
                                                             int64_t C, int D, int k, int logn,
                                                             const LimbConst* __restrict__ lcs) {
@@ -1839,8 +1846,10 @@ static int launch_keymac(const uint64_t* DG, const fcn_keys* keys, uint64_t* ACC
   case DD:                                                                                                         \
     keymac_f64_kernel<DD, LN><<<grid, 256, 0, st>>>(DG, keys->d_fg, keys->d_fa, ACC, C, DD, k, x->logn, x->ext->d_lc); \
     break;
-      FCN_KM(1, false) FCN_KM(2, false) FCN_KM(3, false) FCN_KM(4, false) FCN_KM(5, false) FCN_KM(6, false)
-      FCN_KM(7, false) FCN_KM(8, false) FCN_KM(9, true) FCN_KM(10, true) FCN_KM(11, true) FCN_KM(12, true)
+      FCN_KM(1, 1 >= FCN_KM_LEAN_FROM) FCN_KM(2, 2 >= FCN_KM_LEAN_FROM) FCN_KM(3, 3 >= FCN_KM_LEAN_FROM)
+      FCN_KM(4, 4 >= FCN_KM_LEAN_FROM) FCN_KM(5, 5 >= FCN_KM_LEAN_FROM) FCN_KM(6, 6 >= FCN_KM_LEAN_FROM)
+      FCN_KM(7, 7 >= FCN_KM_LEAN_FROM) FCN_KM(8, 8 >= FCN_KM_LEAN_FROM) FCN_KM(9, true) FCN_KM(10, true)
+      FCN_KM(11, true) FCN_KM(12, true)
 #undef FCN_KM
     }
     FCN_LAUNCH_CHECK("keymac_f64_kernel");
