@@ -1100,16 +1100,29 @@ __global__ void __launch_bounds__(256, DMAX <= 8 ? 3 : 2) keymac_f64_kernel(cons
   const int64_t per = (C + gridDim.y - 1) / gridDim.y;
   const int64_t c0 = (int64_t)blockIdx.y * per;
   const int64_t c1 = c0 + per < C ? c0 + per : C;
-  uint64_t nx[DMAX];
-  if (c0 < c1) {
+  // digits of the next PF ciphertexts in flight (PF = 2 for few digits, so
+  // enough loads are outstanding per SM)
+  constexpr int PF = DMAX <= 4 ? 2 : 1;
+  uint64_t nx[DMAX], nx2[PF > 1 ? DMAX : 1];
 #pragma unroll
-    for (int d = 0; d < DMAX; ++d) nx[d] = d < D ? DG[((c0 * D + d) * k + l) * n + coef] : 0;
+  for (int d = 0; d < DMAX; ++d) nx[d] = (c0 < c1 && d < D) ? DG[((c0 * D + d) * k + l) * n + coef] : 0;
+  if (PF > 1) {
+#pragma unroll
+    for (int d = 0; d < DMAX; ++d) nx2[d] = (c0 + 1 < c1 && d < D) ? DG[(((c0 + 1) * D + d) * k + l) * n + coef] : 0;
   }
   for (int64_t ct = c0; ct < c1; ++ct) {
     double xs[DMAX];
 #pragma unroll
     for (int d = 0; d < DMAX; ++d) xs[d] = u2f(nx[d]);
-    if (ct + 1 < c1) {
+    if (PF > 1) {
+#pragma unroll
+      for (int d = 0; d < DMAX; ++d) nx[d] = nx2[d];
+      if (ct + 2 < c1) {
+#pragma unroll
+        for (int d = 0; d < DMAX; ++d)
+          if (d < D) nx2[d] = DG[(((ct + 2) * D + d) * k + l) * n + coef];
+      }
+    } else if (ct + 1 < c1) {
 #pragma unroll
       for (int d = 0; d < DMAX; ++d)
         if (d < D) nx[d] = DG[(((ct + 1) * D + d) * k + l) * n + coef];
