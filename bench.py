@@ -54,6 +54,7 @@ def _args():
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of one CUDA graph per step")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
     return ap.parse_args()
 
@@ -423,6 +424,20 @@ def run_gpu(args, ws, rank, local):
                                                           transport=transport)[0]
     else:
         evaluate = lambda t: engine.eval_encrypted(net, t, ek, cfg, encoding="batched")[0]  # noqa: E731
+        if not args.no_graph:
+            # the whole network as one CUDA graph over the resident input buffer
+            try:
+                g = engine.EvalGraph(net, tensor, ek, cfg, encoding="batched")
+                ref = evaluate(tensor)
+                if torch.equal(g.replay().buf, ref.buf):
+                    evaluate = lambda t: g.replay() if t is tensor else engine.eval_encrypted(  # noqa: E731
+                        net, t, ek, cfg, encoding="batched")[0]
+                    args.graph_used = True
+                    args.graph_kernels = g.kernels
+                else:
+                    args.graph_note = "graph replay differs from eager evaluation"
+            except Exception as exc:  # noqa: BLE001 - reported in config
+                args.graph_note = f"graph capture failed ({type(exc).__name__}: {exc})"[:200]
 
     def barrier():
         if ws > 1:
@@ -445,6 +460,8 @@ def run_gpu(args, ws, rank, local):
         torch.cuda.synchronize()
         barrier()
     launches = (L.fcn_launch_count() - n0) // args.steps
+    if getattr(args, "graph_used", False):
+        launches = args.graph_kernels  # replays launch the captured kernels, not through the host counter
     t_step = e0.elapsed_time(e1) / 1e3 / args.steps
     if ws > 1:
         tt = torch.tensor([t_step], device="cuda", dtype=torch.float64)
@@ -581,6 +598,8 @@ def run_gpu(args, ws, rank, local):
         "data": "synthetic (seeded uint8 images, one per slot; random-init pruned pow2 weights)",
         "config": dict(_config(W, args.workload, ws, args.shard, hops,
                                "inputs larger than L2 (%d MB of input ciphertexts per step)" % (tensor.buf.numel() * 8 >> 20)),
+                       cuda_graph=bool(getattr(args, "graph_used", False)),
+                       **({"graph_note": args.graph_note} if getattr(args, "graph_note", None) else {}),
                        **({"transport": getattr(args, "transport_used", args.transport)} if sharded else {}),
                        **({"transport_note": args.transport_note} if getattr(args, "transport_note", None) else {})),
         "clocks": clk.summary(),

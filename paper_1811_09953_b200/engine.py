@@ -650,14 +650,16 @@ def _gather_meta(taps, depths, scales, empty_scale):
 
 
 def eval_encrypted(net, tensor: CipherTensor, ek: EvalKeys, cfg: FixedPointConfig, workers: int = 1,
-                   encoding: str = "integer", mul_chunk: int | None = None):
+                   encoding: str = "integer", mul_chunk: int | None = None, timing: bool = True):
     """Execute the compiled plan over a ciphertext tensor, tallying every HOP.
 
     Same contract as reference engine.eval_encrypted (engine.py:651-774);
     `workers` is accepted for API compatibility (the GPU parallelises
     every layer's outputs).  `encoding` selects the plaintext encoding of
     the integer constants ("integer" = the reference's base-2 encoder;
-    "batched" = constant polynomials for SIMD-packed slots)."""
+    "batched" = constant polynomials for SIMD-packed slots).  `timing=False`
+    records no per-layer CUDA events (layer wall_ms then reads 0), e.g. for
+    CUDA-graph capture (`EvalGraph`)."""
     if encoding not in ENCODINGS:
         raise EngineError(f"encoding must be one of {ENCODINGS}")
     if not isinstance(tensor, CipherTensor):
@@ -683,19 +685,56 @@ def eval_encrypted(net, tensor: CipherTensor, ek: EvalKeys, cfg: FixedPointConfi
     factor = tensor.scale_factor
     events = []
     for plan, lw in zip(compiled.plans, low):
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record()
+        if timing:
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
         n_out = lw[1].n_out if lw[0] in ("linear", "pool") else plan.nodes
         depths, scales, scale, factor = _meta_step(plan, lw, depths, scales, scale, factor, prec)
         cur = _layer_range(params, lane, ek, plan, lw, cur, 0, n_out, encoding, mul_chunk)
-        ev1.record()
-        events.append((ev0, ev1))
+        if timing:
+            ev1.record()
+            events.append((ev0, ev1))
     # wall_ms resolves from the events on first access (no device sync here)
-    counter.layer_counts = [TimedLayerCounts(c, (a, b, 1.0)) for c, (a, b) in zip(counter.layer_counts, events)]
+    if timing:
+        counter.layer_counts = [TimedLayerCounts(c, (a, b, 1.0)) for c, (a, b) in zip(counter.layer_counts, events)]
     out = CipherTensor(compiled.out_shape, scale_exponent=scale, scale_factor=factor, buf=cur, params=params, lane=lane,
                        depths=depths, scales=scales)
     return out, counter
+
+
+# ---------------------------------------------------------------- CUDA graphs
+
+
+class EvalGraph:
+    """One `eval_encrypted` over a fixed input buffer, captured as a CUDA graph.
+
+    The plan's ~17 kernel launches per cfg2 step (and the host-side layer
+    walk that issues them) become one graph launch: `replay()` re-runs the
+    whole network on whatever ciphertexts are in `tensor.buf` at that moment
+    and returns the output CipherTensor, whose buffer is the graph's own
+    (overwritten by the next replay).  Intermediates live in the graph's
+    private memory pool.  Same bytes as `eval_encrypted` (tested)."""
+
+    def __init__(self, net, tensor: CipherTensor, ek: EvalKeys, cfg: FixedPointConfig, encoding: str = "batched",
+                 mul_chunk: int | None = None):
+        import torch
+
+        # lowering, kernel attributes and workspace sizes settle outside the capture
+        eval_encrypted(net, tensor, ek, cfg, encoding=encoding, mul_chunk=mul_chunk, timing=False)
+        torch.cuda.synchronize()
+        self.tensor = tensor
+        self.graph = torch.cuda.CUDAGraph()
+        lib = _lib.lib()
+        n0 = lib.fcn_launch_count()
+        with torch.cuda.graph(self.graph):
+            self.out, self.counter = eval_encrypted(net, tensor, ek, cfg, encoding=encoding, mul_chunk=mul_chunk,
+                                                    timing=False)
+        self.kernels = int(lib.fcn_launch_count() - n0)  # libfcn kernels each replay runs
+
+    def replay(self) -> CipherTensor:
+        self.graph.replay()
+        return self.out
 
 
 # ---------------------------------------------------------------- streaming

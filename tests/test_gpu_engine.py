@@ -347,3 +347,31 @@ def test_evaluate_stream_matches_eval(E):
     assert len(got) == 5
     for g, w in zip(got, wants):
         assert np.array_equal(g.numpy().view(np.uint64), w)
+
+
+def test_eval_graph_replay_matches_eager(E):
+    """EvalGraph: the cfg2 network captured once as a CUDA graph; replays are
+    byte-identical to eval_encrypted, also after new ciphertexts are copied
+    into the captured input buffer (cfg2 shape, reduced slot count is not
+    possible: the ring is fixed, so a second batch is a different seed)."""
+    import torch
+
+    from paper_1811_09953_b200 import configs
+    from paper_1811_09953_b200 import fv
+
+    W = configs.WORKLOADS["cfg2"]
+    P = fv.EncryptionParams(W.n, W.primes, (W.t,), W.beta)
+    cfg = W.fixed_point()
+    net = configs.build_network("cfg2")
+    sk, pk, ek = fv.keygen(P, configs.SEED_KEYS)
+    x = configs.build_inputs("cfg2")
+    tensor = E.encrypt_tensor_batched(pk, P, x, cfg, 0, configs.SEED_ENC)
+    other = E.encrypt_tensor_batched(pk, P, x[::-1].copy(), cfg, 0, configs.SEED_ENC + 7)
+    g = E.EvalGraph(net, tensor, ek, cfg, encoding="batched")
+    assert g.kernels > 0
+    want1 = E.eval_encrypted(net, tensor, ek, cfg, encoding="batched")[0].buf.clone()
+    want2 = E.eval_encrypted(net, other, ek, cfg, encoding="batched")[0].buf.clone()
+    assert torch.equal(g.replay().buf, want1)
+    tensor.buf.copy_(other.buf)
+    assert torch.equal(g.replay().buf, want2)
+    assert torch.equal(g.replay().buf, want2)
