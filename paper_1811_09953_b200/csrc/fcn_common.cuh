@@ -308,6 +308,10 @@ struct NttEpi {
   // mode 0 on the FP64 inverse: replacement twist table (n^-1 psi^-j times a
   // per-limb constant), e.g. the rescale's (B/b_l)^-1 folded into the tensor's INTT
   const double2* ftwist = nullptr;
+  // FP64 kernels only: rows as signed residues in raw doubles instead of
+  // canonical u64 (forward: output; plain inverse: input and output; epilogue
+  // inverse: input), the internal format of the square pipeline
+  int dbl = 0;
   uint64_t c2[kEpiLimbs], c1[kEpiLimbs];
   double fc2[kEpiLimbs], fc2q[kEpiLimbs], fc1[kEpiLimbs], fc1q[kEpiLimbs];
 };
@@ -322,7 +326,7 @@ int ntt_family(const fcn_ring* r, int period, int offset);
 // tensor (ntt_f64.cuh ntt_f64_fwd_sq): FP64 rings with 2^10 <= n <= 2^14 only
 // (returns 1 when not applicable, nothing launched).
 int launch_ntt_square_tensor(const fcn_ring* r, const uint64_t* a, const uint64_t* aux, uint64_t* Tout, int64_t C,
-                             int k, int m, cudaStream_t st);
+                             int k, int m, cudaStream_t st, bool dbl = false);
 
 inline int grid_for(int64_t work, int block, int max_blocks = 148 * 16) {
   int64_t g = (work + block - 1) / block;

@@ -458,6 +458,8 @@ struct RescaleP {
   int act;
   // FP64 path: the inputs are already y_j = T_j (B/b_j)^-1 (folded into the INTT's twist)
   int prescaled;
+  // ... and stored as signed doubles (|y_j| <= b_j / 2 + 2^-40 b_j), not canonical u64
+  int dbl_in;
   double fc2[KQ], fc2q[KQ], fc1[KQ], fc1q[KQ];
 };
 
@@ -915,8 +917,10 @@ __global__ void __launch_bounds__(256, FCN_RS_MINB(KQ))
     for (int j = 0; j < KE; ++j) {
       y[j] = 0.0;
       if (j < K) {
-        const double x = u2f(cur[j]);
-        if (P.prescaled)
+        const double x = P.dbl_in ? __longlong_as_double((long long)cur[j]) : u2f(cur[j]);
+        if (P.dbl_in)
+          y[j] = x;
+        else if (P.prescaled)
           y[j] = x > 0.5 * P.fb[j] ? x - P.fb[j] : x;  // centred: |y_j| <= b_j / 2
         else
           y[j] = fmulq_m(x, P.fbinv[j], P.fbinvq[j], P.fb[j]);
@@ -1072,7 +1076,9 @@ __global__ void key_to_f64_kernel(const uint64_t* __restrict__ w, double2* __res
 #ifndef FCN_KM_LEAN_FROM
 #define FCN_KM_LEAN_FROM 5
 #endif
-template <int DMAX, bool LEAN = false>
+// DBL: digits in and accumulators out are signed residues as raw doubles
+// (the square pipeline's internal row format), |.| <= q/2 + 2^-40 q.
+template <int DMAX, bool LEAN = false, bool DBL = false>
 __global__ void __launch_bounds__(256, DMAX <= 8 ? 3 : 2) keymac_f64_kernel(const uint64_t* __restrict__ DG, const double2* __restrict__ kg,
                                                             const double2* __restrict__ ka, uint64_t* __restrict__ ACC,
                                                             int64_t C, int D, int k, int logn,
@@ -1113,7 +1119,7 @@ __global__ void __launch_bounds__(256, DMAX <= 8 ? 3 : 2) keymac_f64_kernel(cons
   for (int64_t ct = c0; ct < c1; ++ct) {
     double xs[DMAX];
 #pragma unroll
-    for (int d = 0; d < DMAX; ++d) xs[d] = u2f(nx[d]);
+    for (int d = 0; d < DMAX; ++d) xs[d] = DBL ? __longlong_as_double((long long)nx[d]) : u2f(nx[d]);
     if (PF > 1) {
 #pragma unroll
       for (int d = 0; d < DMAX; ++d) nx[d] = nx2[d];
@@ -1144,8 +1150,9 @@ __global__ void __launch_bounds__(256, DMAX <= 8 ? 3 : 2) keymac_f64_kernel(cons
         }
       }
     }
-    ACC[((ct * 2 + 0) * k + l) * n + coef] = f2u_canon(fredq(g, qi, q), q);
-    ACC[((ct * 2 + 1) * k + l) * n + coef] = f2u_canon(fredq(a, qi, q), q);
+    const double gr = fredq(g, qi, q), ar = fredq(a, qi, q);
+    ACC[((ct * 2 + 0) * k + l) * n + coef] = DBL ? (uint64_t)__double_as_longlong(gr) : f2u_canon(gr, q);
+    ACC[((ct * 2 + 1) * k + l) * n + coef] = DBL ? (uint64_t)__double_as_longlong(ar) : f2u_canon(ar, q);
   }
 }
 
@@ -1739,6 +1746,7 @@ struct ActArgs {
   const uint64_t* lin = nullptr;
   bool applied = false;  // set when the rescale kernel folded it into R01
   bool prescaled = false;  // the tensor INTT already multiplied by (B/b_j)^-1 (FP64 rescale only)
+  bool dbl_in = false;     // ... and left the rows as signed doubles
 };
 
 template <int KQ, int KE>
@@ -1763,6 +1771,7 @@ static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_
     if (act && act->prescaled) {
       if (!f64) return set_error(FCN_ERR_STATE, "prescaled rescale inputs need the FP64 rescale kernel");
       P.prescaled = 1;
+      P.dbl_in = act->dbl_in ? 1 : 0;
     }
     if (f64 && act && act->on) {
       P.act = 1;
@@ -1825,6 +1834,17 @@ static int lift_or_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t
   return set_error(FCN_ERR_PARAM, "unsupported limb counts k=%d m=%d", k, m);
 }
 
+// Whether the square pipeline's workspace rows stay signed doubles between its
+// FP64 kernels (FCN_DBL_ROWS=0: canonical u64 rows, A/B tests).  Needs the
+// FP64 key MAC (at most 12 digits, keys converted) and the fused epilogue.
+static bool dbl_rows(const fcn_ctx* x) {
+  static const bool on = [] {
+    const char* ev = getenv("FCN_DBL_ROWS");
+    return !(ev && ev[0] == '0');
+  }();
+  return on && x->fp && x->ell + 1 <= 12;
+}
+
 // FCN_PRESCALE=0 keeps (B/b_j)^-1 in the rescale kernel instead of the INTT twist (A/B tests).
 static bool prescale_enabled() {
   static const bool on = [] {
@@ -1844,20 +1864,26 @@ static bool sq_fuse_enabled() {
 }
 
 static int launch_keymac(const uint64_t* DG, const fcn_keys* keys, uint64_t* ACC, int64_t C, int D, int k, const fcn_ctx* x,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool dbl = false) {
   const int64_t kn = (int64_t)k * x->n;  // one residue per thread
   const int bx = (int)((kn + 255) / 256);
   int64_t split = (148LL * 1024 * 4 + kn - 1) / kn;
   if (split > C) split = C;
   if (split < 1) split = 1;
   dim3 grid(bx, (unsigned)split);
+  if (dbl && !(keys->d_fg && D <= 12)) return set_error(FCN_ERR_STATE, "double-format rows need the FP64 key MAC");
   if (keys->d_fg && D <= 12) {
     // exact digit count as the template argument: key words of unused digits take no registers;
     // beyond 8 digits only the key words stay in registers (LEAN); beyond 12 they spill: integer kernel
     switch (D) {
-#define FCN_KM(DD, LN)                                                                                             \
-  case DD:                                                                                                         \
-    keymac_f64_kernel<DD, LN><<<grid, 256, 0, st>>>(DG, keys->d_fg, keys->d_fa, ACC, C, DD, k, x->logn, x->ext->d_lc); \
+#define FCN_KM(DD, LN)                                                                                            \
+  case DD:                                                                                                        \
+    if (dbl)                                                                                                      \
+      keymac_f64_kernel<DD, LN, true><<<grid, 256, 0, st>>>(DG, keys->d_fg, keys->d_fa, ACC, C, DD, k, x->logn,    \
+                                                              x->ext->d_lc);                                      \
+    else                                                                                                          \
+      keymac_f64_kernel<DD, LN, false><<<grid, 256, 0, st>>>(DG, keys->d_fg, keys->d_fa, ACC, C, DD, k, x->logn,   \
+                                                               x->ext->d_lc);                                     \
     break;
       FCN_KM(1, 1 >= FCN_KM_LEAN_FROM) FCN_KM(2, 2 >= FCN_KM_LEAN_FROM) FCN_KM(3, 3 >= FCN_KM_LEAN_FROM)
       FCN_KM(4, 4 >= FCN_KM_LEAN_FROM) FCN_KM(5, 5 >= FCN_KM_LEAN_FROM) FCN_KM(6, 6 >= FCN_KM_LEAN_FROM)
@@ -1946,7 +1972,7 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
       int rc = lift_or_rescale(true, x, lane, a, EA, C * 2, nullptr, nullptr, st, nullptr, &fused);
       if (rc) return rc;
       if (fused) {
-        rc = launch_ntt_square_tensor(x->ext, a, EA, T, C, k, x->m, st);
+        rc = launch_ntt_square_tensor(x->ext, a, EA, T, C, k, x->m, st, dbl_rows(x));
         if (rc) return rc < 0 ? rc : set_error(FCN_ERR_STATE, "fused square tensor unavailable");
       } else {  // the lift wrote the full extended rows
         rc = launch_ntt(x->ext, EA, C * 2 * K, K, 0, true, st);
@@ -1973,9 +1999,13 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
     // (iii) inverse NTT; on the FP64 path its twist also applies the
     // rescale's first factor (B/b_j)^-1 (one multiply per residue saved)
     const bool prescale = x->d_ftwist_binv && ntt_family(x->ext, K, 0) == 2 && f64_lift_rescale(x) && prescale_enabled();
+    // the square pipeline keeps its workspace rows as signed doubles from the
+    // fused forward NTT to the final INTT (no u64 round trips in between)
+    const bool dbl = fused && prescale && dbl_rows(x);
     NttEpi tw_epi;
     tw_epi.mode = 0;
     tw_epi.ftwist = x->d_ftwist_binv;
+    tw_epi.dbl = dbl;
     int rc = launch_ntt(x->ext, T, C * 3 * K, K, 0, false, st, nullptr, 1, prescale ? &tw_epi : nullptr);
     if (rc) return rc;
     // (iv) exact rescale + digit decomposition (FP64: R01 <- c2 R01 + c1 a for the activation)
@@ -1985,21 +2015,25 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
     aa.c1 = act_c1;
     aa.lin = a;
     aa.prescaled = prescale;
+    aa.dbl_in = dbl;
     rc = lift_or_rescale(false, x, lane, T, nullptr, C, R01, direct ? DGR : DGN, st, &aa);
     if (rc) return rc;
     epi.mode = !act ? 1 : (aa.applied ? 3 : 2);
     // (v) digits to NTT (broadcast rows when digits are limb-independent), key MAC
+    NttEpi dg_epi;
+    dg_epi.dbl = dbl;
     if (direct)
-      rc = launch_ntt(x->ext, DGN, C * D * k, k, 0, true, st, DGR, k);
+      rc = launch_ntt(x->ext, DGN, C * D * k, k, 0, true, st, DGR, k, dbl ? &dg_epi : nullptr);
     else
-      rc = launch_ntt(x->ext, DGN, C * D * k, k, 0, true, st);
+      rc = launch_ntt(x->ext, DGN, C * D * k, k, 0, true, st, nullptr, 1, dbl ? &dg_epi : nullptr);
     if (rc) return rc;
-    rc = launch_keymac(DGN, keys, ACC, C, D, k, x, st);
+    rc = launch_keymac(DGN, keys, ACC, C, D, k, x, st, dbl);
     if (rc) return rc;
     // (vi) inverse NTT with the fused epilogue: out = R01 + INTT(ACC)
     //      [ * c2 + c1 * a  when FCN_MUL_ACT: the a2 x^2 + a1 x activation]
     epi.add = R01;
     epi.lin = a;
+    epi.dbl = dbl;
     epi.out.n = n_dst;
     for (int d = 0; d < n_dst; ++d) epi.out.dst[d] = d_outs[d] + off * ct_words;
     rc = launch_ntt(x->ext, ACC, C * 2 * k, k, 0, false, st, nullptr, 1, &epi);

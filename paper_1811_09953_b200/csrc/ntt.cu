@@ -638,7 +638,7 @@ namespace fcn {
 
 template <int RS>
 int launch_ntt_f64_sq(const fcn_ring* r, const uint64_t* a, const uint64_t* aux, uint64_t* Tout, int64_t units, int k,
-                      int m, cudaStream_t st, int sms);  // ntt_f64.cuh
+                      int m, cudaStream_t st, int sms, bool dbl);  // ntt_f64.cuh
 
 static int g_force_int = -1;  // FCN_NTT_INT=1 selects the integer kernels (A/B tests)
 
@@ -662,7 +662,7 @@ int ntt_family(const fcn_ring* r, int period, int offset) {
 int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st,
                const uint64_t* src, int src_div, const NttEpi* epi) {
   if (n_rows <= 0) return FCN_OK;
-  if (fwd) epi = nullptr;
+  if (fwd && epi && !epi->dbl) epi = nullptr;  // a forward takes only the row-format flag
   if (!src) {
     src = d;
     src_div = 1;
@@ -674,6 +674,8 @@ int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int o
   const int family = ntt_family(r, period, offset);
   if (epi && epi->ftwist && (family != 2 || epi->mode != 0))
     return set_error(FCN_ERR_STATE, "a replacement twist needs the FP64 inverse without epilogue");
+  if (epi && epi->dbl && (family != 2 || epi->mode == 2))
+    return set_error(FCN_ERR_STATE, "double-format rows need the FP64 kernels");
   if (family == 0) {
     const int rc = launch_v1(r, d, n_rows, period, offset, fwd, st, src, src_div);
     return rc ? rc : launch_epi_int(r, d, n_rows, period, offset, st, epi);
@@ -707,7 +709,7 @@ int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int o
 }
 
 int launch_ntt_square_tensor(const fcn_ring* r, const uint64_t* a, const uint64_t* aux, uint64_t* Tout, int64_t C,
-                             int k, int m, cudaStream_t st) {
+                             int k, int m, cudaStream_t st, bool dbl) {
   if (C <= 0) return FCN_OK;
   if (!r->d_ffwd || r->logn < 10 || r->logn > 14 || r->L != k + m) return 1;
   uint64_t qmax = 0;
@@ -719,9 +721,9 @@ int launch_ntt_square_tensor(const fcn_ring* r, const uint64_t* a, const uint64_
   if (g_init_err != cudaSuccess) return check_cuda(g_init_err, "ntt init");
   const int64_t units = C * (k + m);
   switch (f64_schedule(r->logn, qmax)) {
-    case 2: return launch_ntt_f64_sq<2>(r, a, aux, Tout, units, k, m, st, g_sms);
-    case 1: return launch_ntt_f64_sq<1>(r, a, aux, Tout, units, k, m, st, g_sms);
-    default: return launch_ntt_f64_sq<0>(r, a, aux, Tout, units, k, m, st, g_sms);
+    case 2: return launch_ntt_f64_sq<2>(r, a, aux, Tout, units, k, m, st, g_sms, dbl);
+    case 1: return launch_ntt_f64_sq<1>(r, a, aux, Tout, units, k, m, st, g_sms, dbl);
+    default: return launch_ntt_f64_sq<0>(r, a, aux, Tout, units, k, m, st, g_sms, dbl);
   }
 }
 

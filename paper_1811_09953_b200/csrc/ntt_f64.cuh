@@ -165,7 +165,10 @@ __device__ __forceinline__ void fwd_body(double* x, int tid, double* fs, const d
   fwd_ctf_last<LOGN, RS, LOGN - 5>(x, tid, T, tl, q, qi, w3);
 }
 
-template <int LOGN, int RS>
+// DBL: outputs are the reduced signed residues as raw doubles (|x| <= q/2 +
+// 2^-40 q), the internal row format of the square pipeline (no conversion to
+// canonical u64 and back between its kernels).
+template <int LOGN, int RS, bool DBL = false>
 __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     ntt_f64_fwd(uint64_t* __restrict__ data, int64_t n_rows, int period, int offset, const LimbConst* __restrict__ lcs,
                 const double2* __restrict__ tws, const double2* __restrict__ twl, const uint64_t* __restrict__ src,
@@ -191,7 +194,10 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     for (int j = 0; j < 32; ++j) x[j] = u2f((uint64_t)__double_as_longlong(x[j]));
     fwd_body<LOGN, RS>(x, tid, fs, tw, twl + (int64_t)limb * N, q, qi);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) sm[tid * 33 + j] = f2u_canon(fredq(x[j], qi, q), q);
+    for (int j = 0; j < 32; ++j) {
+      const double y = fredq(x[j], qi, q);
+      sm[tid * 33 + j] = DBL ? (uint64_t)__double_as_longlong(y) : f2u_canon(y, q);
+    }
     // A warp's 32 threads own residues [1024 w, 1024 w + 1024): it copies
     // them out coalesced on its own (no CTA barrier), while the next row's
     // loads are in flight.
@@ -223,7 +229,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 // copy-out and read back by the very thread that wrote it.  Input rows: limb
 // l < k from the ciphertexts a ([C][2][k][n]), l >= k from the lift's compact
 // auxiliary rows aux ([C][2][m][n]).
-template <int LOGN, int RS>
+template <int LOGN, int RS, bool DBL = false>
 __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     ntt_f64_fwd_sq(const uint64_t* __restrict__ a, const uint64_t* __restrict__ aux, uint64_t* __restrict__ Tout,
                    int64_t units, int k, int m, const LimbConst* __restrict__ lcs, const double2* __restrict__ tws,
@@ -296,10 +302,12 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
           const double x0 = x[2 * i + v], x1 = fw[66 * i + v];
-          t0[v] = f2u_canon(fprod(x0, x0, q, qi), q);
-          const double mm = fprod(x0, x1, q, qi);
-          t1[v] = f2u_canon(fredq(mm + mm, qi, q), q);
-          t2[v] = f2u_canon(fprod(x1, x1, q, qi), q);
+          const double p0 = fprod(x0, x0, q, qi), mm = fprod(x0, x1, q, qi), p2 = fprod(x1, x1, q, qi);
+          const double p1 = fredq(mm + mm, qi, q);
+          // DBL: signed doubles, |.| < 0.6 q (the INTT's input bound assumes <= q)
+          t0[v] = DBL ? (uint64_t)__double_as_longlong(p0) : f2u_canon(p0, q);
+          t1[v] = DBL ? (uint64_t)__double_as_longlong(p1) : f2u_canon(p1, q);
+          t2[v] = DBL ? (uint64_t)__double_as_longlong(p2) : f2u_canon(p2, q);
         }
         o0[32 * i] = make_ulonglong2(t0[0], t0[1]);
         o1[32 * i] = make_ulonglong2(t1[0], t1[1]);
@@ -316,7 +324,9 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
   }
 }
 
-template <int LOGN, int RS>
+// DBL: rows in and out are signed residues as raw doubles (in: |x| <= q,
+// out: |x| <= q/2 + 2^-40 q).
+template <int LOGN, int RS, bool DBL = false>
 __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     ntt_f64_inv(uint64_t* __restrict__ data, int64_t n_rows, int period, int offset, const LimbConst* __restrict__ lcs,
                 const double2* __restrict__ tws, const double2* __restrict__ twists) {
@@ -345,7 +355,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     cp_async_wait_all();
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = u2f(sm[tid * 33 + j]);
+    for (int j = 0; j < 32; ++j) x[j] = DBL ? __longlong_as_double((long long)sm[tid * 33 + j]) : u2f(sm[tid * 33 + j]);
     inv_ctf<LOGN, RS, 5, 0>(x, 0, tw, q, qi);
 #pragma unroll
     for (int j = 0; j < 32; ++j) fs[tid * 33 + j] = x[j];
@@ -384,7 +394,8 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const double2 w = ld_ftw(twist + tid + j * T);
-      p[tid + j * T] = f2u_canon(fredq(fmulq(x[j], w.x, w.y, q), qi, q), q);
+      const double y = fredq(fmulq(x[j], w.x, w.y, q), qi, q);
+      p[tid + j * T] = DBL ? (uint64_t)__double_as_longlong(y) : f2u_canon(y, q);
     }
   }
   cp_async_wait_all();
@@ -395,7 +406,8 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 // during the last pass (each thread fetches exactly the residues it will
 // combine, so no barrier is needed); the next input row is prefetched into
 // registers instead (coalesced, as in the forward kernel).
-template <int LOGN, int RS, bool SCALE, bool FAN>
+// DBL: the input rows (data) are signed residues as raw doubles, |x| <= q.
+template <int LOGN, int RS, bool SCALE, bool FAN, bool DBL = false>
 __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     ntt_f64_inv_epi(const uint64_t* __restrict__ data, int64_t n_rows, int period, int offset,
                     const LimbConst* __restrict__ lcs, const double2* __restrict__ tws,
@@ -423,7 +435,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     for (int j = 0; j < 32; ++j) sm[pst + j * (T + T / 32)] = (uint64_t)__double_as_longlong(x[j]);
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = u2f(sm[tid * 33 + j]);
+    for (int j = 0; j < 32; ++j) x[j] = DBL ? __longlong_as_double((long long)sm[tid * 33 + j]) : u2f(sm[tid * 33 + j]);
     inv_ctf<LOGN, RS, 5, 0>(x, 0, tw, q, qi);
     __syncthreads();
 #pragma unroll
@@ -497,48 +509,54 @@ struct F64Occ {
   }
 };
 
+// Launch one FP64 NTT kernel with the grid its occupancy allows.
+template <int LOGN, int RS, int V, class Kern, class... Args>
+static int f64_go(Kern kern, int sms, int64_t n_rows, size_t sm, cudaStream_t st, Args... args) {
+  cudaError_t err = cudaSuccess;
+  const int occ = F64Occ<LOGN, RS, V>::get((const void*)kern, sm, &err);
+  if (err != cudaSuccess) return check_cuda(err, "FP64 NTT attributes");
+  int64_t g = (int64_t)sms * occ;
+  if (g > n_rows) g = n_rows;
+  kern<<<(int)g, (1 << LOGN) / 32, sm, st>>>(args...);
+  FCN_LAUNCH_CHECK("ntt_f64");
+  return FCN_OK;
+}
+
 template <int LOGN, int RS>
 static int f64_launch_t(bool fwd, int sms, uint64_t* d, int64_t n_rows, int period, int offset, const fcn_ring* r,
                         cudaStream_t st, const uint64_t* src, int src_div, const NttEpi* epi) {
-  constexpr int threads = (1 << LOGN) / 32;
   const size_t sm = (size_t)((1 << LOGN) + (1 << LOGN) / 32 + 2) * sizeof(uint64_t);
-  cudaError_t err = cudaSuccess;
-  auto grid_of = [&](int occ) {
-    int64_t g = (int64_t)sms * occ;
-    return (int)(g > n_rows ? n_rows : g);
-  };
+  const bool dbl = epi && epi->dbl;
   if (fwd) {
-    const int g = grid_of(F64Occ<LOGN, RS, 0>::get((const void*)ntt_f64_fwd<LOGN, RS>, sm, &err));
-    if (err != cudaSuccess) return check_cuda(err, "ntt_f64_fwd attributes");
-    ntt_f64_fwd<LOGN, RS><<<g, threads, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_ffwd, r->d_ffl, src, src_div);
-  } else if (!epi || epi->mode == 0) {
-    const int g = grid_of(F64Occ<LOGN, RS, 1>::get((const void*)ntt_f64_inv<LOGN, RS>, sm, &err));
-    if (err != cudaSuccess) return check_cuda(err, "ntt_f64_inv attributes");
-    ntt_f64_inv<LOGN, RS><<<g, threads, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict,
-                                                  epi && epi->ftwist ? epi->ftwist : r->d_ftwist);
-  } else if (epi->out.n == 1 && epi->mode == 1) {
-    const int g = grid_of(F64Occ<LOGN, RS, 2>::get((const void*)ntt_f64_inv_epi<LOGN, RS, false, false>, sm, &err));
-    if (err != cudaSuccess) return check_cuda(err, "ntt_f64_inv_epi attributes");
-    ntt_f64_inv_epi<LOGN, RS, false, false><<<g, threads, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict,
-                                                                    r->d_ftwist, *epi);
-  } else if (epi->out.n == 1) {
-    const int g = grid_of(F64Occ<LOGN, RS, 3>::get((const void*)ntt_f64_inv_epi<LOGN, RS, true, false>, sm, &err));
-    if (err != cudaSuccess) return check_cuda(err, "ntt_f64_inv_epi attributes");
-    ntt_f64_inv_epi<LOGN, RS, true, false><<<g, threads, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict,
-                                                                   r->d_ftwist, *epi);
-  } else if (epi->mode == 1) {
-    const int g = grid_of(F64Occ<LOGN, RS, 4>::get((const void*)ntt_f64_inv_epi<LOGN, RS, false, true>, sm, &err));
-    if (err != cudaSuccess) return check_cuda(err, "ntt_f64_inv_epi attributes");
-    ntt_f64_inv_epi<LOGN, RS, false, true><<<g, threads, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict,
-                                                                   r->d_ftwist, *epi);
-  } else {
-    const int g = grid_of(F64Occ<LOGN, RS, 5>::get((const void*)ntt_f64_inv_epi<LOGN, RS, true, true>, sm, &err));
-    if (err != cudaSuccess) return check_cuda(err, "ntt_f64_inv_epi attributes");
-    ntt_f64_inv_epi<LOGN, RS, true, true><<<g, threads, sm, st>>>(d, n_rows, period, offset, r->d_lc, r->d_fict,
-                                                                  r->d_ftwist, *epi);
+    if (dbl)
+      return f64_go<LOGN, RS, 7>(ntt_f64_fwd<LOGN, RS, true>, sms, n_rows, sm, st, d, n_rows, period, offset, r->d_lc,
+                                 r->d_ffwd, r->d_ffl, src, src_div);
+    return f64_go<LOGN, RS, 0>(ntt_f64_fwd<LOGN, RS, false>, sms, n_rows, sm, st, d, n_rows, period, offset, r->d_lc,
+                               r->d_ffwd, r->d_ffl, src, src_div);
   }
-  FCN_LAUNCH_CHECK(fwd ? "ntt_f64_fwd" : "ntt_f64_inv");
-  return FCN_OK;
+  if (!epi || epi->mode == 0) {
+    const double2* twist = epi && epi->ftwist ? epi->ftwist : r->d_ftwist;
+    if (dbl)
+      return f64_go<LOGN, RS, 8>(ntt_f64_inv<LOGN, RS, true>, sms, n_rows, sm, st, d, n_rows, period, offset, r->d_lc,
+                                 r->d_fict, twist);
+    return f64_go<LOGN, RS, 1>(ntt_f64_inv<LOGN, RS, false>, sms, n_rows, sm, st, d, n_rows, period, offset, r->d_lc,
+                               r->d_fict, twist);
+  }
+  const bool scale = epi->mode != 1, fan = epi->out.n != 1;
+#define FCN_EPI_GO(V, SC, FN, DB)                                                                                  \
+  if (scale == SC && fan == FN && dbl == DB)                                                                        \
+    return f64_go<LOGN, RS, V>(ntt_f64_inv_epi<LOGN, RS, SC, FN, DB>, sms, n_rows, sm, st, d, n_rows, period, offset, \
+                               r->d_lc, r->d_fict, r->d_ftwist, *epi);
+  FCN_EPI_GO(2, false, false, false)
+  FCN_EPI_GO(3, true, false, false)
+  FCN_EPI_GO(4, false, true, false)
+  FCN_EPI_GO(5, true, true, false)
+  FCN_EPI_GO(9, false, false, true)
+  FCN_EPI_GO(10, true, false, true)
+  FCN_EPI_GO(11, false, true, true)
+  FCN_EPI_GO(12, true, true, true)
+#undef FCN_EPI_GO
+  return set_error(FCN_ERR_STATE, "no FP64 inverse-NTT epilogue for mode %d", epi->mode);
 }
 
 template <int RS>
@@ -556,28 +574,24 @@ int launch_ntt_f64(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, i
 
 template <int LOGN, int RS>
 static int f64_sq_launch_t(int sms, const fcn_ring* r, const uint64_t* a, const uint64_t* aux, uint64_t* Tout,
-                           int64_t units, int k, int m, cudaStream_t st) {
-  constexpr int threads = (1 << LOGN) / 32;
+                           int64_t units, int k, int m, cudaStream_t st, bool dbl) {
   const size_t sm = (size_t)((1 << LOGN) + (1 << LOGN) / 32 + 2) * sizeof(uint64_t);
-  cudaError_t err = cudaSuccess;
-  const int occ = F64Occ<LOGN, RS, 6>::get((const void*)ntt_f64_fwd_sq<LOGN, RS>, sm, &err);
-  if (err != cudaSuccess) return check_cuda(err, "ntt_f64_fwd_sq attributes");
-  int64_t g = (int64_t)sms * occ;
-  if (g > units) g = units;
-  ntt_f64_fwd_sq<LOGN, RS><<<(int)g, threads, sm, st>>>(a, aux, Tout, units, k, m, r->d_lc, r->d_ffwd, r->d_ffl);
-  FCN_LAUNCH_CHECK("ntt_f64_fwd_sq");
-  return FCN_OK;
+  if (dbl)
+    return f64_go<LOGN, RS, 13>(ntt_f64_fwd_sq<LOGN, RS, true>, sms, units, sm, st, a, aux, Tout, units, k, m, r->d_lc,
+                                r->d_ffwd, r->d_ffl);
+  return f64_go<LOGN, RS, 6>(ntt_f64_fwd_sq<LOGN, RS, false>, sms, units, sm, st, a, aux, Tout, units, k, m, r->d_lc,
+                             r->d_ffwd, r->d_ffl);
 }
 
 template <int RS>
 int launch_ntt_f64_sq(const fcn_ring* r, const uint64_t* a, const uint64_t* aux, uint64_t* Tout, int64_t units, int k,
-                      int m, cudaStream_t st, int sms) {
+                      int m, cudaStream_t st, int sms, bool dbl) {
   switch (r->logn) {
-    case 10: return f64_sq_launch_t<10, RS>(sms, r, a, aux, Tout, units, k, m, st);
-    case 11: return f64_sq_launch_t<11, RS>(sms, r, a, aux, Tout, units, k, m, st);
-    case 12: return f64_sq_launch_t<12, RS>(sms, r, a, aux, Tout, units, k, m, st);
-    case 13: return f64_sq_launch_t<13, RS>(sms, r, a, aux, Tout, units, k, m, st);
-    case 14: return f64_sq_launch_t<14, RS>(sms, r, a, aux, Tout, units, k, m, st);
+    case 10: return f64_sq_launch_t<10, RS>(sms, r, a, aux, Tout, units, k, m, st, dbl);
+    case 11: return f64_sq_launch_t<11, RS>(sms, r, a, aux, Tout, units, k, m, st, dbl);
+    case 12: return f64_sq_launch_t<12, RS>(sms, r, a, aux, Tout, units, k, m, st, dbl);
+    case 13: return f64_sq_launch_t<13, RS>(sms, r, a, aux, Tout, units, k, m, st, dbl);
+    case 14: return f64_sq_launch_t<14, RS>(sms, r, a, aux, Tout, units, k, m, st, dbl);
     default: return set_error(FCN_ERR_ARG, "FP64 NTT: unsupported log n %d", r->logn);
   }
 }

@@ -5,5 +5,5 @@ namespace fcn {
 template int launch_ntt_f64<1>(const fcn_ring*, uint64_t*, int64_t, int, int, bool, cudaStream_t, const uint64_t*, int,
                                  const NttEpi*, int);
 template int launch_ntt_f64_sq<1>(const fcn_ring*, const uint64_t*, const uint64_t*, uint64_t*, int64_t, int, int,
-                                    cudaStream_t, int);
+                                    cudaStream_t, int, bool);
 }  // namespace fcn

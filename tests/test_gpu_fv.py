@@ -329,14 +329,17 @@ def test_errors(F):
     assert F.add_pt(ct, F.PlainPoly.zero(P.t_lanes[0])) is ct
 
 
-@pytest.mark.parametrize("env", [{"FCN_NTT_INT": "1"}, {"FCN_SQ_FUSE": "0"}, {"FCN_NTT_RS": "0"}],
-                         ids=["integer-kernels", "unfused-square", "ntt-rs0"])
+@pytest.mark.parametrize("env", [{"FCN_NTT_INT": "1"}, {"FCN_SQ_FUSE": "0"}, {"FCN_NTT_RS": "0"},
+                                 {"FCN_DBL_ROWS": "0", "FCN_PRESCALE": "0"}],
+                         ids=["integer-kernels", "unfused-square", "ntt-rs0", "u64-rows"])
 def test_kernel_family_subprocess(env):
     """Kernel families the default dispatch does not pick for these shapes,
     each forced in a fresh process (the switches are read once per process):
     FCN_NTT_INT=1 the integer kernels (used for limbs >= 2^51), FCN_SQ_FUSE=0
     the separate forward NTT + tensor kernels for squares, FCN_NTT_RS=0 the
-    FP64 NTT's every-third-stage reduction schedule (limbs near 2^51).
+    FP64 NTT's every-third-stage reduction schedule (limbs near 2^51),
+    FCN_DBL_ROWS=0 / FCN_PRESCALE=0 the square pipeline with canonical u64
+    workspace rows and the rescale's first factor in the rescale kernel.
     Squares and NTTs on the cfg1/cfg2 shapes must match the oracle."""
     import os
     import subprocess
