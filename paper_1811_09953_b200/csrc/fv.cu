@@ -533,8 +533,10 @@ __global__ void __launch_bounds__(256) lift_kernel(const uint64_t* __restrict__ 
 // y_i -> y_i + q_i together with v -> v + 1), aux residues as in
 // rescale_f64_kernel with a reduction before every 4th product.  The K input
 // loads of the next coefficient are issued before this one computes.
-// Instantiated for exact limb counts (k = KQ, m = KA) only.
-template <int KQ, int KA, int NW>
+// Instantiated for exact limb counts (k = KQ, m = KA) only.  RP: products
+// between reductions of an auxiliary residue (4 for any prime < 2^51, 12
+// when every prime is below 2^50.07: f64_product_period).
+template <int KQ, int KA, int NW, int RP = 4>
 __global__ void __launch_bounds__(256) lift_f64_kernel(const uint64_t* __restrict__ in, uint64_t* __restrict__ ext,
                                                        int64_t npoly, int logn, const __grid_constant__ LiftP<KQ, KA> P,
                                                        const MulCtConst* __restrict__ cc,
@@ -613,7 +615,7 @@ __global__ void __launch_bounds__(256) lift_f64_kernel(const uint64_t* __restric
         double acc = fmulq_m(v, P.fnqp[j], P.fnqpq[j], pj);
 #pragma unroll
         for (int i = 0; i < KQ; ++i) {
-          if ((i & 3) == 3) acc = fredq(acc, pji, pj);
+          if (i % RP == RP - 1) acc = fredq(acc, pji, pj);
           acc += fmulq_m(y[i], P.flc[j][i], P.flcq[j][i], pj);
         }
         ext[(compact ? poly * m + j : poly * K + k + j) * n + coef] = f2u_canon(fredq(acc, pji, pj), pj);
@@ -861,8 +863,11 @@ __global__ void __launch_bounds__(256, (KQ <= 4 ? 3 : 2)) rescale_kernel(const u
 //  3. R mod q_i = sum_j y_j rc_ij + sum h_j + g - v tP, every product
 //     |.| < 0.7 q_i, reduced to |.| <= q_i/2 + 1 before products 3, 7, 11..
 //     so all partial sums stay below 3.6 q_i < 2^53.
-// Instantiated for exact limb counts (k = KQ, K = KE) only.
-template <int KQ, int KE, int NW>
+// Instantiated for exact limb counts (k = KQ, K = KE) only.  RP: products
+// between reductions in step 3 (4 as above for any prime < 2^51; 12 when
+// every prime is below 2^50.07: partial sums < 0.5 + 12 x 0.6 q < 7.7 q < 2^53,
+// f64_product_period).
+template <int KQ, int KE, int NW, int RP = 4>
 #ifndef FCN_RS_MINB
 #define FCN_RS_MINB(KQ) ((KQ) <= 4 ? 3 : 2)
 #endif
@@ -977,7 +982,7 @@ __global__ void __launch_bounds__(256, FCN_RS_MINB(KQ))
         if (NSH > 1) acc = fredq(acc, qii, qi);
 #pragma unroll
         for (int j = 0; j < KE; ++j) {
-          if ((j & 3) == 3) acc = fredq(acc, qii, qi);
+          if (j % RP == RP - 1) acc = fredq(acc, qii, qi);
           acc += fmulq_m(y[j], P.frc[i][j], P.frcq[i][j], qi);
         }
         out[i] = f2u_canon(fredq(acc, qii, qi), qi);
@@ -1749,6 +1754,20 @@ struct ActArgs {
   bool dbl_in = false;     // ... and left the rows as signed doubles
 };
 
+// Products accumulated between reductions in the FP64 lift / rescale: a
+// product a w mod q with |a| <= 0.75 b, |w| <= q/2 (b, q < 2^51) is
+// |.| <= (1/2 + 0.75 b 2^-53) q, a reduced sum |.| <= q/2, and a sum starts
+// at <= q; 12 products are allowed when 1/2 + 12 p and 1 + 11 p stay below
+// 2^53 / q for the largest prime (limbs just above 2^50), else 4.
+static int f64_product_period(const fcn_ctx* x) {
+  uint64_t mx = 0;
+  for (uint64_t v : x->primes) mx = v > mx ? v : mx;
+  for (uint64_t v : x->aux) mx = v > mx ? v : mx;
+  const double p = 0.5 + 0.75 * (double)mx * 0x1p-53 + 0x1p-20;
+  const double lim = 0x1p53 / ((double)mx + 1.0) * (1.0 - 1e-9);
+  return (0.5 + 12 * p < lim && 1.0 + 11 * p < lim) ? 12 : 4;
+}
+
 template <int KQ, int KE>
 static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t* in, uint64_t* out, int64_t cnt,
                             uint64_t* R01, uint64_t* DG, cudaStream_t st, ActArgs* act, bool* compact) {
@@ -1759,7 +1778,10 @@ static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_
     const LiftP<KQ, KE - KQ> P = make_lift_params<KQ, KE - KQ>(x, mc);
     const int64_t total = cnt << x->logn;  // cnt = polys
     if (compact) *compact = *compact && f64;  // only the FP64 lift writes the compact layout
-    if (f64)
+    if (f64 && f64_product_period(x) == 12)
+      lift_f64_kernel<KQ, KE - KQ, KQ + 2, 12><<<grid_for(total, 256), 256, 0, st>>>(
+          in, out, cnt, x->logn, P, dmc, x->d_fallbacks, compact && *compact ? 1 : 0);
+    else if (f64)
       lift_f64_kernel<KQ, KE - KQ, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(
           in, out, cnt, x->logn, P, dmc, x->d_fallbacks, compact && *compact ? 1 : 0);
     else
@@ -1793,9 +1815,14 @@ static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_
       static std::once_flag once;
       std::call_once(once, [&] {
         cudaFuncSetAttribute(rescale_f64_kernel<KQ, KE, KQ + 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(rescale_f64_kernel<KQ, KE, KQ + 2, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       });
-      rescale_f64_kernel<KQ, KE, KQ + 2><<<grid_for(total, 256), 256, smem, st>>>(in, R01, DG, cnt, x->logn, P, dmc,
-                                                                                  x->d_fallbacks, act ? act->lin : nullptr);
+      if (f64_product_period(x) == 12)
+        rescale_f64_kernel<KQ, KE, KQ + 2, 12><<<grid_for(total, 256), 256, smem, st>>>(
+            in, R01, DG, cnt, x->logn, P, dmc, x->d_fallbacks, act ? act->lin : nullptr);
+      else
+        rescale_f64_kernel<KQ, KE, KQ + 2><<<grid_for(total, 256), 256, smem, st>>>(
+            in, R01, DG, cnt, x->logn, P, dmc, x->d_fallbacks, act ? act->lin : nullptr);
     }
     else
       rescale_kernel<KQ, KE, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, R01, DG, cnt, x->logn, P, dmc,
