@@ -372,3 +372,40 @@ print("ok")
     env = dict(os.environ, PYTHONPATH=repo, **env)
     res = subprocess.run([sys.executable, "-c", code], cwd=repo, env=env, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0 and res.stdout.strip().endswith("ok"), res.stdout[-2000:] + res.stderr[-2000:]
+
+
+def test_empty_and_single_unit_batches(F):
+    """Edge cases of the C ABI on the cfg2 ring: zero-count calls return OK and
+    leave the output untouched; squares of batches of 1, 2 and 5 ciphertexts
+    (fewer fused (ciphertext, limb) units than resident CTAs, an odd count)
+    match the oracle."""
+    import torch
+
+    from oracle import rns as orn
+    from paper_1811_09953_b200 import _lib, configs
+    from paper_1811_09953_b200 import device as dev
+
+    W = configs.WORKLOADS["cfg2"]
+    P = F.EncryptionParams(W.n, W.primes, (W.t,), W.beta)
+    OP = ob.Params(W.n, W.primes, (W.t,), W.beta)
+    sk, pk, ek = F.keygen(P, 2)
+    L, h, st = _lib.lib(), P.native(), dev.stream_ptr()
+    k, n = len(W.primes), W.n
+    sentinel = dev.zeros((1, 2, k, n)) + 7
+    ws = F.mul_ct_workspace(P, 1)
+    kh = ek.native(P)
+    assert L.fcn_ntt_forward(h.ring_ptr, sentinel.data_ptr(), 0, k, 0, st) == 0
+    assert L.fcn_ntt_inverse(h.ring_ptr, sentinel.data_ptr(), 0, k, 0, st) == 0
+    assert L.fcn_mul_ct_ex(h.ptr, kh.ptr, 0, sentinel.data_ptr(), None, sentinel.data_ptr(), 0, 0, 1, 0,
+                           ws.data_ptr(), ws.numel() * 8, st) == 0
+    assert L.fcn_key_mac(h.ptr, kh.ptr, sentinel.data_ptr(), sentinel.data_ptr(), 0, st) == 0
+    torch.cuda.synchronize()
+    assert bool((sentinel == 7).all())
+    K = ob.Keys(sk.s.host(), pk.p0.host(), pk.p1.host(), [x.host() for x in ek.a], [x.host() for x in ek.g])
+    rng = np.random.default_rng(3)
+    for B in (1, 2, 5):
+        x = np.stack([np.stack([orn.random_uniform(W.primes, n, rng) for _ in range(2)]) for _ in range(B)])
+        out = dev.to_host(F.mul_ct_batch(P, ek, 0, dev.to_device(x)))
+        for b in {0, B - 1}:
+            want = ob.mul_ct(OP, ob.Ct(x[b, 0], x[b, 1]), ob.Ct(x[b, 0], x[b, 1]), K)
+            assert np.array_equal(out[b], np.stack([want.c0, want.c1])), (B, b)
