@@ -164,9 +164,6 @@ __device__ __forceinline__ uint64_t submod(uint64_t a, uint64_t b, uint64_t q) {
 // a0*s0 and the low halves of the cross products, so it undershoots
 // floor(a ws / 2^64) by at most 2 (remainder < 2q + 2q).  9 IMAD-pipe ops.
 __device__ __forceinline__ uint64_t mulw(uint64_t a, uint64_t w, uint64_t ws, uint64_t nq) {
-#ifdef FCN_EXP_NO_MUL
-  return (a ^ w) + ws;
-#endif
   uint64_t r;
   asm("{\n\t"
       ".reg .u32 a0, a1, w0, w1, s0, s1, n0, n1, hl, hh, rl, rh;\n\t"

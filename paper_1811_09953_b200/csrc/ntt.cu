@@ -238,13 +238,8 @@ __global__ void ntt_v1_inv_last(uint64_t* __restrict__ data, int64_t n_rows, int
 // ================================================================= v2
 
 __device__ __forceinline__ Twiddle ld_tw(const Twiddle* p) {
-#ifdef FCN_EXP_NO_TW
-  const uint64_t a = (uint64_t)p;
-  return Twiddle{a >> 9, (a << 7) ^ a};
-#else
   const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
   return Twiddle{v.x, v.y};
-#endif
 }
 
 // Cooley-Tukey butterfly without reduction: X' = X + wY, Y' = X - wY + 4q.
