@@ -16,6 +16,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <mutex>
 
 #include "bigint.hpp"
@@ -73,6 +74,10 @@ struct fcn_ctx {
   // FP64 inverse twist of the tensor INTT with the rescale's first factor
   // folded in: {w, w/b_l}, w = n^-1 psi_l^-j (B/b_l)^-1 mod b_l signed
   double2* d_ftwist_binv = nullptr;
+  // final-INTT twists of the q-limbs scaled by an activation's c2 (the
+  // epilogue's c2 multiply folded into the twist), built on first use
+  std::mutex twist_mu;
+  std::map<int64_t, double2*> ftwist_c2;
 };
 
 struct fcn_keys {
@@ -1439,6 +1444,7 @@ extern "C" int fcn_ctx_destroy(fcn_ctx* x) {
     cudaFree(x->d_mc);
     cudaFree(x->d_fallbacks);
     cudaFree(x->d_ftwist_binv);
+    for (auto& kv : x->ftwist_c2) cudaFree(kv.second);
   }
   fcn_ring_destroy(x->ext);
   delete x;
@@ -1872,6 +1878,50 @@ static bool dbl_rows(const fcn_ctx* x) {
   return on && x->fp && x->ell + 1 <= 12;
 }
 
+// The q-limb inverse twist n^-1 psi_l^-j times (c2 mod q_l) as {w, w/q_l}
+// (layout of fcn_ring::d_ftwist's first k limbs), cached per c2.  Returns
+// nullptr when it would have to be built while the stream is being captured
+// into a CUDA graph (no allocation there): the caller keeps the scaling
+// epilogue.  FCN_TWIST_C2=0 disables it (A/B tests).
+static const double2* c2_twist(fcn_ctx* x, int64_t c2, cudaStream_t st) {
+  static const bool on = [] {
+    const char* ev = getenv("FCN_TWIST_C2");
+    return !(ev && ev[0] == '0');
+  }();
+  if (!on) return nullptr;
+  std::lock_guard<std::mutex> lk(x->twist_mu);
+  auto it = x->ftwist_c2.find(c2);
+  if (it != x->ftwist_c2.end()) return it->second;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+  const int k = x->k, n = x->n;
+  std::vector<double2> tw((size_t)k * n);
+  for (int l = 0; l < k; ++l) {
+    const uint64_t q = x->primes[l];
+    const int64_t m = c2 % (int64_t)q;
+    const uint64_t cm = (uint64_t)(m < 0 ? m + (int64_t)q : m);
+    const uint64_t iroot = h_powmod(x->ext->roots[l], q - 2, q);
+    uint64_t w = h_mulmod(h_powmod((uint64_t)n % q, q - 2, q), cm, q);
+    for (int j = 0; j < n; ++j) {
+      const double ws = w > q / 2 ? -(double)(q - w) : (double)w;
+      tw[(size_t)l * n + j] = make_double2(ws, ws / (double)q);
+      w = h_mulmod(w, iroot, q);
+    }
+  }
+  double2* d = nullptr;
+  if (cudaMalloc(&d, sizeof(double2) * tw.size()) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (cudaMemcpy(d, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    cudaGetLastError();
+    return nullptr;
+  }
+  x->ftwist_c2[c2] = d;
+  return d;
+}
+
 // FCN_PRESCALE=0 keeps (B/b_j)^-1 in the rescale kernel instead of the INTT twist (A/B tests).
 static bool prescale_enabled() {
   static const bool on = [] {
@@ -2046,6 +2096,14 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
     rc = lift_or_rescale(false, x, lane, T, nullptr, C, R01, direct ? DGR : DGN, st, &aa);
     if (rc) return rc;
     epi.mode = !act ? 1 : (aa.applied ? 3 : 2);
+    epi.ftwist = nullptr;
+    if (epi.mode == 3 && x->fp && ntt_family(x->ext, k, 0) == 2) {
+      // out = R + c2 INTT(ACC) == R + INTT'(ACC) with c2 folded into the twist
+      if (const double2* tw = c2_twist(const_cast<fcn_ctx*>(x), act_c2, st)) {
+        epi.mode = 1;
+        epi.ftwist = tw;
+      }
+    }
     // (v) digits to NTT (broadcast rows when digits are limb-independent), key MAC
     NttEpi dg_epi;
     dg_epi.dbl = dbl;

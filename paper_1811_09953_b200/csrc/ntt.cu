@@ -667,8 +667,8 @@ int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int o
   if (g_init_err != cudaSuccess) return check_cuda(g_init_err, "ntt init");
   const int logn = r->logn;
   const int family = ntt_family(r, period, offset);
-  if (epi && epi->ftwist && (family != 2 || epi->mode != 0))
-    return set_error(FCN_ERR_STATE, "a replacement twist needs the FP64 inverse without epilogue");
+  if (epi && epi->ftwist && (family != 2 || epi->mode == 2 || fwd))
+    return set_error(FCN_ERR_STATE, "a replacement twist needs an FP64 inverse (epilogue mode 0, 1 or 3)");
   if (epi && epi->dbl && (family != 2 || epi->mode == 2))
     return set_error(FCN_ERR_STATE, "double-format rows need the FP64 kernels");
   if (family == 0) {

@@ -478,8 +478,8 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const double2 w = ld_ftw(twist + tid + j * T);
-      double y = fredq(fmulq(x[j], w.x, w.y, q), qi, q);  // |y| <= q/2 + 1
-      if (SCALE) y = fmulq(y, c2, c2q, q);              // |y| < 0.7 q
+      double y = fmulq(x[j], w.x, w.y, q);  // |y| < 1.5 q (|x| < 7.5 q)
+      if (SCALE) y = fmulq(y, c2, c2q, q);  // |y| < 0.7 q
       const uint64_t v = f2u_canon(fredq(y + u2f(sm[pst + j * (T + T / 32)]), qi, q), q);
       po[tid + j * T] = v;
       if (FAN) {  // fan-out to the peers' buffers
@@ -543,10 +543,11 @@ static int f64_launch_t(bool fwd, int sms, uint64_t* d, int64_t n_rows, int peri
                                r->d_fict, twist);
   }
   const bool scale = epi->mode != 1, fan = epi->out.n != 1;
+  const double2* etwist = epi->ftwist ? epi->ftwist : r->d_ftwist;  // e.g. the c2-scaled twist (mode 1)
 #define FCN_EPI_GO(V, SC, FN, DB)                                                                                  \
   if (scale == SC && fan == FN && dbl == DB)                                                                        \
     return f64_go<LOGN, RS, V>(ntt_f64_inv_epi<LOGN, RS, SC, FN, DB>, sms, n_rows, sm, st, d, n_rows, period, offset, \
-                               r->d_lc, r->d_fict, r->d_ftwist, *epi);
+                               r->d_lc, r->d_fict, etwist, *epi);
   FCN_EPI_GO(2, false, false, false)
   FCN_EPI_GO(3, true, false, false)
   FCN_EPI_GO(4, false, true, false)

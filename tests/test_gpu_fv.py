@@ -330,8 +330,8 @@ def test_errors(F):
 
 
 @pytest.mark.parametrize("env", [{"FCN_NTT_INT": "1"}, {"FCN_SQ_FUSE": "0"}, {"FCN_NTT_RS": "0"},
-                                 {"FCN_DBL_ROWS": "0", "FCN_PRESCALE": "0"}],
-                         ids=["integer-kernels", "unfused-square", "ntt-rs0", "u64-rows"])
+                                 {"FCN_DBL_ROWS": "0", "FCN_PRESCALE": "0"}, {"FCN_TWIST_C2": "0"}],
+                         ids=["integer-kernels", "unfused-square", "ntt-rs0", "u64-rows", "scaling-epilogue"])
 def test_kernel_family_subprocess(env):
     """Kernel families the default dispatch does not pick for these shapes,
     each forced in a fresh process (the switches are read once per process):
@@ -339,7 +339,10 @@ def test_kernel_family_subprocess(env):
     the separate forward NTT + tensor kernels for squares, FCN_NTT_RS=0 the
     FP64 NTT's every-third-stage reduction schedule (limbs near 2^51),
     FCN_DBL_ROWS=0 / FCN_PRESCALE=0 the square pipeline with canonical u64
-    workspace rows and the rescale's first factor in the rescale kernel.
+    workspace rows and the rescale's first factor in the rescale kernel,
+    FCN_TWIST_C2=0 the activation's c2 in the final INTT's epilogue instead
+    of its twist.  Squares (plain and with the fused a2 x^2 + a1 x
+    activation) and NTTs on the cfg1/cfg2 shapes must match the oracle.
     Squares and NTTs on the cfg1/cfg2 shapes must match the oracle."""
     import os
     import subprocess
@@ -359,10 +362,15 @@ for name in ("cfg1", "cfg2"):
     rng = np.random.default_rng(1)
     x = np.stack([np.stack([orn.random_uniform(W.primes, W.n, rng) for _ in range(2)]) for _ in range(2)])
     out = dev.to_host(fv.mul_ct_batch(P, ek, 0, dev.to_device(x)))
+    act = dev.to_host(fv.mul_ct_batch(P, ek, 0, dev.to_device(x), act=(-3, 5)))
     for b in range(2):
         c = ob.Ct(x[b, 0], x[b, 1])
         w = ob.mul_ct(OP, c, c, K)
         assert np.array_equal(out[b], np.stack([w.c0, w.c1])), (name, b)
+        for p_i, (pa, xa) in enumerate(((w.c0, x[b, 0]), (w.c1, x[b, 1]))):
+            for l, q in enumerate(W.primes):
+                want = (pa[l].astype(object) * (-3 % q) + xa[l].astype(object) * 5) % q
+                assert np.array_equal(act[b, p_i, l].astype(object), want), (name, b, p_i, l)
     ctx = ring.RingContext.create(W.n, W.primes)
     r = x[0, 0]
     assert np.array_equal(ring.ntt_forward(ring.RingPoly(ctx, r)).host(), orn.ntt(r, W.primes))
