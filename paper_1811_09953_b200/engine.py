@@ -655,7 +655,10 @@ def eval_encrypted(net, tensor: CipherTensor, ek: EvalKeys, cfg: FixedPointConfi
 
     Same contract as reference engine.eval_encrypted (engine.py:651-774);
     `workers` is accepted for API compatibility (the GPU parallelises
-    every layer's outputs).  `encoding` selects the plaintext encoding of
+    every layer's outputs).  `net` may also be the CompiledNet that
+    `compile_network(net, cfg)` returned, which skips the per-call content
+    hash of the weights that keys the plan cache (~0.7 ms for cfg2; a server
+    evaluating one network repeatedly compiles it once).  `encoding` selects the plaintext encoding of
     the integer constants ("integer" = the reference's base-2 encoder;
     "batched" = constant polynomials for SIMD-packed slots).  `timing=False`
     records no per-layer CUDA events (layer wall_ms then reads 0), e.g. for
@@ -671,7 +674,10 @@ def eval_encrypted(net, tensor: CipherTensor, ek: EvalKeys, cfg: FixedPointConfi
     t = int(params.t_lanes[lane])
     if int(cfg.t_lanes[lane]) != t:
         raise EngineError("fixed-point lane configuration disagrees with ciphertexts")
-    acts = sum(type(l).__name__ == "PolyActivation" for l in net.layers)
+    if isinstance(net, CompiledNet):  # a plan from compile_network: no per-call content hash
+        acts = sum(isinstance(p, ActPlan) for p in net.plans)
+    else:
+        acts = sum(type(l).__name__ == "PolyActivation" for l in net.layers)
     if acts > params.mul_depth_budget:
         raise EngineError(f"{acts} activations exceed the parameter depth budget {params.mul_depth_budget}")
     compiled = _compiled(net, cfg)

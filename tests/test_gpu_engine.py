@@ -372,6 +372,9 @@ def test_eval_graph_replay_matches_eager(E):
     want1 = E.eval_encrypted(net, tensor, ek, cfg, encoding="batched")[0].buf.clone()
     want2 = E.eval_encrypted(net, other, ek, cfg, encoding="batched")[0].buf.clone()
     assert torch.equal(g.replay().buf, want1)
+    # a precompiled plan evaluates to the same bytes (no per-call weight hash)
+    comp = E.compile_network(net, cfg)
+    assert torch.equal(E.eval_encrypted(comp, tensor, ek, cfg, encoding="batched")[0].buf, want1)
     tensor.buf.copy_(other.buf)
     assert torch.equal(g.replay().buf, want2)
     assert torch.equal(g.replay().buf, want2)
