@@ -323,6 +323,26 @@ def _ref_init(workload):
     _ref_worker.state = (OP, K, cts)
 
 
+def _host_cpu() -> dict:
+    """The host the CPU numbers ran on (count, physical cores, model)."""
+    info = {"os_cpu_count": os.cpu_count()}
+    try:
+        import psutil
+
+        info["physical_cores"] = psutil.cpu_count(logical=False)
+    except Exception:  # noqa: BLE001 - optional
+        pass
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    info["model"] = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return info
+
+
 def run_reference(args, ws, rank):
     """CPU oracle port on all host cores (multiprocessing over independent outputs)."""
     if rank != 0:
@@ -376,6 +396,7 @@ def run_reference(args, ws, rank):
             "unit": "images/s",
             "cores": cores,
             "kind": "port",
+            "host": _host_cpu(),
             "sample": f"per step: {cores} mul_ct + {16 * cores} (mul_pt+add_ct) across a {cores}-process pool; "
             f"pass time extrapolated by the plan's HOP counts ({tot.ct_ct_mul} ct_ct_mul, {tot.pt_ct_mul} pt_ct_mul)",
         },
@@ -583,7 +604,8 @@ def run_gpu(args, ws, rank, local):
         slots = engine.decrypt_tensor_slots(sk, out)
         check = bool(np.array_equal(slots, od.plain_model_batched(comp, x << cfg.precision_bits, W.t)))
         v, t_pass, sample, per = _cpu_sample(args.workload, args.cpu_seconds, hops, W.slots)
-        cpu = {"value": v, "unit": "images/s", "cores": 1, "kind": "port", "sample": sample, "seconds_per_pass": t_pass, **per}
+        cpu = {"value": v, "unit": "images/s", "cores": 1, "kind": "port", "sample": sample, "seconds_per_pass": t_pass,
+               "host": _host_cpu(), **per}
     line = {
         "metric": "encrypted images/sec",
         "value": value,
