@@ -93,6 +93,12 @@ def main():
     res["square_relin_gbs"] = byts / t / 1e9
     res["square_relin_frac_hbm"] = byts / t / 1e9 / peak
     res["square_relin_cts_per_s"] = B / t
+    K = len(W.primes) + len(h.aux)
+    rows = 2 * K + 3 * K + (P.ell + 1) * k + 2 * k  # NTT rows per square (fused fwd, tensor INTT, digits, final INTT)
+    res["square_relin_ntt_rows_per_ct"] = rows
+    res["square_relin_note"] = (
+        f"FP64-bound, not HBM-bound: each square runs {rows} NTT rows of n={n} over the {K}-limb extended base "
+        "plus the exact rescale; square_relin_frac_hbm only relates the in/out/key bytes (SURVEY 8(d)) to the time")
 
     # key-switching inner product alone (digits -> accumulators), 256 cts per launch
     D = P.ell + 1
