@@ -533,6 +533,22 @@ __global__ void __launch_bounds__(256) lift_kernel(const uint64_t* __restrict__ 
   }
 }
 
+// Constant-multiplier product of the FP64 lift / rescale.  FCN_LR_FRND=1:
+// the quotient is rounded by FRND (XU pipe) instead of the magic-constant
+// DFMA + DADD: one FP64-pipe operation fewer per product.  The quotient error
+// is then 1/2 + |a w/q| 2^-52 (two roundings) instead of 1/2 + |a w/q| 2^-53,
+// which is the bound f64_product_period and the 0.7 q product bounds assume.
+#ifndef FCN_LR_FRND
+#define FCN_LR_FRND 1
+#endif
+__device__ __forceinline__ double fmulq_lr(double a, double w, double wq, double q) {
+#if FCN_LR_FRND
+  return fmulq(a, w, wq, q);
+#else
+  return fmulq_m(a, w, wq, q);
+#endif
+}
+
 // FP64-pipe variant of lift_kernel (every ext prime < 2^51): y_i signed
 // (|y_i| < 0.75 q_i), v = floor(sum y_i/q_i + 1/2) (centred: invariant under
 // y_i -> y_i + q_i together with v -> v + 1), aux residues as in
@@ -578,7 +594,7 @@ __global__ void __launch_bounds__(256) lift_f64_kernel(const uint64_t* __restric
       y[i] = 0.0;
       if (i < k) {
         if (!compact) ext[(poly * K + i) * n + coef] = cur[i];
-        y[i] = fmulq_m(u2f(cur[i]), P.fqinv[i], P.fqinvq[i], P.fq[i]);
+        y[i] = fmulq_lr(u2f(cur[i]), P.fqinv[i], P.fqinvq[i], P.fq[i]);
         f = fma(y[i], P.rq[i], f);
       }
     }
@@ -617,11 +633,11 @@ __global__ void __launch_bounds__(256) lift_f64_kernel(const uint64_t* __restric
     for (int j = 0; j < KA; ++j) {
       if (j < m) {
         const double pj = P.fp[j], pji = P.fpi[j];
-        double acc = fmulq_m(v, P.fnqp[j], P.fnqpq[j], pj);
+        double acc = fmulq_lr(v, P.fnqp[j], P.fnqpq[j], pj);
 #pragma unroll
         for (int i = 0; i < KQ; ++i) {
           if (i % RP == RP - 1) acc = fredq(acc, pji, pj);
-          acc += fmulq_m(y[i], P.flc[j][i], P.flcq[j][i], pj);
+          acc += fmulq_lr(y[i], P.flc[j][i], P.flcq[j][i], pj);
         }
         ext[(compact ? poly * m + j : poly * K + k + j) * n + coef] = f2u_canon(fredq(acc, pji, pj), pj);
       }
@@ -981,14 +997,14 @@ __global__ void __launch_bounds__(256, FCN_RS_MINB(KQ))
       out[i] = 0;
       if (i < k) {
         const double qi = P.fq[i], qii = P.fqi[i];
-        double acc = gd + fmulq_m(v, P.fntp[i], P.fntpq[i], qi);
+        double acc = gd + fmulq_lr(v, P.fntp[i], P.fntpq[i], qi);
 #pragma unroll
         for (int g2 = 0; g2 < NSH; ++g2) acc += fredq(sh[g2], qii, qi);
         if (NSH > 1) acc = fredq(acc, qii, qi);
 #pragma unroll
         for (int j = 0; j < KE; ++j) {
           if (j % RP == RP - 1) acc = fredq(acc, qii, qi);
-          acc += fmulq_m(y[j], P.frc[i][j], P.frcq[i][j], qi);
+          acc += fmulq_lr(y[j], P.frc[i][j], P.frcq[i][j], qi);
         }
         out[i] = f2u_canon(fredq(acc, qii, qi), qi);
       }
