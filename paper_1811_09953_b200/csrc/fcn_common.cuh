@@ -243,11 +243,23 @@ __device__ __forceinline__ double fprod(double a, double b, double q, double qi)
   const double qt = fma(h, qi, M) - M;
   return fma(-qt, q, h) + l;
 }
-// x mod q centred: |r| <= q/2 + 2^-40 q for |x| < 2^53 (magic-constant rint,
-// valid since |x / q| < 2^51).
+// x mod q centred: |r| <= q/2 + 2^-40 q for |x| < 2^53 and |x / q| < 2^10
+// (every use: sums of a few reduced products or butterfly outputs).
+// The quotient is rounded with the 1.5 * 2^52 magic constant (DFMA + DADD +
+// DFMA); FCN_FRED_FRND=1 uses FRND instead (XU pipe, DMUL + FRND + DFMA), one
+// FP64 operation fewer but measured slower: the NTT butterflies already keep
+// the XU busy with their own FRND (kbench 0.370 -> 0.378 ms forward).  Either
+// quotient is within 1/2 + |x/q| 2^-52 of x/q.
+#ifndef FCN_FRED_FRND
+#define FCN_FRED_FRND 0
+#endif
 __device__ __forceinline__ double fredq(double x, double qi, double q) {
+#if FCN_FRED_FRND
+  const double qt = rint(x * qi);
+#else
   const double M = 6755399441055744.0;  // 1.5 * 2^52
   const double qt = fma(x, qi, M) - M;
+#endif
   return fma(-qt, q, x);
 }
 // Reduction schedules of the FP64 NTT (ntt_f64.cuh): reduce every value
