@@ -232,9 +232,11 @@ def test_sharded_evaluator_single_rank_nccl(E):
     try:
         got, gc = fdist.eval_encrypted_sharded(net, tensor, ek, cfg, encoding="batched")
         got_p, gc_p = fdist.eval_encrypted_sharded(net, tensor, ek, cfg, encoding="batched", transport="p2p")
+        comp = E.compile_network(net, cfg)  # the bench's form: a precompiled plan
+        got_c, gc_c = fdist.eval_encrypted_sharded(comp, tensor, ek, cfg, encoding="batched", transport="p2p")
     finally:
         dist.destroy_process_group()
-    for g, c in ((got, gc), (got_p, gc_p)):
+    for g, c in ((got, gc), (got_p, gc_p), (got_c, gc_c)):
         assert np.array_equal(g.host_bodies(), want.host_bodies())
         assert list(g.depths) == list(want.depths) and list(g.scales) == list(want.scales)
         assert c.same_ops(wc)
