@@ -334,7 +334,11 @@ __device__ __forceinline__ uint64_t mac32(uint64_t acc, uint64_t x, uint32_t m) 
 // four residues of NR rows of the same limb (rows r, r + k: c0 and c1), so
 // the term metadata (column, coefficient, source address: uniform-datapath
 // work) is amortised over 4 NR residues.
-template <bool SMALL, int NR>
+// SGN (with SMALL): one signed accumulator per residue instead of a
+// positive and a negative one (acc -/+= x |c| in two's complement, |acc| <
+// 2^60 by the host's fold), reduced as reduce_small(acc + OFF) with OFF =
+// q ceil(2^60 / q): half the accumulator registers.
+template <bool SMALL, int NR, bool SGN = false>
 __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restrict__ in0, int64_t n_in0,
                                                        const uint64_t* __restrict__ in1,
                                                        const int32_t* __restrict__ rowptr,
@@ -352,11 +356,14 @@ __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restric
   const uint32_t m32 = c.m32;
   const int64_t ct_words = (int64_t)2 * k * n;
   const int64_t rstep = (int64_t)k * n;
+  const uint64_t off60 = SGN ? q * ((1ull << 60) / q + 1) : 0;
   // outputs o = blockIdx.y + i * gridDim.y: per-CTA setup amortised over several outputs
   for (int o = blockIdx.x; o < n_out; o += gridDim.x) {
-    uint64_t pos[V], neg[V];
+    uint64_t pos[V], neg[SGN ? 1 : V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) pos[v] = neg[v] = 0;
+    for (int v = 0; v < V; ++v) pos[v] = 0;
+#pragma unroll
+    for (int v = 0; v < (SGN ? 1 : V); ++v) neg[v] = 0;
     const int e0 = rowptr[o], e1 = rowptr[o + 1];
     int cnt = 0;
     for (int e = e0; e < e1; ++e) {
@@ -371,9 +378,16 @@ __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restric
         vb[h] = *reinterpret_cast<const ulonglong2*>(src + h * rstep + 2);
       }
       // |c| < 2^32 on this path (fold >= 2)
-      uint64_t* acc = cf >= 0 ? pos : neg;
       const uint32_t m = (uint32_t)(cf >= 0 ? cf : -cf);
-      if (cf >= 0) {
+      if (SGN && cf < 0) {
+#pragma unroll
+        for (int h = 0; h < NR; ++h) {
+          pos[4 * h + 0] -= mac32(0, va[h].x, m);
+          pos[4 * h + 1] -= mac32(0, va[h].y, m);
+          pos[4 * h + 2] -= mac32(0, vb[h].x, m);
+          pos[4 * h + 3] -= mac32(0, vb[h].y, m);
+        }
+      } else if (SGN || cf >= 0) {
 #pragma unroll
         for (int h = 0; h < NR; ++h) {
           pos[4 * h + 0] = mac32(pos[4 * h + 0], va[h].x, m);
@@ -381,7 +395,7 @@ __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restric
           pos[4 * h + 2] = mac32(pos[4 * h + 2], vb[h].x, m);
           pos[4 * h + 3] = mac32(pos[4 * h + 3], vb[h].y, m);
         }
-      } else {
+      } else if (!SGN) {
 #pragma unroll
         for (int h = 0; h < NR; ++h) {
           neg[4 * h + 0] = mac32(neg[4 * h + 0], va[h].x, m);
@@ -390,17 +404,18 @@ __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restric
           neg[4 * h + 3] = mac32(neg[4 * h + 3], vb[h].y, m);
         }
       }
-      (void)acc;
       if (++cnt == fold) {
         cnt = 0;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          if (SMALL) {
+          if (SGN) {
+            pos[v] = reduce_small(pos[v] + off60, m32, q);
+          } else if (SMALL) {
             pos[v] = reduce_small(pos[v], m32, q);
-            neg[v] = reduce_small(neg[v], m32, q);
+            neg[SGN ? 0 : v] = reduce_small(neg[SGN ? 0 : v], m32, q);
           } else {
             pos[v] = mulw(pos[v], 1, one_s, nq);
-            neg[v] = mulw(neg[v], 1, one_s, nq);
+            neg[SGN ? 0 : v] = mulw(neg[SGN ? 0 : v], 1, one_s, nq);
           }
         }
       }
@@ -408,9 +423,13 @@ __global__ void __launch_bounds__(256) mac_fast_kernel(const uint64_t* __restric
     uint64_t res[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
+      if (SGN) {
+        res[v] = reduce_small(pos[v] + off60, m32, q);
+        continue;
+      }
       // SMALL: sums kept below 2^62 (fold), reduced by the high-word quotient
       const uint64_t a = SMALL ? reduce_small(pos[v], m32, q) : csub(csub(mulw(pos[v], 1, one_s, nq), 2 * q), q);
-      const uint64_t b = SMALL ? reduce_small(neg[v], m32, q) : csub(csub(mulw(neg[v], 1, one_s, nq), 2 * q), q);
+      const uint64_t b = SMALL ? reduce_small(neg[SGN ? 0 : v], m32, q) : csub(csub(mulw(neg[SGN ? 0 : v], 1, one_s, nq), 2 * q), q);
       res[v] = submod(a, b, q);
     }
 #pragma unroll
@@ -1588,6 +1607,8 @@ extern "C" int fcn_linear_mac_ex(const fcn_ctx* x, const uint64_t* d_in0, int64_
                               max_abs_coef, stream);
 }
 
+static bool mac_sgn_enabled();
+
 extern "C" int fcn_linear_mac_multi(const fcn_ctx* x, const uint64_t* d_in0, int64_t n_in0, const uint64_t* d_in1,
                                     int64_t n_in1, const int32_t* d_rowptr, const int32_t* d_col, const int32_t* d_rot,
                                     const int64_t* d_coef, uint64_t* const* d_outs, int n_dst, int64_t n_out, int no_rot,
@@ -1625,6 +1646,13 @@ extern "C" int fcn_linear_mac_multi(const fcn_ctx* x, const uint64_t* d_in0, int
     fold_small = f > 1024 ? 1024 : (int)f;
     small = fold_small >= 2;
   }
+  // signed single-accumulator variant: |acc| < 2^60
+  int fold_sgn = 0;
+  if (small) {
+    const unsigned __int128 f = (((unsigned __int128)1 << 60) - qmax) / ((unsigned __int128)qmax * max_abs_coef);
+    fold_sgn = f > 1024 ? 1024 : (int)f;
+  }
+  const bool sgn = small && fold_sgn >= 4 && mac_sgn_enabled();
   if (fold >= 2 && x->n >= 4) {
     // blockIdx.x (fastest) walks outputs, so the CTAs resident at any time
     // (~148 x 8) share one (row, coefficient tile): that tile's slice of
@@ -1640,7 +1668,10 @@ extern "C" int fcn_linear_mac_multi(const fcn_ctx* x, const uint64_t* d_in0, int
     if (gx > n_out) gx = n_out;
     if (gx < 1) gx = 1;
     dim3 grid((unsigned)gx, gy, gz);
-    if (small)
+    if (sgn)
+      mac_fast_kernel<true, NR, true><<<grid, th, 0, (cudaStream_t)stream>>>(
+          d_in0, n_in0, d_in1, d_rowptr, d_col, d_coef, F, x->logn, x->k, x->ext->d_lc, fold_sgn, (int)n_out);
+    else if (small)
       mac_fast_kernel<true, NR><<<grid, th, 0, (cudaStream_t)stream>>>(d_in0, n_in0, d_in1, d_rowptr, d_col, d_coef, F,
                                                                      x->logn, x->k, x->ext->d_lc, fold_small, (int)n_out);
     else
@@ -1936,6 +1967,15 @@ static const double2* c2_twist(fcn_ctx* x, int64_t c2, cudaStream_t st) {
   }
   x->ftwist_c2[c2] = d;
   return d;
+}
+
+// FCN_MAC_SGN=0: the MAC keeps separate positive / negative accumulators (A/B tests).
+static bool mac_sgn_enabled() {
+  static const bool on = [] {
+    const char* ev = getenv("FCN_MAC_SGN");
+    return !(ev && ev[0] == '0');
+  }();
+  return on;
 }
 
 // FCN_PRESCALE=0 keeps (B/b_j)^-1 in the rescale kernel instead of the INTT twist (A/B tests).

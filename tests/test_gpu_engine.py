@@ -380,3 +380,34 @@ def test_eval_graph_replay_matches_eager(E):
     tensor.buf.copy_(other.buf)
     assert torch.equal(g.replay().buf, want2)
     assert torch.equal(g.replay().buf, want2)
+
+
+@pytest.mark.parametrize("scale", [1, 16, 512], ids=["signed-acc", "two-acc", "generic"])
+def test_mac_coefficient_ranges_vs_oracle(E, scale):
+    """The three sparse-MAC kernels the coefficient range selects (cfg2 ring,
+    50-bit limbs): |c| <= 64 one signed accumulator per residue, |c| <= 2^10
+    positive / negative accumulators, |c| <= 2^15 the generic kernel; each
+    exact vs the oracle's mul_pt + add_ct chain (batched constants scaled by
+    `scale`, still centred mod t)."""
+    from paper_1811_09953_b200 import configs
+    from paper_1811_09953_b200 import device as dev
+    from paper_1811_09953_b200 import fv
+
+    W = configs.WORKLOADS["cfg2"]
+    P = fv.EncryptionParams(W.n, W.primes, (W.t,), W.beta)
+    OP = ob.Params(W.n, W.primes, (W.t,), W.beta)
+    plan = configs.mac_sweep_plan(n_out=5, n_in=40, terms=12, seed=9)
+    rng = np.random.default_rng(4)
+    x = np.stack([np.stack([orn.random_uniform(W.primes, W.n, rng) for _ in range(2)]) for _ in range(40)])
+    mac, _, _ = E._lower_linear(plan, W.t, W.n, "batched")
+    coef = mac.coef.cpu().numpy() * scale
+    assert np.abs(coef).max() <= W.t // 2
+    m2 = E._Mac(mac.rowptr, mac.col, mac.rot, mac.coef * scale, mac.n_out, mac.n_terms, mac.no_rot,
+                int(np.abs(coef).max()))
+    out = dev.to_host(E._mac_out(P, m2, dev.to_device(x), None))
+    for o in range(5):
+        acc = None
+        for tp in plan.outputs[o].taps:
+            term = ob.mul_pt(OP, ob.Ct(x[tp.in_index, 0], x[tp.in_index, 1]), [(tp.weight_int * scale) % W.t])
+            acc = term if acc is None else ob.add_ct(OP, acc, term)
+        assert np.array_equal(out[o], np.stack([acc.c0, acc.c1])), o
