@@ -605,14 +605,13 @@ int launch_ntt_f64(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, i
 // inputs are canonical (B = 1), and every value must stay below 2^53.
 // Returns the cheapest schedule (2, then 1) whose bound holds for limbs up
 // to qmax, else 0 (proved for every q < 2^51).  FCN_NTT_RS=0/1/2 caps it.
-static int g_rs_cap = -1;
 int f64_schedule(int logn, uint64_t qmax) {
-  if (g_rs_cap < 0) {
+  static const int rs_cap = [] {  // thread-safe one-time read
     const char* ev = getenv("FCN_NTT_RS");
-    g_rs_cap = (ev && ev[0] >= '0' && ev[0] <= '2') ? ev[0] - '0' : 2;
-  }
+    return (ev && ev[0] >= '0' && ev[0] <= '2') ? ev[0] - '0' : 2;
+  }();
   const double e = ((double)qmax + 1.0) * 0x1p-53 * (1.0 + 1e-12);
-  for (int rs = g_rs_cap; rs >= 1; --rs) {
+  for (int rs = rs_cap; rs >= 1; --rs) {
     double B = 1.0;
     bool ok = true;
     for (int s = 0; s < logn && ok; ++s) {
@@ -635,7 +634,14 @@ template <int RS>
 int launch_ntt_f64_sq(const fcn_ring* r, const uint64_t* a, const uint64_t* aux, uint64_t* Tout, int64_t units, int k,
                       int m, cudaStream_t st, int sms, bool dbl);  // ntt_f64.cuh
 
-static int g_force_int = -1;  // FCN_NTT_INT=1 selects the integer kernels (A/B tests)
+// FCN_NTT_INT=1 selects the integer kernels (A/B tests); read once, thread-safe
+static bool force_int() {
+  static const bool on = [] {
+    const char* ev = getenv("FCN_NTT_INT");
+    return ev && ev[0] == '1';
+  }();
+  return on;
+}
 
 int ntt_family(const fcn_ring* r, int period, int offset) {
   const int logn = r->logn;
@@ -645,11 +651,7 @@ int ntt_family(const fcn_ring* r, int period, int offset) {
     v2 = q >= (1ull << 34) && q < (1ull << 56);
   }
   if (!v2) return 0;
-  if (g_force_int < 0) {
-    const char* ev = getenv("FCN_NTT_INT");
-    g_force_int = (ev && ev[0] == '1') ? 1 : 0;
-  }
-  bool f64 = !g_force_int && r->d_ffwd;
+  bool f64 = !force_int() && r->d_ffwd;
   for (int l = 0; f64 && l < period; ++l) f64 = r->primes[offset + l] < (1ull << 51);
   return f64 ? 2 : 1;
 }
