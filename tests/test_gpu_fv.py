@@ -417,3 +417,32 @@ def test_empty_and_single_unit_batches(F):
         for b in {0, B - 1}:
             want = ob.mul_ct(OP, ob.Ct(x[b, 0], x[b, 1]), ob.Ct(x[b, 0], x[b, 1]), K)
             assert np.array_equal(out[b], np.stack([want.c0, want.c1])), (B, b)
+
+
+def test_wire_format_round_trip_cfg2(F):
+    """Reference A6 / test_fv.py serialization: at the cfg2 shape a
+    ciphertext is 65,544 u64 words (64-byte header + [2][4][8192] body), so
+    784 of them are 411,091,968 bytes; bytes -> ciphertext -> bytes is the
+    identity (data and lane / scale / depth metadata), truncation, trailing
+    bytes and evaluation-key bytes are rejected."""
+    from paper_1811_09953_b200 import configs
+
+    W = configs.WORKLOADS["cfg2"]
+    P = F.EncryptionParams(W.n, W.primes, (W.t,), W.beta)
+    sk, pk, ek = F.keygen(P, 2)
+    assert F.ciphertext_num_words(P) == 65544
+    assert 784 * F.ciphertext_num_words(P) * 8 == 411091968
+    ct = F.encrypt(pk, P, F.PlainPoly(W.t, [7, 0, 3]), 0, 5, np.random.default_rng(1))
+    sq = F.mul_ct(ct, ct, ek)
+    for c in (ct, sq):
+        data = F.ciphertext_to_bytes(c)
+        assert len(data) == 65544 * 8
+        back = F.ciphertext_from_bytes(data, P)
+        assert F.ciphertext_to_bytes(back) == data
+        assert (back.lane, back.scale_exponent, back.mul_depth) == (c.lane, c.scale_exponent, c.mul_depth)
+        with pytest.raises(F.FVError):
+            F.ciphertext_from_bytes(data[:-8], P)
+        with pytest.raises(F.FVError):
+            F.ciphertext_from_bytes(data + bytes(8), P)
+    with pytest.raises(F.FVError):
+        F.ciphertext_from_bytes(F.eval_keys_to_bytes(ek, P), P)

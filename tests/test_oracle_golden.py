@@ -194,3 +194,16 @@ def test_config_plans_match_reference(name, golden_meta):
     hops = netplan.plan_hops(comp, "integer")
     assert [list(r[:5]) + [r[6]] for r in hops.rows()] == g["layers"]
     assert comp.out_scale == g["out_scale"]
+
+
+def test_integer_encoder_known_answers():
+    """Reference test_encode.py:19-35 known answers of the base-2 encoder the
+    integer encoding uses (host code, no GPU): 5 -> [1, 0, 1], -3 -> [t-1,
+    t-1], 0 -> zero polynomial; decode inverts them."""
+    from paper_1811_09953_b200 import encode
+
+    t = 65537
+    assert encode.encode_integer(5, t).coeffs.tolist() == [1, 0, 1]
+    assert encode.encode_integer(-3, t).coeffs.tolist() == [t - 1, t - 1]
+    for z in (0, 1, -1, 5, -3, 1 << 40, -(1 << 40) + 7):
+        assert encode.decode_integer(encode.encode_integer(z, t)) == z
