@@ -446,3 +446,43 @@ def test_wire_format_round_trip_cfg2(F):
             F.ciphertext_from_bytes(data + bytes(8), P)
     with pytest.raises(F.FVError):
         F.ciphertext_from_bytes(F.eval_keys_to_bytes(ek, P), P)
+
+
+def test_homomorphic_round_trips_random(F):
+    """Reference A2-style homomorphism on the FP64 hot path (n = 1024, three
+    primes just above 2^50, t = 65537): for random plaintext polynomials a, b
+    and constants c, decrypt(add_ct) = a + b, decrypt(mul_pt) = c a and
+    decrypt(mul_ct) = a b in Z_t[x]/(x^n + 1)."""
+    from paper_1811_09953_b200 import configs
+
+    n, t = 1024, 65537
+    primes = tuple(configs.find_ntt_primes(n, 3, bits=50))
+    P = F.EncryptionParams(n, primes, (t,), 1 << 32)
+    sk, pk, ek = F.keygen(P, 11)
+    rng = np.random.default_rng(12)
+
+    def negacyclic(a, b):
+        full = np.zeros(2 * n, dtype=object)
+        for i in np.nonzero(a)[0]:
+            full[i : i + n] += int(a[i]) * b.astype(object)
+        return np.array([(full[j] - full[j + n]) % t for j in range(n)], dtype=object)
+
+    def dense(p):
+        out = np.zeros(n, dtype=object)
+        out[: p.coeffs.size] = p.coeffs.astype(object)
+        return out
+
+    for trial in range(12):
+        a = np.zeros(n, dtype=np.uint64)
+        b = np.zeros(n, dtype=np.uint64)
+        ia = rng.choice(n, 6, replace=False)
+        ib = rng.choice(n, 6, replace=False)
+        a[ia] = rng.integers(0, t, 6)
+        b[ib] = rng.integers(0, t, 6)
+        c = int(rng.integers(1, t))
+        ca = F.encrypt(pk, P, F.PlainPoly(t, a), 0, 0, rng)
+        cb = F.encrypt(pk, P, F.PlainPoly(t, b), 0, 0, rng)
+        A, B = a.astype(object), b.astype(object)
+        assert np.array_equal(dense(F.decrypt(sk, F.add_ct(ca, cb))), (A + B) % t), trial
+        assert np.array_equal(dense(F.decrypt(sk, F.mul_pt(ca, F.PlainPoly(t, [c])))), (A * c) % t), trial
+        assert np.array_equal(dense(F.decrypt(sk, F.mul_ct(ca, cb, ek))), negacyclic(a, b)), trial
