@@ -105,14 +105,20 @@ __device__ __forceinline__ void mw_mac(uint64_t (&a)[NW], const uint64_t* __rest
   uint64_t carry = 0;
 #pragma unroll
   for (int i = 0; i < NW; ++i) {
-    const uint64_t s = i < nsrc ? src[i] : 0;
-    uint64_t lo = s * y, hi = __umul64hi(s, y);
-    uint64_t t = a[i] + lo;
-    hi += t < lo;
-    uint64_t t2 = t + carry;
-    hi += t2 < carry;
-    a[i] = t2;
-    carry = hi;
+    if (i < nsrc) {  // a compile-time bound folds the products away past it
+      const uint64_t s = src[i];
+      uint64_t lo = s * y, hi = __umul64hi(s, y);
+      uint64_t t = a[i] + lo;
+      hi += t < lo;
+      uint64_t t2 = t + carry;
+      hi += t2 < carry;
+      a[i] = t2;
+      carry = hi;
+    } else {
+      const uint64_t t = a[i] + carry;
+      carry = t < carry;
+      a[i] = t;
+    }
   }
 }
 
@@ -701,23 +707,33 @@ __global__ void tensor_kernel(const uint64_t* __restrict__ A, const uint64_t* __
 // Base-beta digits of the canonical R2 (fv.py:524-533) from its residues:
 // one row per digit when every digit is already < q_i (P.direct), else
 // per-limb rows.
-template <int KQ, int KE, int NW>
+// NARROW (FP64 path: every prime < 2^51, exact limb count k = KQ): q has at
+// most NQ = ceil(51 KQ / 64) words and q/q_i at most NS = ceil(51 (KQ-1) / 64),
+// so the multiword CRT runs on NQ + 1 words with NS-word multiplicands
+// instead of NW-word ones (half the 64-bit products at KQ = 4).
+template <int KQ, int KE, int NW, bool NARROW = false>
 __device__ __forceinline__ void emit_digits(const uint64_t* out, const RescaleP<KQ, KE>& P,
                                             const MulCtConst* __restrict__ cc, uint64_t* __restrict__ DG, int64_t ct,
                                             int coef, int n) {
   const int k = P.k;
-  uint64_t a[NW];
-  mw_zero<NW>(a);
+  constexpr int NQ = (51 * KQ + 63) / 64;
+  constexpr int NA = (NARROW && NQ + 1 < NW) ? NQ + 1 : NW;
+  constexpr int NS = NARROW ? ((51 * (KQ - 1) + 63) / 64 < NA ? (51 * (KQ - 1) + 63) / 64 : NA) : NA;
+  uint64_t b[NA];
+  mw_zero<NA>(b);
   double fu = 0.0;
 #pragma unroll
   for (int i = 0; i < KQ; ++i) {
     if (i < k) {
       const uint64_t z = shoup(out[i], P.qinv[i], P.qinv_s[i], P.q[i]);
       fu += (double)z * P.rq[i];
-      mw_mac<NW>(a, cc->Qw[i], cc->qwords, z);
+      mw_mac<NA>(b, cc->Qw[i], NARROW ? NS : cc->qwords, z);
     }
   }
-  mw_reduce_q<NW>(a, cc, (int64_t)floor(fu));
+  mw_reduce_q<NA>(b, cc, (int64_t)floor(fu));
+  uint64_t a[NW];
+#pragma unroll
+  for (int i = 0; i < NW; ++i) a[i] = i < NA ? b[i] : 0;
   const int D = P.D, w = P.w;
   if (P.direct && w == 32) {
     // beta = 2^32 (the configs): digit d is half d&1 of word d>>1 (compile-time indices)
@@ -1042,7 +1058,7 @@ __global__ void __launch_bounds__(256, FCN_RS_MINB(KQ))
       for (int i = 0; i < KQ; ++i)
         if (i < k) R01[((ct * 2 + p) * k + i) * n + coef] = out[i];
     } else {
-      emit_digits<KQ, KE, NW>(out, P, cc, DG, ct, coef, n);
+      emit_digits<KQ, KE, NW, true>(out, P, cc, DG, ct, coef, n);
     }
   }
 }
