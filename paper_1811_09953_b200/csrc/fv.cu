@@ -943,16 +943,19 @@ __global__ void __launch_bounds__(256, FCN_RS_MINB(KQ))
   constexpr int SL = KE + KQ;  // staged words per coefficient: K tensor residues (+ k activation inputs)
   const int tid = threadIdx.x, T = blockDim.x;
   const bool act = P.act != 0;
+  // (ciphertext, poly) index pairs stay below 2^31 (C 3 rows): 32-bit
+  // division by 3, and one base pointer per staged coefficient
   auto stage = [&](int64_t ee, uint64_t* buf) {
-    const int64_t cpp = ee >> logn;
+    const int cpp = (int)(ee >> logn);
     const int cf = (int)(ee & (n - 1));
+    const uint64_t* src = T_in + ((int64_t)cpp * K << logn) + cf;
 #pragma unroll
-    for (int j = 0; j < KE; ++j) cp_async8(&buf[j * T + tid], &T_in[(cpp * K + j) * n + cf]);
-    const int pp = (int)(cpp % 3);
+    for (int j = 0; j < KE; ++j) cp_async8(&buf[j * T + tid], src + ((int64_t)j << logn));
+    const int ctt = cpp / 3, pp = cpp - 3 * ctt;
     if (act && pp < 2) {
-      const int64_t ctt = cpp / 3;
+      const uint64_t* ls = lin + ((int64_t)(ctt * 2 + pp) * k << logn) + cf;
 #pragma unroll
-      for (int i = 0; i < KQ; ++i) cp_async8(&buf[(KE + i) * T + tid], &lin[((ctt * 2 + pp) * k + i) * n + cf]);
+      for (int i = 0; i < KQ; ++i) cp_async8(&buf[(KE + i) * T + tid], ls + ((int64_t)i << logn));
     }
   };
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -960,10 +963,10 @@ __global__ void __launch_bounds__(256, FCN_RS_MINB(KQ))
   cp_async_commit();
   int sb = 0;
   for (; e < total; e += stride) {
-    const int64_t cp = e >> logn;
+    const int cp32 = (int)(e >> logn);
     const int coef = (int)(e & (n - 1));
-    const int64_t ct = cp / 3;
-    const int p = (int)(cp % 3);
+    const int64_t ct = cp32 / 3;
+    const int p = cp32 - 3 * (int)ct;
     if (e + stride < total) stage(e + stride, stage_buf + (sb ^ 1) * SL * T);
     cp_async_commit();
     cp_async_wait<1>();
