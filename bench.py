@@ -55,6 +55,7 @@ def _args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of one CUDA graph per step")
+    ap.add_argument("--force-sharded", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
     return ap.parse_args()
 
@@ -419,7 +420,9 @@ def run_gpu(args, ws, rank, local):
     W, P, sk, pk, ek, net, cfg, x, tensor = _setup(args.workload, seed_offset=rank if args.shard == "replicas" else 0)
     comp = engine.compile_network(net, cfg)
     plan = comp  # evaluations take the compiled plan (no per-call content hash of the weights)
-    sharded = ws > 1 and args.shard == "outputs"
+    # --force-sharded: the sharded code path at world size 1 (checks the
+    # multi-GPU plumbing -- pre-flight, transports, timing -- on one GPU)
+    sharded = (ws > 1 or args.force_sharded) and args.shard == "outputs"
     if sharded:
         from paper_1811_09953_b200 import dist as fdist
 
@@ -505,10 +508,35 @@ def run_gpu(args, ws, rank, local):
         if sharded:
             from paper_1811_09953_b200 import dist as fdist
 
+            n_in = tensor.buf.shape[0]
+            parts = fdist.partition(n_in, ws)
+            lo, hi = parts[rank]
+            block = parts[0][1] - parts[0][0]
+            copy = torch.cuda.Stream()
+
             def stream(batches):
-                for hb in batches:
-                    t_in = engine.CipherTensor(tensor.shape, scale_exponent=tensor.scale_exponent,
-                                               buf=hb.to("cuda", non_blocking=True), params=P, lane=0)
+                # each rank uploads its 1/world of batch i+1 on a copy stream
+                # while batch i computes; an NVLink all-gather assembles it
+                # (dist.upload_sharded, split in two for the overlap)
+                def up(hb):
+                    with torch.cuda.stream(copy):
+                        loc = hb[lo:hi].to("cuda", non_blocking=True)
+                        ev = torch.cuda.Event()
+                        ev.record(copy)
+                    return loc, ev
+
+                it = iter(batches)
+                hb = next(it, None)
+                nxt = up(hb) if hb is not None else None
+                while nxt is not None:
+                    loc, ev = nxt
+                    torch.cuda.current_stream().wait_event(ev)
+                    loc.record_stream(torch.cuda.current_stream())
+                    hb = next(it, None)
+                    nxt = up(hb) if hb is not None else None
+                    full = fdist._torch_gather(loc, n_in, block)
+                    t_in = engine.CipherTensor(tensor.shape, scale_exponent=tensor.scale_exponent, buf=full, params=P,
+                                               lane=0)
                     yield evaluate(t_in).buf.to("cpu")
         else:
             # result ring allocated once, like a server would (pinned allocation is slow)
@@ -539,7 +567,9 @@ def run_gpu(args, ws, rank, local):
             t_e2e = float(tt.item())
         e2e = {"value": images / t_e2e, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": t_e2e * 1e3, "batches": n_e2e,
-               "api": "engine.evaluate_stream (pinned host batches in, host result bodies out)"}
+               "api": "engine.evaluate_stream (pinned host batches in, host result bodies out)" if not sharded else
+               "dist.upload_sharded (each rank uploads 1/world of the pinned batch, NVLink all-gather) + "
+               "dist.eval_encrypted_sharded + host result bodies out"}
 
     if rank != 0:
         return
@@ -639,7 +669,8 @@ def run_gpu(args, ws, rank, local):
 def main():
     args = _args()
     ws, rank, local = _dist()
-    if ws > 1:
+    group = ws > 1 or (args.force_sharded and args.impl != "reference")
+    if group:
         import torch
         import torch.distributed as dist
 
@@ -651,7 +682,7 @@ def main():
         run_reference(args, ws, rank)
     else:
         run_gpu(args, ws, rank, local)
-    if ws > 1:
+    if group:
         import torch.distributed as dist
 
         dist.destroy_process_group()

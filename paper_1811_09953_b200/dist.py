@@ -95,6 +95,29 @@ def _torch_gather(local, count: int, block: int, group=None):
     return full[:count].contiguous()
 
 
+def upload_sharded(host_batch, group=None, device=None):
+    """One input batch onto every rank with 1/world of the PCIe traffic each.
+
+    Rank r copies its contiguous block of the [count][...] host rows
+    (pinned memory: asynchronous) to its own GPU, and the blocks are
+    all-gathered over NVLink (NCCL) into the full device batch on every rank
+    -- the first layer reads all inputs, so every rank needs the whole batch,
+    but no rank's PCIe link carries more than its share.  gloo groups gather
+    on the CPU (tests)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    count = host_batch.shape[0]
+    parts = partition(count, world)
+    lo, hi = parts[rank]
+    block = parts[0][1] - parts[0][0]
+    if device is None:
+        device = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    local = host_batch[lo:hi].to(device, non_blocking=True)
+    return _torch_gather(local, count, block, group)
+
+
 def _prepare(net, tensor, cfg, encoding):
     from . import engine
 

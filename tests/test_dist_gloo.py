@@ -141,3 +141,35 @@ def test_sharded_schedule_matches_single_process(world):
     for (body, scale, depth), w in zip(got, want):
         assert body == np.stack([w.c0, w.c1]).tobytes()
         assert (scale, depth) == (w.scale, w.depth)
+
+
+def _upload_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        for count in (7, 2, 1):
+            g = torch.Generator().manual_seed(count)
+            host = torch.randint(0, 1 << 50, (count, 2, 3, 16), generator=g, dtype=torch.int64)
+            full = fdist.upload_sharded(host)
+            q.put((rank, count, bool(torch.equal(full, host))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_upload_sharded_reassembles_the_batch(world):
+    """dist.upload_sharded: every rank copies only its block of the host batch
+    and the all-gather hands every rank the whole batch, including counts
+    smaller than the world size (empty blocks)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_upload_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(3 * world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert all(ok for _, _, ok in res), res
