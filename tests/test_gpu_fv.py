@@ -486,3 +486,39 @@ def test_homomorphic_round_trips_random(F):
         assert np.array_equal(dense(F.decrypt(sk, F.add_ct(ca, cb))), (A + B) % t), trial
         assert np.array_equal(dense(F.decrypt(sk, F.mul_pt(ca, F.PlainPoly(t, [c])))), (A * c) % t), trial
         assert np.array_equal(dense(F.decrypt(sk, F.mul_ct(ca, cb, ek))), negacyclic(a, b)), trial
+
+
+def test_cfg5_full_batch_square_decrypts():
+    """BASELINE configs[4] at full size: 4,096 ciphertexts of n = 16384 over
+    8 limbs, squared and relinearised with the dnum = 3 key (beta = 2^134) in
+    one batched call (the sweep's operation); every result decrypts to the
+    square of its plaintext m = c + d x^j in Z_t[x]/(x^n + 1)."""
+    from paper_1811_09953_b200 import configs
+    from paper_1811_09953_b200 import device as dev
+    from paper_1811_09953_b200 import fv as F
+
+    W = configs.WORKLOADS["cfg5"]
+    P = F.EncryptionParams(W.n, W.primes, (W.t,), W.beta)
+    assert P.ell + 1 == 3
+    sk, pk, ek = F.keygen(P, configs.SEED_KEYS)
+    B, n, t = 4096, W.n, W.t
+    rng = np.random.default_rng(21)
+    c = rng.integers(-(t // 2), t // 2 + 1, B)
+    d = rng.integers(-(t // 2), t // 2 + 1, B)
+    j = rng.integers(1, n, B)
+    plain = np.zeros((B, n), dtype=np.int64)
+    plain[:, 0] = c
+    plain[np.arange(B), j] = d
+    cts = F.encrypt_batch(pk, P, plain, 0, np.random.default_rng(22))
+    sq = F.mul_ct_batch(P, ek, 0, cts)
+    got = F.decrypt_batch(sk, P, sq).astype(np.int64)
+    want = np.zeros((B, n), dtype=object)
+    want[:, 0] = c.astype(object) ** 2
+    want[np.arange(B), j] += 2 * c.astype(object) * d.astype(object)
+    for b in range(B):  # d^2 x^(2j): negacyclic wrap
+        e = 2 * int(j[b])
+        if e < n:
+            want[b, e] += int(d[b]) ** 2
+        else:
+            want[b, e - n] -= int(d[b]) ** 2
+    assert np.array_equal(got, (want % t).astype(np.int64))
