@@ -1029,10 +1029,10 @@ __global__ void __launch_bounds__(256, FCN_RS_MINB(KQ))
       atomicAdd(fallbacks, 1ull);
     }
     const double gd = (double)g;
-    uint64_t out[KQ];
+    double od[KQ];  // R mod q_i, reduced: |.| <= q_i / 2 + 2^-40 q_i
 #pragma unroll
     for (int i = 0; i < KQ; ++i) {
-      out[i] = 0;
+      od[i] = 0.0;
       if (i < k) {
         const double qi = P.fq[i], qii = P.fqi[i];
         double acc = gd + fmulq_lr(v, P.fntp[i], P.fntpq[i], qi);
@@ -1044,23 +1044,28 @@ __global__ void __launch_bounds__(256, FCN_RS_MINB(KQ))
           if (j % RP == RP - 1) acc = fredq(acc, qii, qi);
           acc += fmulq_lr(y[j], P.frc[i][j], P.frcq[i][j], qi);
         }
-        out[i] = f2u_canon(fredq(acc, qii, qi), qi);
+        od[i] = fredq(acc, qii, qi);
       }
     }
     if (p < 2) {
-      if (P.act) {
+      // R0 / R1 rows for the final INTT's epilogue; dbl_in: as signed doubles
+      // like the other rows of the square pipeline
 #pragma unroll
-        for (int i = 0; i < KQ; ++i) {
+      for (int i = 0; i < KQ; ++i) {
+        if (i < k) {
           const double qi = P.fq[i], qii = P.fqi[i];
-          const double a = u2f(cb[(KE + i) * T + tid]);
-          const double s2 = fmulq(u2f(out[i]), P.fc2[i], P.fc2q[i], qi) + fmulq(a, P.fc1[i], P.fc1q[i], qi);
-          out[i] = f2u_canon(fredq(s2, qii, qi), qi);
+          double r = od[i];
+          if (P.act) {
+            const double a = u2f(cb[(KE + i) * T + tid]);
+            r = fredq(fmulq(r, P.fc2[i], P.fc2q[i], qi) + fmulq(a, P.fc1[i], P.fc1q[i], qi), qii, qi);
+          }
+          R01[((ct * 2 + p) * k + i) * n + coef] = P.dbl_in ? (uint64_t)__double_as_longlong(r) : f2u_canon(r, qi);
         }
       }
-#pragma unroll
-      for (int i = 0; i < KQ; ++i)
-        if (i < k) R01[((ct * 2 + p) * k + i) * n + coef] = out[i];
     } else {
+      uint64_t out[KQ];
+#pragma unroll
+      for (int i = 0; i < KQ; ++i) out[i] = i < k ? f2u_canon(od[i], P.fq[i]) : 0;
       emit_digits<KQ, KE, NW, true>(out, P, cc, DG, ct, coef, n);
     }
   }

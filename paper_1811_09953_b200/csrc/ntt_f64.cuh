@@ -406,7 +406,8 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 // during the last pass (each thread fetches exactly the residues it will
 // combine, so no barrier is needed); the next input row is prefetched into
 // registers instead (coalesced, as in the forward kernel).
-// DBL: the input rows (data) are signed residues as raw doubles, |x| <= q.
+// DBL: the input rows (data) and the add rows are signed residues as raw
+// doubles (|x| <= q), the square pipeline's internal format.
 template <int LOGN, int RS, bool SCALE, bool FAN, bool DBL = false>
 __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     ntt_f64_inv_epi(const uint64_t* __restrict__ data, int64_t n_rows, int period, int offset,
@@ -480,7 +481,8 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
       const double2 w = ld_ftw(twist + tid + j * T);
       double y = fmulq(x[j], w.x, w.y, q);  // |y| < 1.5 q (|x| < 7.5 q)
       if (SCALE) y = fmulq(y, c2, c2q, q);  // |y| < 0.7 q
-      const uint64_t v = f2u_canon(fredq(y + u2f(sm[pst + j * (T + T / 32)]), qi, q), q);
+      const uint64_t ar = sm[pst + j * (T + T / 32)];  // DBL: the add row (R0/R1) is signed doubles too
+      const uint64_t v = f2u_canon(fredq(y + (DBL ? __longlong_as_double((long long)ar) : u2f(ar)), qi, q), q);
       po[tid + j * T] = v;
       if (FAN) {  // fan-out to the peers' buffers
         for (int d = 1; d < nd; ++d) E.out.dst[d][row * N + tid + j * T] = v;
