@@ -590,7 +590,8 @@ __global__ void __launch_bounds__(256) lift_f64_kernel(const uint64_t* __restric
   const int n = 1 << logn;
   constexpr int k = KQ, m = KA, K = KQ + KA;  // exact-size instantiations only
   // compact: only the m auxiliary rows are written, as [poly][m][n] (the
-  // q-limb rows of the lift are the input rows themselves)
+  // q-limb rows of the lift are the input rows themselves); compact == 2:
+  // as signed doubles (the square pipeline's double-row format)
   const int64_t total = npoly << logn;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   constexpr double M = 6755399441055744.0;
@@ -664,7 +665,9 @@ __global__ void __launch_bounds__(256) lift_f64_kernel(const uint64_t* __restric
           if (i % RP == RP - 1) acc = fredq(acc, pji, pj);
           acc += fmulq_lr(y[i], P.flc[j][i], P.flcq[j][i], pj);
         }
-        ext[(compact ? poly * m + j : poly * K + k + j) * n + coef] = f2u_canon(fredq(acc, pji, pj), pj);
+        const double rr = fredq(acc, pji, pj);
+        ext[(compact ? poly * m + j : poly * K + k + j) * n + coef] =
+            compact == 2 ? (uint64_t)__double_as_longlong(rr) : f2u_canon(rr, pj);
       }
     }
   }
@@ -1847,7 +1850,8 @@ static int f64_product_period(const fcn_ctx* x) {
 
 template <int KQ, int KE>
 static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t* in, uint64_t* out, int64_t cnt,
-                            uint64_t* R01, uint64_t* DG, cudaStream_t st, ActArgs* act, bool* compact) {
+                            uint64_t* R01, uint64_t* DG, cudaStream_t st, ActArgs* act, bool* compact,
+                            const int* lift_mode) {
   const bool f64 = x->fp && x->k == KQ && x->k + x->m == KE;  // FP64 kernels: exact sizes
   const MulCtConst& mc = x->host_mc[lane];
   const MulCtConst* dmc = x->d_mc + lane;
@@ -1857,10 +1861,10 @@ static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_
     if (compact) *compact = *compact && f64;  // only the FP64 lift writes the compact layout
     if (f64 && f64_product_period(x) == 12)
       lift_f64_kernel<KQ, KE - KQ, KQ + 2, 12><<<grid_for(total, 256), 256, 0, st>>>(
-          in, out, cnt, x->logn, P, dmc, x->d_fallbacks, compact && *compact ? 1 : 0);
+          in, out, cnt, x->logn, P, dmc, x->d_fallbacks, compact && *compact ? (lift_mode ? *lift_mode : 1) : 0);
     else if (f64)
       lift_f64_kernel<KQ, KE - KQ, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(
-          in, out, cnt, x->logn, P, dmc, x->d_fallbacks, compact && *compact ? 1 : 0);
+          in, out, cnt, x->logn, P, dmc, x->d_fallbacks, compact && *compact ? (lift_mode ? *lift_mode : 1) : 0);
     else
       lift_kernel<KQ, KE - KQ, KQ + 2><<<grid_for(total, 256), 256, 0, st>>>(in, out, cnt, x->logn, P, dmc,
                                                                              x->d_fallbacks);
@@ -1920,10 +1924,11 @@ static bool f64_lift_rescale(const fcn_ctx* x) {
 
 static int lift_or_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t* in, uint64_t* out, int64_t cnt,
                            uint64_t* R01, uint64_t* DG, cudaStream_t st, ActArgs* act = nullptr,
-                           bool* compact = nullptr) {
+                           bool* compact = nullptr, const int* lift_mode = nullptr) {
   const int k = x->k, m = x->m;
 #define FCN_TRY(KQ, KE) \
-  if (k <= KQ && m <= KE - KQ) return run_lift_rescale<KQ, KE>(lift, x, lane, in, out, cnt, R01, DG, st, act, compact);
+  if (k <= KQ && m <= KE - KQ)                                                                                   \
+    return run_lift_rescale<KQ, KE>(lift, x, lane, in, out, cnt, R01, DG, st, act, compact, lift_mode);
   FCN_TRY(2, 5)
   FCN_TRY(2, 6)
   FCN_TRY(3, 6)
@@ -2125,11 +2130,18 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
     // FP64 rings: compact lift (auxiliary rows only) and one fused
     // forward-NTT + tensor kernel that reads the q-limb rows from a itself.
     bool fused = !b && x->fp && sq_fuse_enabled() && logn >= 10 && logn <= 14;
+    // the tensor INTT's twist also applies the rescale's first factor
+    // (B/b_j)^-1 on the FP64 path (one multiply per residue saved), and the
+    // square pipeline keeps its workspace rows as signed doubles from the
+    // compact lift to the final INTT (no u64 round trips in between)
+    const bool prescale = x->d_ftwist_binv && ntt_family(x->ext, K, 0) == 2 && f64_lift_rescale(x) && prescale_enabled();
+    const bool want_dbl = fused && prescale && dbl_rows(x);
     if (fused) {
-      int rc = lift_or_rescale(true, x, lane, a, EA, C * 2, nullptr, nullptr, st, nullptr, &fused);
+      int lift_mode = want_dbl ? 2 : 1;  // compact lift; 2: auxiliary rows as signed doubles
+      int rc = lift_or_rescale(true, x, lane, a, EA, C * 2, nullptr, nullptr, st, nullptr, &fused, &lift_mode);
       if (rc) return rc;
       if (fused) {
-        rc = launch_ntt_square_tensor(x->ext, a, EA, T, C, k, x->m, st, dbl_rows(x));
+        rc = launch_ntt_square_tensor(x->ext, a, EA, T, C, k, x->m, st, want_dbl);
         if (rc) return rc < 0 ? rc : set_error(FCN_ERR_STATE, "fused square tensor unavailable");
       } else {  // the lift wrote the full extended rows
         rc = launch_ntt(x->ext, EA, C * 2 * K, K, 0, true, st);
@@ -2153,12 +2165,8 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
                                                                             x->ext->d_lc);
       FCN_LAUNCH_CHECK(x->fp ? "tensor_f64_kernel" : "tensor_kernel");
     }
-    // (iii) inverse NTT; on the FP64 path its twist also applies the
-    // rescale's first factor (B/b_j)^-1 (one multiply per residue saved)
-    const bool prescale = x->d_ftwist_binv && ntt_family(x->ext, K, 0) == 2 && f64_lift_rescale(x) && prescale_enabled();
-    // the square pipeline keeps its workspace rows as signed doubles from the
-    // fused forward NTT to the final INTT (no u64 round trips in between)
-    const bool dbl = fused && prescale && dbl_rows(x);
+    // (iii) inverse NTT
+    const bool dbl = fused && want_dbl;
     NttEpi tw_epi;
     tw_epi.mode = 0;
     tw_epi.ftwist = x->d_ftwist_binv;

@@ -228,7 +228,8 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 // kernel.  A0 is parked (centred doubles) in the d2 row by the per-warp
 // copy-out and read back by the very thread that wrote it.  Input rows: limb
 // l < k from the ciphertexts a ([C][2][k][n]), l >= k from the lift's compact
-// auxiliary rows aux ([C][2][m][n]).
+// auxiliary rows aux ([C][2][m][n]; DBL: signed doubles).  DBL also makes the
+// outputs signed doubles.
 template <int LOGN, int RS, bool DBL = false>
 __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     ntt_f64_fwd_sq(const uint64_t* __restrict__ a, const uint64_t* __restrict__ aux, uint64_t* __restrict__ Tout,
@@ -260,8 +261,10 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     const int limb = (int)(u - ct * K);
     const LimbConst& c = lcs[limb];
     const double q = c.fq, qi = c.fqi;
+    if (!DBL || limb < k) {  // DBL: the auxiliary rows (limb >= k) arrive as signed doubles from the lift
 #pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = u2f((uint64_t)__double_as_longlong(x[j]));
+      for (int j = 0; j < 32; ++j) x[j] = u2f((uint64_t)__double_as_longlong(x[j]));
+    }
     fwd_body<LOGN, RS>(x, tid, fs, tws + (int64_t)limb * N, twl + (int64_t)limb * N, q, qi);
 #pragma unroll
     for (int j = 0; j < 32; ++j) fs[tid * 33 + j] = fredq(x[j], qi, q);  // |.| <= q/2 + 2^-40 q

@@ -330,8 +330,10 @@ def test_errors(F):
 
 
 @pytest.mark.parametrize("env", [{"FCN_NTT_INT": "1"}, {"FCN_SQ_FUSE": "0"}, {"FCN_NTT_RS": "0"},
-                                 {"FCN_DBL_ROWS": "0", "FCN_PRESCALE": "0"}, {"FCN_TWIST_C2": "0"}],
-                         ids=["integer-kernels", "unfused-square", "ntt-rs0", "u64-rows", "scaling-epilogue"])
+                                 {"FCN_DBL_ROWS": "0", "FCN_PRESCALE": "0"}, {"FCN_TWIST_C2": "0"},
+                                 {"FCN_PRESCALE": "0"}],
+                         ids=["integer-kernels", "unfused-square", "ntt-rs0", "u64-rows", "scaling-epilogue",
+                              "no-prescale"])
 def test_kernel_family_subprocess(env):
     """Kernel families the default dispatch does not pick for these shapes,
     each forced in a fresh process (the switches are read once per process):
