@@ -1,10 +1,13 @@
 #!/usr/bin/env python
 """Throughput of the homomorphic evaluation path on B200.
 
-Default workload: BASELINE.json configs[1] ("cfg2"), the MNIST-shaped
-Faster-CryptoNets network at N=8192 with 4 RNS limbs and t=65537 batching,
-one synthetic image per slot (8,192 images per pass).  A step is one
-`engine.eval_encrypted` pass over the encrypted batch.
+Default workload: BASELINE.json configs[2] ("cfg3"), the largest network
+configuration (CIFAR-shaped, N=16384, 6 RNS limbs, t=65537 batching, one
+synthetic image per slot: 16,384 images per pass); `--workload` selects
+cfg1/cfg2/cfg4 (the other network configs) or cfg5 (the primitive sweep:
+NTT fwd+inv, square + relinearisation with dnum=3 keys, the 1024-term sparse
+pow2 MAC over 4,096 ciphertexts).  A step is one `engine.eval_encrypted`
+pass over the encrypted batch (cfg5: one pass of the three primitives).
 
   value  -- encrypted images/s with the input ciphertexts resident in HBM
   e2e    -- the same through the public API with host (pinned) ciphertext
@@ -12,11 +15,16 @@ one synthetic image per slot (8,192 images per pass).  A step is one
             timed region
   roofline -- the batched NTT kernel (dominant kernel of the path), timed
             live with CUDA events, algorithmic bytes vs measured HBM copy BW
-  cpu_baseline -- the CPU oracle port (oracle/) timed on this host on a
-            bounded sample, extrapolated with the plan's HOP counts
+  keyswitch_roofline -- relinearisation (digit NTT + key MAC + INTT with
+            the add) with SURVEY 8(d)'s bytes 2.5 B P + keys, and square +
+            relinearisation end to end with 2 B P + keys
+  cpu_baseline -- the reference package itself (baseline/_ref, `hecnet`)
+            on one host core, on a bounded sample extrapolated with the
+            plan's HOP counts (refarm.py)
 
-`--impl reference` times the CPU oracle port (the reference's algorithm
-restated in numpy + Python big ints) with all host cores instead.
+`--impl reference` runs the reference (`hecnet` from baseline/_ref) on all
+host cores: a fork pool over each layer's independent outputs (the value),
+plus its as-shipped one-core loop and its own ThreadPool (refarm.py).
 
 Multi-GPU (torchrun, one rank per GPU): `--shard outputs` (default) splits
 every layer's outputs across ranks (strong scaling of one batch); with
@@ -49,14 +57,16 @@ def _args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["fcn", "reference"], default="fcn")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--workload", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--shard", choices=["outputs", "replicas"], default="outputs")
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of one CUDA graph per step")
     ap.add_argument("--force-sharded", action="store_true", help=argparse.SUPPRESS)
-    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the cpu_baseline sample")
+    ap.add_argument("--ref-mode-seconds", type=float, default=12.0,
+                    help="budget of each of the reference arm's one-core and ThreadPool samples")
     return ap.parse_args()
 
 
@@ -230,7 +240,7 @@ def _ntt_roofline(P, iters: int = 20):
 def _keyswitch_roofline(P, ek, count: int = 256, iters: int = 20):
     """Average duration of the key-switching inner product (fcn_key_mac) over
     `count` ciphertexts of NTT-domain digits (> L2): bytes = digits read +
-    accumulators written (keys excluded, SURVEY 8(d) convention)."""
+    accumulators written (keys excluded).  A sub-kernel figure."""
     import torch
 
     from paper_1811_09953_b200 import _lib
@@ -254,127 +264,124 @@ def _keyswitch_roofline(P, ek, count: int = 256, iters: int = 20):
     e1.record()
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / iters / 1e3
+    del dig, acc
     return {"count": count, "digits": D, "bytes": count * (D * k + 2 * k) * n * 8, "t_s": t}
+
+
+STAGES = ("lift", "forward_ntt_tensor", "tensor_intt", "rescale_digits", "digit_ntt", "key_mac", "final_intt_add")
+
+
+def _square_relin_stages(P, ek, count: int, iters: int = 3, act=(8, 131072)):
+    """Squares + relinearisation of `count` random ciphertexts (fcn_mul_ct_ex,
+    the activation epilogue of the workloads) with per-stage CUDA events
+    (fcn_stage_timing), averaged over `iters` calls after a warm-up."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1811_09953_b200 import _lib, fv
+
+    k, n = len(P.limb_primes), P.n
+    g = torch.Generator(device="cuda").manual_seed(2)
+    hi = min(P.limb_primes)
+    x = torch.randint(0, hi, (count, 2, k, n), device="cuda", dtype=torch.int64, generator=g)
+    out = torch.empty_like(x)
+    L = _lib.lib()
+    ws = fv.mul_ct_workspace(P, count)
+    fv.mul_ct_batch(P, ek, 0, x, out=out, workspace=ws, act=act)
+    torch.cuda.synchronize()
+    L.fcn_stage_timing(1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fv.mul_ct_batch(P, ek, 0, x, out=out, workspace=ws, act=act)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = (C.c_double * len(STAGES))()
+    _lib.check(L.fcn_stage_times(ms, len(STAGES)))
+    L.fcn_stage_timing(0)
+    total = e0.elapsed_time(e1) / iters / 1e3
+    stages = {name: ms[i] / iters / 1e3 for i, name in enumerate(STAGES)}
+    del x, out, ws
+    torch.cuda.empty_cache()
+    return total, stages
+
+
+def _keyswitch_objects(P, ek, peak, count: int):
+    """relinearisation bytes 2.5 B P + 2 dnum k n 8 over the digit
+    NTT + key MAC + INTT-with-add chain; square + relin 2 B P + keys over the
+    whole fcn_mul_ct_ex call.  Both chains are FP64-pipe bound,
+    so the fractions relate the in/out/key bytes to the time."""
+    k, n, D = len(P.limb_primes), P.n, P.ell + 1
+    Pb = 2 * k * n * 8
+    keys = 2 * D * k * n * 8
+    total, st = _square_relin_stages(P, ek, count)
+    t_ks = st["digit_ntt"] + st["key_mac"] + st["final_intt_add"]
+    ks_bytes = 2.5 * count * Pb + keys
+    sq_bytes = 2.0 * count * Pb + keys
+    keyswitch = {
+        "kernel": "relinearisation chain: ntt_f64_fwd (digits) + keymac_f64_kernel + ntt_f64_inv_epi",
+        "bound": "hbm",
+        "achieved": ks_bytes / t_ks / 1e9,
+        "peak": peak,
+        "unit": "GB/s",
+        "frac": ks_bytes / t_ks / 1e9 / peak,
+        "algorithmic_bytes": ks_bytes,
+        "formula": "2.5 B P + 2 dnum k n 8 (SURVEY 8(d))",
+        "ciphertexts": count,
+        "digits": D,
+        "ms": t_ks * 1e3,
+    }
+    square = {
+        "kernel": "square + relinearisation end to end (fcn_mul_ct_ex with the activation epilogue)",
+        "achieved": sq_bytes / total / 1e9,
+        "peak": peak,
+        "unit": "GB/s",
+        "frac": sq_bytes / total / 1e9 / peak,
+        "algorithmic_bytes": sq_bytes,
+        "formula": "2 B P + keys (SURVEY 8(d))",
+        "ciphertexts": count,
+        "ms": total * 1e3,
+        "ciphertexts_per_s": count / total,
+        "stage_ms": {name: v * 1e3 for name, v in st.items()},
+    }
+    return keyswitch, square
 
 
 # ----------------------------------------------------------------- CPU leg
 
 
-def _cpu_sample(workload: str, seconds: float, hops_tot, slots: int):
-    """Oracle (numpy + big-int) per-op times at the workload's ring shape on a
-    bounded sample, extrapolated by the plan's HOP counts to one pass."""
-    from oracle import bfv as ob
-    from oracle import rns as orn
-    from paper_1811_09953_b200 import configs
-
-    W = configs.WORKLOADS[workload]
-    OP = ob.Params(W.n, W.primes, (W.t,), W.beta)
-    K = ob.keygen(OP, configs.SEED_KEYS)
-    rng = np.random.default_rng(11)
-    cts = [ob.Ct(orn.random_uniform(W.primes, W.n, rng), orn.random_uniform(W.primes, W.n, rng)) for _ in range(4)]
-    t_end = time.perf_counter() + seconds * 0.7
-    n_mul, t0 = 0, time.perf_counter()
-    while n_mul < 2 or (time.perf_counter() < t_end and n_mul < 64):
-        ob.mul_ct(OP, cts[n_mul % 4], cts[n_mul % 4], K)
-        n_mul += 1
-    t_mul = (time.perf_counter() - t0) / n_mul
-    t_end = time.perf_counter() + seconds * 0.3
-    n_pt, t0 = 0, time.perf_counter()
-    acc = cts[0]
-    while n_pt < 8 or (time.perf_counter() < t_end and n_pt < 4096):
-        term = ob.mul_pt(OP, cts[n_pt % 4], [8], 0)
-        acc = ob.add_ct(OP, acc, term)
-        n_pt += 1
-    t_pair = (time.perf_counter() - t0) / n_pt
-    # add_pt at most once per output; cost ~ one add (bounded by the pair time)
-    t_pass = hops_tot.ct_ct_mul * t_mul + hops_tot.pt_ct_mul * t_pair + hops_tot.pt_ct_add * t_pair
-    sample = f"{n_mul} mul_ct + {n_pt} (mul_pt+add_ct) at n={W.n}, k={len(W.primes)}; extrapolated by HOP counts"
-    return slots / t_pass, t_pass, sample, {"t_mul_ct_s": t_mul, "t_mulpt_addct_s": t_pair}
-
-
-def _ref_worker(job):
-    kind, workload, count = job
-    from oracle import bfv as ob
-    from oracle import rns as orn
-    from paper_1811_09953_b200 import configs
-
-    st = _ref_worker.state
-    OP, K, cts = st
-    t0 = time.perf_counter()
-    if kind == "mul":
-        for i in range(count):
-            ob.mul_ct(OP, cts[i % len(cts)], cts[i % len(cts)], K)
-    else:
-        acc = cts[0]
-        for i in range(count):
-            acc = ob.add_ct(OP, acc, ob.mul_pt(OP, cts[i % len(cts)], [8], 0))
-    return time.perf_counter() - t0
-
-
-def _ref_init(workload):
-    from oracle import bfv as ob
-    from oracle import rns as orn
-    from paper_1811_09953_b200 import configs
-
-    W = configs.WORKLOADS[workload]
-    OP = ob.Params(W.n, W.primes, (W.t,), W.beta)
-    K = ob.keygen(OP, configs.SEED_KEYS)
-    rng = np.random.default_rng(11 + os.getpid() % 7)
-    cts = [ob.Ct(orn.random_uniform(W.primes, W.n, rng), orn.random_uniform(W.primes, W.n, rng)) for _ in range(2)]
-    _ref_worker.state = (OP, K, cts)
-
-
-def _host_cpu() -> dict:
-    """The host the CPU numbers ran on (count, physical cores, model)."""
-    info = {"os_cpu_count": os.cpu_count()}
-    try:
-        import psutil
-
-        info["physical_cores"] = psutil.cpu_count(logical=False)
-    except Exception:  # noqa: BLE001 - optional
-        pass
-    try:
-        with open("/proc/cpuinfo") as f:
-            for line in f:
-                if line.startswith("model name"):
-                    info["model"] = line.split(":", 1)[1].strip()
-                    break
-    except OSError:
-        pass
-    return info
-
-
 def run_reference(args, ws, rank):
-    """CPU oracle port on all host cores (multiprocessing over independent outputs)."""
+    """The reference package on this host's cores (refarm.py): the value is
+    mode (c), a fork pool over each layer's independent outputs; modes (a)
+    one core as shipped and (b) the shipped ThreadPool are reported beside it."""
     if rank != 0:
         return
-    import multiprocessing as mp
+    import refarm
 
-    from paper_1811_09953_b200 import configs, netplan
-
-    W = configs.WORKLOADS[args.workload]
-    comp = netplan.compile_network(configs.build_network(args.workload), W.fixed_point())
-    tot = netplan.plan_hops(comp, "batched", W.t).totals
+    if args.workload == "cfg5":
+        print(json.dumps({"impl": "reference", "unavailable": "cfg5 is a primitive sweep with no network pass; "
+                          "the reference arm times the network workloads cfg1-cfg4"}), flush=True)
+        return
     cores = os.cpu_count() or 1
-    ctx = mp.get_context("fork")
-    with ctx.Pool(cores, initializer=_ref_init, initargs=(args.workload,)) as pool:
-        def step():
-            t0 = time.perf_counter()
-            pool.map(_ref_worker, [("mul", args.workload, 1)] * cores)
-            t_mul = time.perf_counter() - t0
-            t0 = time.perf_counter()
-            pool.map(_ref_worker, [("pt", args.workload, 16)] * cores)
-            t_pt = time.perf_counter() - t0
-            # cores ops in t_mul; 16*cores pairs in t_pt
-            return tot.ct_ct_mul * t_mul / cores + (tot.pt_ct_mul + tot.pt_ct_add) * t_pt / (16 * cores)
-
+    st = refarm.RefState(args.workload)
+    pool = refarm.ProcessPool(st, cores)
+    try:
         for _ in range(args.warmup):
-            step()
+            pool.step()
         t0 = time.perf_counter()
-        passes = [step() for _ in range(args.steps)]
+        steps = [pool.step() for _ in range(args.steps)]
         wall = time.perf_counter() - t0
-    t_pass = float(np.mean(passes))
-    value = W.slots / t_pass
+    finally:
+        pool.close()
+    t_pass = float(np.mean([r["seconds_per_pass"] for r in steps]))
+    value = st.W.slots / t_pass
+    seq = refarm.sequential(st, args.ref_mode_seconds)
+    thr = refarm.threadpool(st, cores, args.ref_mode_seconds, seq["t_act_output_s"])
+    tot = st.hop_totals()
+    sample = (f"per step: {cores} activation outputs (mul_ct + mul_pt + mul_pt + add_ct) and {cores} x 32 linear taps "
+              f"(mul_pt + add_ct) over a {cores}-process fork pool, pass time extrapolated by the plan's HOP structure "
+              f"({tot.ct_ct_mul} ct_ct_mul, {tot.pt_ct_mul} pt_ct_mul)")
     line = {
         "impl": "reference",
         "metric": "encrypted images/sec",
@@ -388,18 +395,22 @@ def run_reference(args, ws, rank):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "u64",
-        "data": "synthetic (seeded uniform ciphertexts at the workload's ring shape)",
-        "config": _config(W, args.workload, ws, args.shard, tot,
-                          "inputs larger than L2 (%d MB of input ciphertexts per step)" % (784 * 2 * len(W.primes) * W.n * 8 >> 20)
-                          if args.workload in ("cfg1", "cfg2") else None),
+        "data": "synthetic (seeded uint8 images encrypted by the reference's own fv.encrypt; reference keygen)",
+        "config": _config(st.W, args.workload, ws, args.shard, tot),
         "cpu_baseline": {
             "value": value,
             "unit": "images/s",
             "cores": cores,
-            "kind": "port",
-            "host": _host_cpu(),
-            "sample": f"per step: {cores} mul_ct + {16 * cores} (mul_pt+add_ct) across a {cores}-process pool; "
-            f"pass time extrapolated by the plan's HOP counts ({tot.ct_ct_mul} ct_ct_mul, {tot.pt_ct_mul} pt_ct_mul)",
+            "kind": st.kind,
+            "host": refarm.host_cpu(),
+            "sample": sample,
+            "seconds_per_pass": t_pass,
+            "t_act_output_s": float(np.mean([r["t_act_output_s"] for r in steps])),
+            "t_tap_s": float(np.mean([r["t_tap_s"] for r in steps])),
+            "modes": {"workers1": seq, "threadpool": thr,
+                      "process_pool": {"images_per_s": value, "seconds_per_pass": t_pass, "cores": cores}},
+            "implementation": "hecnet (reference package, unmodified, baseline/_ref)" if st.kind == "reference"
+            else "oracle port (baseline/_ref missing)",
         },
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -612,30 +623,35 @@ def run_gpu(args, ws, rank, local):
                 "fp64_roofline.ceiling_frac_of_hbm is the register-resident butterfly ceiling as a fraction of HBM",
     }
     ks = _keyswitch_roofline(P, ek)
-    ks_ach = ks["bytes"] / ks["t_s"] / 1e9
-    keyswitch = {
-        "kernel": "keymac_f64_kernel (fcn_key_mac: sum_d key_d * digit_d, NTT domain)",
-        "bound": "hbm",
-        "achieved": ks_ach,
-        "peak": peak,
-        "unit": "GB/s",
-        "frac": ks_ach / peak,
-        "algorithmic_bytes_per_launch": ks["bytes"],
-        "ciphertexts_per_launch": ks["count"],
-        "digits": ks["digits"],
-        "ms": ks["t_s"] * 1e3,
-    }
+    keyswitch, square = _keyswitch_objects(P, ek, peak, 256 if P.n <= 8192 else 128)
+    keyswitch["inner_product_subkernel"] = {
+        "kernel": "keymac_f64_kernel alone (sum_d key_d * digit_d, NTT domain; bytes = digits + accumulators)",
+        "achieved": ks["bytes"] / ks["t_s"] / 1e9, "frac": ks["bytes"] / ks["t_s"] / 1e9 / peak,
+        "ciphertexts_per_launch": ks["count"], "ms": ks["t_s"] * 1e3}
     hops = engine.plan_hops(comp, "batched", W.t).totals
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
-        # cpu_baseline leg: the oracle also checks the decrypted timed output
+        # cpu_baseline leg: the reference package (baseline/_ref) on one host
+        # core; the oracle's plain mod-t model also checks the decrypted output
+        import refarm
         from oracle import drivers as od
 
         slots = engine.decrypt_tensor_slots(sk, out)
         check = bool(np.array_equal(slots, od.plain_model_batched(comp, x << cfg.precision_bits, W.t)))
-        v, t_pass, sample, per = _cpu_sample(args.workload, args.cpu_seconds, hops, W.slots)
-        cpu = {"value": v, "unit": "images/s", "cores": 1, "kind": "port", "sample": sample, "seconds_per_pass": t_pass,
-               "host": _host_cpu(), **per}
+        rst = refarm.RefState(args.workload)
+        seq = refarm.sequential(rst, args.cpu_seconds)
+        cpu = {"value": seq["images_per_s"], "unit": "images/s", "cores": 1, "kind": rst.kind,
+               "sample": seq["sample"] + "; pass time extrapolated by the plan's HOP structure",
+               "seconds_per_pass": seq["seconds_per_pass"], "host": refarm.host_cpu(),
+               "t_act_output_s": seq["t_act_output_s"], "t_mul_pt_s": seq["t_mul_pt_s"], "t_add_ct_s": seq["t_add_ct_s"],
+               "implementation": "hecnet (reference package, unmodified, baseline/_ref)" if rst.kind == "reference"
+               else "oracle port (baseline/_ref missing)"}
+    try:
+        import refarm
+
+        digest = refarm.output_digest(out.buf)
+    except Exception:  # noqa: BLE001 - informational
+        digest = None
     line = {
         "metric": "encrypted images/sec",
         "value": value,
@@ -660,7 +676,160 @@ def run_gpu(args, ws, rank, local):
         "decrypt_check": check,
         "roofline": roofline,
         "keyswitch_roofline": keyswitch,
+        "square_relin": square,
         "cpu_baseline": cpu,
+        "output_sha256": digest,
+        "e2e": e2e,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_sweep(args, ws, rank, local):
+    """cfg5: the primitive pass (NTT fwd+inv, square + relinearisation with
+    dnum = 3 keys, the 1024-term sparse pow2 MAC) over 4,096 uniform
+    ciphertexts, sharded over the ranks by ciphertext with one all-gather of
+    the squares before the MAC (paper_1811_09953_b200/sweep.py).
+    value = ciphertexts through the whole pass per second."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1811_09953_b200 import _lib, configs, dist as fdist, fv, sweep
+
+    torch.cuda.set_device(local)
+    _lib.load()
+    W = configs.WORKLOADS["cfg5"]
+    P = fv.EncryptionParams(W.n, W.primes, (W.t,), W.beta)
+    sk, pk, ek = fv.keygen(P, configs.SEED_KEYS)
+    B, terms = 4096, 1024
+    plan = configs.mac_sweep_plan(n_out=B, n_in=B, terms=terms, seed=1)
+    group = dist.group.WORLD if ws > 1 else None
+    pp = sweep.PrimitivePass(P, ek, plan, rank, ws, group)
+    x = sweep.uniform_batch(P, B, seed=0)
+    lo, hi = fdist.partition(B, ws)[rank]
+    x_local = x[lo:hi].contiguous()
+    del x
+    torch.cuda.empty_cache()
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    for _ in range(max(3, args.warmup)):
+        nt, sq, mac = pp.run(x_local)
+    torch.cuda.synchronize()
+    ntt_ok = bool(torch.equal(nt, x_local))
+    L = _lib.lib()
+    n0 = L.fcn_launch_count()
+    per_op = []
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            nt, sq, mac = pp.run(x_local)
+            e1.record()
+            e1.synchronize()
+            per_op.append(pp.times())
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+    launches = (L.fcn_launch_count() - n0) // args.steps
+    t_step = e0.elapsed_time(e1) / 1e3 / args.steps
+    if ws > 1:
+        tt = torch.tensor([t_step], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step = float(tt.item())
+    ops = {k: float(np.mean([d[k] for d in per_op])) for k in per_op[0]}
+    if ws > 1:
+        for k_ in list(ops):
+            tt = torch.tensor([ops[k_]], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ops[k_] = float(tt.item())
+    # e2e through the same API: the rank's block of ciphertexts from pinned
+    # host memory in, its MAC output rows out, every step
+    e2e = None
+    if not args.no_e2e:
+        host_in = x_local.cpu().pin_memory()
+        host_out = torch.empty(mac.shape, dtype=torch.int64, pin_memory=True)
+        dev_in = torch.empty_like(x_local)
+        barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_e2e = max(1, min(args.steps, 5))
+        s0.record()
+        for _ in range(n_e2e):
+            dev_in.copy_(host_in, non_blocking=True)
+            _, _, m = pp.run(dev_in)
+            host_out.copy_(m, non_blocking=True)
+        s1.record()
+        torch.cuda.synchronize()
+        barrier()
+        t_e2e = s0.elapsed_time(s1) / 1e3 / n_e2e
+        if ws > 1:
+            tt = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        e2e = {"value": B / t_e2e, "unit": "ciphertexts/s", "h2d_bytes_per_step": host_in.numel() * 8,
+               "d2h_bytes_per_step": host_out.numel() * 8, "ms_per_step": t_e2e * 1e3, "batches": n_e2e,
+               "api": "sweep.PrimitivePass.run (pinned host block in, host MAC rows out)"}
+        del host_in, host_out, dev_in
+    if rank != 0:
+        return
+    peak, _ = _peaks()
+    k, n = len(W.primes), W.n
+    Pb = 2 * k * n * 8
+    b_loc = hi - lo
+    keys = 2 * (P.ell + 1) * k * n * 8
+    fp = _fp64_peak()
+    h = P.native()
+    rs = L.fcn_ntt_f64_schedule(n.bit_length() - 1, max(tuple(W.primes)))
+    bfly = 2 * (2 * b_loc * k) * (n // 2) * (n.bit_length() - 1)
+    pk_b = (fp.get("butterfly_rs1_per_s", fp["butterfly_per_s"]) if rs >= 1 else fp["butterfly_per_s"]) if fp else None
+    o_loc = fdist.partition(B, ws)[0][1]
+    term_coeffs = o_loc * terms * 2 * k * n
+    per_op_roof = {
+        "ntt_fwd_inv": {"ms": ops["ntt_fwd_inv_s"] * 1e3, "bytes": 4 * b_loc * Pb,
+                        "achieved_gbs": 4 * b_loc * Pb / ops["ntt_fwd_inv_s"] / 1e9,
+                        "frac": 4 * b_loc * Pb / ops["ntt_fwd_inv_s"] / 1e9 / peak,
+                        "frac_fp64_butterfly_peak": (bfly / ops["ntt_fwd_inv_s"] / pk_b) if pk_b else None},
+        "square_relin": {"ms": ops["square_relin_s"] * 1e3, "bytes": 2 * b_loc * Pb + keys,
+                         "achieved_gbs": (2 * b_loc * Pb + keys) / ops["square_relin_s"] / 1e9,
+                         "frac": (2 * b_loc * Pb + keys) / ops["square_relin_s"] / 1e9 / peak,
+                         "ciphertexts_per_s": b_loc / ops["square_relin_s"]},
+        "mac_1024_terms": {"ms": ops["mac_s"] * 1e3, "bytes": (B + o_loc) * Pb,
+                           "achieved_gbs": (B + o_loc) * Pb / ops["mac_s"] / 1e9,
+                           "frac": (B + o_loc) * Pb / ops["mac_s"] / 1e9 / peak,
+                           "term_coeffs_per_s": term_coeffs / ops["mac_s"]},
+        "allgather": {"ms": ops["allgather_s"] * 1e3, "bytes_per_rank": (B - b_loc) * Pb},
+    }
+    ks, square = _keyswitch_objects(P, ek, peak, 128)
+    line = {
+        "metric": "cfg5 primitive pass (NTT fwd+inv, square+relin dnum=3, 1024-term MAC)",
+        "value": B / t_step,
+        "unit": "ciphertexts/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": max(3, args.warmup),
+        "ms_per_step": t_step * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "u64",
+        "data": "synthetic (4,096 seeded uniform ciphertexts; MAC plan seed 1)",
+        "config": {"workload": "cfg5", "n": n, "limbs": k, "t": W.t, "beta_log2": 134, "dnum": P.ell + 1,
+                   "ciphertexts": B, "mac_terms": terms, "parallelism": f"ciphertext-shard{ws}" if ws > 1 else "single",
+                   "l2": "inputs larger than L2 (%d MB of ciphertexts per rank)" % (b_loc * Pb >> 20)},
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+        "ntt_roundtrip_identity": ntt_ok,
+        "per_op": per_op_roof,
+        "roofline": dict(per_op_roof["ntt_fwd_inv"], kernel="ntt_f64_fwd / ntt_f64_inv", bound="hbm",
+                         achieved=per_op_roof["ntt_fwd_inv"]["achieved_gbs"], peak=peak, unit="GB/s",
+                         traffic=_profile_traffic("ntt_cfg5")),
+        "keyswitch_roofline": ks,
+        "square_relin": square,
+        "cpu_baseline": None,
         "e2e": e2e,
     }
     print(json.dumps(line), flush=True)
@@ -677,9 +846,19 @@ def main():
         backend = "gloo" if args.impl == "reference" else "nccl"
         if backend == "nccl":
             torch.cuda.set_device(local)
+            # NCCL's own init log (nranks / transport per rank) on stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group(backend)
+        if backend == "nccl":
+            probe = torch.ones(1, device="cuda")
+            dist.all_reduce(probe)  # creates the communicator now
+            print(f"[bench] rank {rank}/{ws} local {local} nccl communicator nranks={int(probe.item())} "
+                  f"device={torch.cuda.get_device_name(local)}", file=sys.stderr, flush=True)
     if args.impl == "reference":
         run_reference(args, ws, rank)
+    elif args.workload == "cfg5":
+        run_sweep(args, ws, rank, local)
     else:
         run_gpu(args, ws, rank, local)
     if group:

@@ -45,6 +45,16 @@ const char* fcn_last_error(void);
 int fcn_version(void);
 /* Number of kernels this library has launched in the process (bench evidence). */
 long long fcn_launch_count(void);
+/* Per-stage CUDA-event timing of fcn_mul_ct_ex / fcn_mul_ct_multi (bench and
+ * profiling aid; no reference counterpart).  fcn_stage_timing(1) clears the
+ * record and starts recording events around every stage of every chunk on
+ * the call's stream (skipped while a stream is being captured);
+ * fcn_stage_timing(0) clears and stops.  fcn_stage_times synchronises the
+ * recorded events and writes the summed milliseconds per stage id:
+ * 0 lift, 1 forward NTT (+ fused tensor), 2 tensor INTT, 3 exact rescale +
+ * digits, 4 digit NTT, 5 key MAC, 6 final INTT + epilogue.                 */
+int fcn_stage_timing(int enable);
+int fcn_stage_times(double* ms_out, int n_stages);
 /* Reduction schedule the FP64 NTT uses for a transform of size 2^logn whose
  * largest limb is qmax: 0 = reduce every third stage (any q < 2^51), 1 = once
  * per transform, 2 = never (host-only diagnostic; no reference counterpart). */
@@ -103,15 +113,25 @@ int fcn_poly_mul_monomial(const fcn_ring* ring, const uint64_t* d_a, int k, cons
 
 /* EncryptionParams (fv.py:42-124): q-limbs, plaintext lanes, beta = 2^log2_beta.
  * Derives ell (fv.py:78-85), Delta = q // t (fv.py:87-88), the auxiliary
- * base via find_ntt_primes(n, (bitlen(n)+bitlen(q)+1)//54+1, 55, exclude=q)
- * (fv.py:99-107) and all exact-rescale constants.  */
+ * base and all exact-rescale constants.  The
+ * reference's auxiliary base is find_ntt_primes(n, (bitlen(n)+bitlen(q)+1)
+ * //54+1, 55, exclude=q) (fv.py:99-107); the result of mul_ct does not depend
+ * on which base extends q as long as its product P exceeds 2nq, so the
+ * context instead takes the first NTT primes in (2^50, 2^51) (ascending
+ * scan, q-limbs excluded) with the smallest count giving P >= 8nq -- limbs
+ * below 2^51 keep every mul_ct kernel on the exact FP64 path (csrc/fv.cu,
+ * fcn_ctx_create).  When a q-limb is >= 2^51 the integer kernels run instead;
+ * a set for which (2^50, 2^51) holds too few NTT primes is rejected with
+ * FCN_ERR_PARAM.  fcn_ctx_aux_primes returns the base.                      */
 int fcn_ctx_create(int device, int n, int k, const uint64_t* primes, int n_lanes,
                    const uint64_t* t_lanes, int log2_beta, fcn_ctx** out);
 int fcn_ctx_destroy(fcn_ctx* ctx);
 /* The ring over the extended base (q-limbs first, then aux): q-base ops
  * use it with limb_period = k, limb_offset = 0.                          */
 int fcn_ctx_ring(const fcn_ctx* ctx, const fcn_ring** out);
-/* what: 0 n, 1 k, 2 aux count m, 3 ell, 4 n_lanes, 5 log2_beta.          */
+/* what: 0 n, 1 k, 2 aux count m, 3 ell, 4 n_lanes, 5 log2_beta,
+ * 6 whether mul_ct's lift/rescale run the exact-size FP64 kernels (1) or
+ * the integer ones (0; a one-line notice goes to stderr at creation).    */
 int fcn_ctx_query(const fcn_ctx* ctx, int what, int64_t* value);
 int fcn_ctx_aux_primes(const fcn_ctx* ctx, uint64_t* out_m);
 

@@ -256,6 +256,20 @@ def _rescale(P: Params, tpoly: np.ndarray, t: int) -> list[int]:
     return out
 
 
+_KEY_NTT: dict = {}
+
+
+def _key_ntt(P: Params, keys: Keys):
+    """NTT-domain eval keys, computed once per key set like the reference's
+    cached `EvalKeys.g_ntt/a_ntt` (fv.py:192-198, used at :534-535)."""
+    hit = _KEY_NTT.get(id(keys))
+    if hit is None or hit[0] is not keys:
+        hit = (keys, [rns.ntt(g, P.primes) for g in keys.g], [rns.ntt(a, P.primes) for a in keys.a])
+        _KEY_NTT.clear()
+        _KEY_NTT[id(keys)] = hit
+    return hit[1], hit[2]
+
+
 def mul_ct(P: Params, a: Ct, b: Ct, keys: Keys) -> Ct:
     """Tensor -> exact rescale -> base-beta relinearization (fv.py:498-549)."""
     if a.lane != b.lane:
@@ -279,8 +293,9 @@ def mul_ct(P: Params, a: Ct, b: Ct, keys: Keys) -> Ct:
         if not any(d):
             continue
         dn = rns.ntt(ints_to_poly(d, pr), pr)
-        g_t = rns.pmul(rns.ntt(keys.g[i], pr), dn, pr)
-        a_t = rns.pmul(rns.ntt(keys.a[i], pr), dn, pr)
+        g_ntt, a_ntt = _key_ntt(P, keys)
+        g_t = rns.pmul(g_ntt[i], dn, pr)
+        a_t = rns.pmul(a_ntt[i], dn, pr)
         acc0 = g_t if acc0 is None else rns.padd(acc0, g_t, pr)
         acc1 = a_t if acc1 is None else rns.padd(acc1, a_t, pr)
     if acc0 is not None:

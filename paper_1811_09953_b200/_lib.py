@@ -44,6 +44,8 @@ SIGNATURES = {
     "fcn_last_error": (C.c_char_p, []),
     "fcn_version": (_I, []),
     "fcn_launch_count": (C.c_longlong, []),
+    "fcn_stage_timing": (_I, [_I]),
+    "fcn_stage_times": (_I, [C.POINTER(C.c_double), _I]),
     "fcn_ntt_f64_schedule": (_I, [_I, C.c_uint64]),
     "fcn_ring_create": (_I, [_I, _I, _I, _U64P, C.POINTER(_P)]),
     "fcn_ring_destroy": (_I, [_P]),

@@ -31,6 +31,14 @@ extern std::atomic<long long> g_launches;  // kernels launched by this library
     ::fcn::g_launches.fetch_add(1, std::memory_order_relaxed); \
   } while (0)
 
+// Per-device kernel setup (dynamic shared-memory attribute + resident CTAs
+// per SM), cached per (kernel, device, smem) under a lock: the attribute is a
+// per-device property, so one process driving several devices sets it on
+// each (csrc/ring.cu).  Returns the CUDA error of the setup.
+cudaError_t kernel_occupancy(const void* fn, int threads, size_t smem, int* occ_out);
+// SM count of the current device (cached per device).
+int device_sms();
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {

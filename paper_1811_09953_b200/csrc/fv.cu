@@ -18,6 +18,8 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "bigint.hpp"
 #include <cstdlib>
@@ -1381,6 +1383,8 @@ using namespace fcn;
 
 // ----------------------------------------------------------------- C ABI
 
+static bool f64_lift_rescale(const fcn_ctx* x);
+
 extern "C" int fcn_ctx_create(int device, int n, int k, const uint64_t* primes, int n_lanes, const uint64_t* t_lanes,
                               int log2_beta, fcn_ctx** out) {
   if (!out || !primes || !t_lanes || k <= 0 || n_lanes <= 0) return set_error(FCN_ERR_ARG, "bad context arguments");
@@ -1457,6 +1461,11 @@ extern "C" int fcn_ctx_create(int device, int n, int k, const uint64_t* primes, 
     const char* ev = getenv("FCN_NTT_INT");  // A/B switch: integer kernels only
     x->fp = x->ext->fp_ok && !(ev && ev[0] == '1');
   }
+  if (x->fp && !f64_lift_rescale(x) && !getenv("FCN_QUIET"))
+    fprintf(stderr,
+            "[libfcn] k=%d q-limbs + m=%d auxiliary limbs has no exact-size FP64 lift/rescale instantiation "
+            "(csrc/fv.cu lift_or_rescale): mul_ct runs the integer lift/rescale kernels\n",
+            k, x->m);
   std::vector<MulCtConst> host(n_lanes);
   for (int l = 0; l < n_lanes; ++l) {
     rc = build_mulct_const(x, x->lanes[l], &host[l]);
@@ -1528,6 +1537,7 @@ extern "C" int fcn_ctx_query(const fcn_ctx* x, int what, int64_t* value) {
     case 3: *value = x->ell; break;
     case 4: *value = x->n_lanes; break;
     case 5: *value = x->log2_beta; break;
+    case 6: *value = f64_lift_rescale(x) ? 1 : 0; break;
     default: return set_error(FCN_ERR_ARG, "unknown query %d", what);
   }
   return FCN_OK;
@@ -1893,11 +1903,10 @@ static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_
     const int64_t total = (cnt * 3) << x->logn;  // cnt = ciphertexts
     if (f64) {
       const int smem = 2 * (KE + KQ) * 256 * 8;
-      static std::once_flag once;
-      std::call_once(once, [&] {
-        cudaFuncSetAttribute(rescale_f64_kernel<KQ, KE, KQ + 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(rescale_f64_kernel<KQ, KE, KQ + 2, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      });
+      int occ = 0;
+      const void* fn = f64_product_period(x) == 12 ? (const void*)rescale_f64_kernel<KQ, KE, KQ + 2, 12>
+                                                    : (const void*)rescale_f64_kernel<KQ, KE, KQ + 2>;
+      FCN_CUDA(kernel_occupancy(fn, 256, smem, &occ));  // per-device smem attribute
       if (f64_product_period(x) == 12)
         rescale_f64_kernel<KQ, KE, KQ + 2, 12><<<grid_for(total, 256), 256, smem, st>>>(
             in, R01, DG, cnt, x->logn, P, dmc, x->d_fallbacks, act ? act->lin : nullptr);
@@ -1989,7 +1998,9 @@ static const double2* c2_twist(fcn_ctx* x, int64_t c2, cudaStream_t st) {
     cudaGetLastError();
     return nullptr;
   }
-  if (cudaMemcpy(d, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+  // ordered on the caller's stream and complete before the host table goes away
+  if (cudaMemcpyAsync(d, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
     cudaFree(d);
     cudaGetLastError();
     return nullptr;
@@ -2068,6 +2079,71 @@ static int launch_keymac(const uint64_t* DG, const fcn_keys* keys, uint64_t* ACC
   return FCN_OK;
 }
 
+// ---- per-stage CUDA-event timing of fcn_mul_ct_multi (fcn_stage_timing):
+// stage ids 0 lift, 1 forward NTT (+ fused tensor), 2 tensor INTT, 3 exact
+// rescale + digits, 4 digit NTT, 5 key MAC, 6 final INTT + epilogue.
+namespace {
+struct StageTimer {
+  std::mutex mu;
+  bool on = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> recs;
+};
+StageTimer& stage_timer() {
+  static StageTimer t;
+  return t;
+}
+struct StageScope {
+  cudaStream_t st;
+  int id;
+  cudaEvent_t e1 = nullptr;
+  StageScope(int id_, cudaStream_t s) : st(s), id(id_) {
+    StageTimer& T = stage_timer();
+    if (!T.on) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    cudaEvent_t e0;
+    if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+      cudaGetLastError();
+      e1 = nullptr;
+      return;
+    }
+    cudaEventRecord(e0, st);
+    std::lock_guard<std::mutex> lk(T.mu);
+    T.recs.push_back({id, {e0, e1}});
+  }
+  ~StageScope() {
+    if (e1) cudaEventRecord(e1, st);
+  }
+};
+}  // namespace
+
+extern "C" int fcn_stage_timing(int enable) {
+  StageTimer& T = stage_timer();
+  std::lock_guard<std::mutex> lk(T.mu);
+  for (auto& r : T.recs) {
+    cudaEventDestroy(r.second.first);
+    cudaEventDestroy(r.second.second);
+  }
+  T.recs.clear();
+  T.on = enable != 0;
+  return FCN_OK;
+}
+
+extern "C" int fcn_stage_times(double* ms_out, int n_stages) {
+  if (!ms_out || n_stages < 1) return set_error(FCN_ERR_ARG, "null output");
+  for (int i = 0; i < n_stages; ++i) ms_out[i] = 0.0;
+  StageTimer& T = stage_timer();
+  std::lock_guard<std::mutex> lk(T.mu);
+  for (auto& r : T.recs) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(r.second.second) != cudaSuccess ||
+        cudaEventElapsedTime(&ms, r.second.first, r.second.second) != cudaSuccess)
+      return set_error(FCN_ERR_CUDA, "stage event query failed: %s", cudaGetErrorString(cudaGetLastError()));
+    if (r.first >= 0 && r.first < n_stages) ms_out[r.first] += ms;
+  }
+  return FCN_OK;
+}
+
 extern "C" int fcn_mul_ct(const fcn_ctx* x, const fcn_keys* keys, int lane, const uint64_t* d_a, const uint64_t* d_b,
                           uint64_t* d_out, int64_t count, void* d_workspace, size_t workspace_bytes, void* stream) {
   return fcn_mul_ct_ex(x, keys, lane, d_a, d_b, d_out, count, 0, 1, 0, d_workspace, workspace_bytes, stream);
@@ -2138,8 +2214,13 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
     const bool want_dbl = fused && prescale && dbl_rows(x);
     if (fused) {
       int lift_mode = want_dbl ? 2 : 1;  // compact lift; 2: auxiliary rows as signed doubles
-      int rc = lift_or_rescale(true, x, lane, a, EA, C * 2, nullptr, nullptr, st, nullptr, &fused, &lift_mode);
+      int rc;
+      {
+        StageScope ss(0, st);
+        rc = lift_or_rescale(true, x, lane, a, EA, C * 2, nullptr, nullptr, st, nullptr, &fused, &lift_mode);
+      }
       if (rc) return rc;
+      StageScope ss(1, st);
       if (fused) {
         rc = launch_ntt_square_tensor(x->ext, a, EA, T, C, k, x->m, st, want_dbl);
         if (rc) return rc < 0 ? rc : set_error(FCN_ERR_STATE, "fused square tensor unavailable");
@@ -2150,13 +2231,19 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
     } else {
       for (int which = 0; which < (b ? 2 : 1); ++which) {
         uint64_t* dst = which ? EB : EA;
-        int rc = lift_or_rescale(true, x, lane, which ? b : a, dst, C * 2, nullptr, nullptr, st);
+        int rc;
+        {
+          StageScope ss(0, st);
+          rc = lift_or_rescale(true, x, lane, which ? b : a, dst, C * 2, nullptr, nullptr, st);
+        }
         if (rc) return rc;
+        StageScope ss(1, st);
         rc = launch_ntt(x->ext, dst, C * 2 * K, K, 0, true, st);
         if (rc) return rc;
       }
     }
     if (!fused) {
+      StageScope ss(1, st);
       if (x->fp)
         tensor_f64_kernel<<<grid_for((C * K) << (logn - 1), 256), 256, 0, st>>>(EA, b ? EB : nullptr, T, C, K, logn,
                                                                                 x->ext->d_lc);
@@ -2171,7 +2258,11 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
     tw_epi.mode = 0;
     tw_epi.ftwist = x->d_ftwist_binv;
     tw_epi.dbl = dbl;
-    int rc = launch_ntt(x->ext, T, C * 3 * K, K, 0, false, st, nullptr, 1, prescale ? &tw_epi : nullptr);
+    int rc;
+    {
+      StageScope ss(2, st);
+      rc = launch_ntt(x->ext, T, C * 3 * K, K, 0, false, st, nullptr, 1, prescale ? &tw_epi : nullptr);
+    }
     if (rc) return rc;
     // (iv) exact rescale + digit decomposition (FP64: R01 <- c2 R01 + c1 a for the activation)
     ActArgs aa;
@@ -2181,7 +2272,10 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
     aa.lin = a;
     aa.prescaled = prescale;
     aa.dbl_in = dbl;
-    rc = lift_or_rescale(false, x, lane, T, nullptr, C, R01, direct ? DGR : DGN, st, &aa);
+    {
+      StageScope ss(3, st);
+      rc = lift_or_rescale(false, x, lane, T, nullptr, C, R01, direct ? DGR : DGN, st, &aa);
+    }
     if (rc) return rc;
     epi.mode = !act ? 1 : (aa.applied ? 3 : 2);
     epi.ftwist = nullptr;
@@ -2195,12 +2289,18 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
     // (v) digits to NTT (broadcast rows when digits are limb-independent), key MAC
     NttEpi dg_epi;
     dg_epi.dbl = dbl;
-    if (direct)
-      rc = launch_ntt(x->ext, DGN, C * D * k, k, 0, true, st, DGR, k, dbl ? &dg_epi : nullptr);
-    else
-      rc = launch_ntt(x->ext, DGN, C * D * k, k, 0, true, st, nullptr, 1, dbl ? &dg_epi : nullptr);
+    {
+      StageScope ss(4, st);
+      if (direct)
+        rc = launch_ntt(x->ext, DGN, C * D * k, k, 0, true, st, DGR, k, dbl ? &dg_epi : nullptr);
+      else
+        rc = launch_ntt(x->ext, DGN, C * D * k, k, 0, true, st, nullptr, 1, dbl ? &dg_epi : nullptr);
+    }
     if (rc) return rc;
-    rc = launch_keymac(DGN, keys, ACC, C, D, k, x, st, dbl);
+    {
+      StageScope ss(5, st);
+      rc = launch_keymac(DGN, keys, ACC, C, D, k, x, st, dbl);
+    }
     if (rc) return rc;
     // (vi) inverse NTT with the fused epilogue: out = R01 + INTT(ACC)
     //      [ * c2 + c1 * a  when FCN_MUL_ACT: the a2 x^2 + a1 x activation]
@@ -2209,7 +2309,10 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
     epi.dbl = dbl;
     epi.out.n = n_dst;
     for (int d = 0; d < n_dst; ++d) epi.out.dst[d] = d_outs[d] + off * ct_words;
-    rc = launch_ntt(x->ext, ACC, C * 2 * k, k, 0, false, st, nullptr, 1, &epi);
+    {
+      StageScope ss(6, st);
+      rc = launch_ntt(x->ext, ACC, C * 2 * k, k, 0, false, st, nullptr, 1, &epi);
+    }
     if (rc) return rc;
   }
   return FCN_OK;

@@ -492,50 +492,22 @@ __global__ void ntt_epi_kernel(const uint64_t* __restrict__ data, int64_t n_rows
 static size_t v1_smem(int logs) { return (size_t)((1 << logs) + (1 << logs) / 32 + 2) * sizeof(uint64_t); }
 static size_t v2_smem(int logn) { return (size_t)((1 << logn) + (1 << logn) / 32 + 2) * sizeof(uint64_t); }
 
-struct V2Entry {
-  const void* fn;
-  int ctas_per_sm;
-};
-
 template <int LOGN, bool FWD>
 static const void* v2_ptr() {
   return FWD ? (const void*)ntt_v2_fwd<LOGN> : (const void*)ntt_v2_inv<LOGN>;
 }
-static int g_sms = 0;
-static V2Entry g_v2[2][15];
-static std::once_flag g_init;
-static cudaError_t g_init_err = cudaSuccess;
 
-static void init_tables() {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-  const void* fns[2][15] = {};
-  fns[1][10] = v2_ptr<10, true>();
-  fns[1][11] = v2_ptr<11, true>();
-  fns[1][12] = v2_ptr<12, true>();
-  fns[1][13] = v2_ptr<13, true>();
-  fns[1][14] = v2_ptr<14, true>();
-  fns[0][10] = v2_ptr<10, false>();
-  fns[0][11] = v2_ptr<11, false>();
-  fns[0][12] = v2_ptr<12, false>();
-  fns[0][13] = v2_ptr<13, false>();
-  fns[0][14] = v2_ptr<14, false>();
-  for (int f = 0; f < 2; ++f) {
-    for (int lg = 10; lg <= 14; ++lg) {
-      const size_t sm = v2_smem(lg);
-      cudaError_t e = cudaFuncSetAttribute(fns[f][lg], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      int occ = 0;
-      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fns[f][lg], (1 << lg) / 32, sm);
-      if (e != cudaSuccess) g_init_err = e;
-      g_v2[f][lg] = {fns[f][lg], occ > 0 ? occ : 1};
-    }
+// Resident CTAs per SM of the integer NTT kernel for 2^logn (per-device setup).
+static cudaError_t v2_occupancy(bool fwd, int logn, int* occ) {
+  const void* fn = nullptr;
+  switch (logn) {
+    case 10: fn = fwd ? v2_ptr<10, true>() : v2_ptr<10, false>(); break;
+    case 11: fn = fwd ? v2_ptr<11, true>() : v2_ptr<11, false>(); break;
+    case 12: fn = fwd ? v2_ptr<12, true>() : v2_ptr<12, false>(); break;
+    case 13: fn = fwd ? v2_ptr<13, true>() : v2_ptr<13, false>(); break;
+    default: fn = fwd ? v2_ptr<14, true>() : v2_ptr<14, false>(); break;
   }
-  const size_t mx = v1_smem(14);
-  cudaError_t e1 = cudaFuncSetAttribute(ntt_v1_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
-  cudaError_t e2 = cudaFuncSetAttribute(ntt_v1_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
-  if (e1 != cudaSuccess) g_init_err = e1;
-  if (e2 != cudaSuccess) g_init_err = e2;
+  return kernel_occupancy(fn, (1 << logn) / 32, v2_smem(logn), occ);
 }
 
 static int launch_v1(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st,
@@ -547,7 +519,12 @@ static int launch_v1(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period,
   threads = threads < 32 ? 32 : (threads > 512 ? 512 : threads);
   const size_t smem = v1_smem(logs);
   int64_t grid = segs;
-  const int64_t cap = (int64_t)(g_sms ? g_sms : 148) * 64;
+  const int64_t cap = (int64_t)device_sms() * 64;
+  {
+    int occ = 0;  // per-device dynamic smem attribute
+    FCN_CUDA(kernel_occupancy(fwd ? (const void*)ntt_v1_kernel<true> : (const void*)ntt_v1_kernel<false>, threads,
+                              smem, &occ));
+  }
   if (grid > cap) grid = cap;
   if (fwd) {
     if (logs < logn) {
@@ -665,9 +642,8 @@ int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int o
     src_div = 1;
   }
   if (!fwd && src != d) return set_error(FCN_ERR_ARG, "out-of-place inverse NTT is not supported");
-  std::call_once(g_init, init_tables);
-  if (g_init_err != cudaSuccess) return check_cuda(g_init_err, "ntt init");
   const int logn = r->logn;
+  const int sms = device_sms();
   const int family = ntt_family(r, period, offset);
   if (epi && epi->ftwist && (family != 2 || epi->mode == 2 || fwd))
     return set_error(FCN_ERR_STATE, "a replacement twist needs an FP64 inverse (epilogue mode 0, 1 or 3)");
@@ -686,13 +662,14 @@ int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int o
     uint64_t qmax = 0;
     for (int l = 0; l < period; ++l) qmax = r->primes[offset + l] > qmax ? r->primes[offset + l] : qmax;
     switch (f64_schedule(logn, qmax)) {
-      case 2: return launch_ntt_f64<2>(r, d, n_rows, period, offset, fwd, st, src, src_div, epi, g_sms);
-      case 1: return launch_ntt_f64<1>(r, d, n_rows, period, offset, fwd, st, src, src_div, epi, g_sms);
-      default: return launch_ntt_f64<0>(r, d, n_rows, period, offset, fwd, st, src, src_div, epi, g_sms);
+      case 2: return launch_ntt_f64<2>(r, d, n_rows, period, offset, fwd, st, src, src_div, epi, sms);
+      case 1: return launch_ntt_f64<1>(r, d, n_rows, period, offset, fwd, st, src, src_div, epi, sms);
+      default: return launch_ntt_f64<0>(r, d, n_rows, period, offset, fwd, st, src, src_div, epi, sms);
     }
   }
-  const V2Entry& e = g_v2[fwd ? 1 : 0][logn];
-  int64_t grid = (int64_t)g_sms * e.ctas_per_sm;
+  int occ = 1;
+  FCN_CUDA(v2_occupancy(fwd, logn, &occ));
+  int64_t grid = (int64_t)sms * occ;
   if (grid > n_rows) grid = n_rows;
   switch (logn) {
     case 10: launch_v2_t<10>(fwd, (int)grid, d, n_rows, period, offset, r, st, src, src_div); break;
@@ -714,13 +691,12 @@ int launch_ntt_square_tensor(const fcn_ring* r, const uint64_t* a, const uint64_
     if (r->primes[l] >= (1ull << 51)) return 1;
     qmax = r->primes[l] > qmax ? r->primes[l] : qmax;
   }
-  std::call_once(g_init, init_tables);
-  if (g_init_err != cudaSuccess) return check_cuda(g_init_err, "ntt init");
+  const int sms = device_sms();
   const int64_t units = C * (k + m);
   switch (f64_schedule(r->logn, qmax)) {
-    case 2: return launch_ntt_f64_sq<2>(r, a, aux, Tout, units, k, m, st, g_sms, dbl);
-    case 1: return launch_ntt_f64_sq<1>(r, a, aux, Tout, units, k, m, st, g_sms, dbl);
-    default: return launch_ntt_f64_sq<0>(r, a, aux, Tout, units, k, m, st, g_sms, dbl);
+    case 2: return launch_ntt_f64_sq<2>(r, a, aux, Tout, units, k, m, st, sms, dbl);
+    case 1: return launch_ntt_f64_sq<1>(r, a, aux, Tout, units, k, m, st, sms, dbl);
+    default: return launch_ntt_f64_sq<0>(r, a, aux, Tout, units, k, m, st, sms, dbl);
   }
 }
 

@@ -497,19 +497,12 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 
 // ============================================================== dispatch
 
-// Resident CTAs per SM of one kernel (dynamic smem attribute set once).
+// Resident CTAs per SM of one kernel (dynamic smem attribute set per device).
 template <int LOGN, int RS, int V>
 struct F64Occ {
   static int get(const void* fn, size_t smem, cudaError_t* err) {
-    static cudaError_t e0 = cudaSuccess;
-    static const int occ = [&] {
-      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      int o = 0;
-      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, (1 << LOGN) / 32, smem);
-      e0 = e;
-      return o > 0 ? o : 1;
-    }();
-    *err = e0;
+    int occ = 1;
+    *err = kernel_occupancy(fn, (1 << LOGN) / 32, smem, &occ);
     return occ;
   }
 };

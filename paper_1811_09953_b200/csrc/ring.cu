@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 
@@ -35,6 +36,57 @@ int set_error(int code, const char* fmt, ...) {
   va_end(ap);
   g_last_error = buf;
   return code;
+}
+
+cudaError_t kernel_occupancy(const void* fn, int threads, size_t smem, int* occ_out) {
+  struct Key {
+    const void* fn;
+    int dev, threads;
+    size_t smem;
+    bool operator<(const Key& o) const {
+      if (fn != o.fn) return fn < o.fn;
+      if (dev != o.dev) return dev < o.dev;
+      if (threads != o.threads) return threads < o.threads;
+      return smem < o.smem;
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, int> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const Key key{fn, dev, threads, smem};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *occ_out = it->second;
+      return cudaSuccess;
+    }
+  }
+  if (smem > 48 * 1024) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 0;
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
+  if (e != cudaSuccess) return e;
+  if (occ < 1) occ = 1;
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = occ;
+  *occ_out = occ;
+  return cudaSuccess;
+}
+
+int device_sms() {
+  static std::mutex mu;
+  static std::map<int, int> sms;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = sms.find(dev);
+  if (it != sms.end()) return it->second;
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v < 1) v = 148;
+  sms[dev] = v;
+  return v;
 }
 
 int check_cuda(cudaError_t e, const char* what) {

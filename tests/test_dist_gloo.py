@@ -173,3 +173,110 @@ def test_upload_sharded_reassembles_the_batch(world):
         p.join(timeout=120)
         assert p.exitcode == 0
     assert all(ok for _, _, ok in res), res
+
+
+# ---------------------------------------------------------------- cfg5 split
+
+
+def _sweep_setup():
+    """A miniature cfg5: uniform ciphertexts at n=1024 over 3 limbs, a
+    dnum-style large beta, and a sparse pow2 MAC plan (configs.mac_sweep_plan)."""
+    from oracle import bfv as ob
+    from oracle import nt
+    from oracle import rns as orn
+    from paper_1811_09953_b200 import configs
+
+    n = 1024
+    primes = tuple(nt.ntt_primes(n, 3, bits=36))
+    P = ob.Params(n, primes, (65537,), 1 << 40)
+    K = ob.keygen(P, 2)
+    rng = np.random.default_rng(0)
+    B = 5
+    cts = [ob.Ct(orn.random_uniform(primes, n, rng), orn.random_uniform(primes, n, rng), 0, 6, 0) for _ in range(B)]
+    plan = configs.mac_sweep_plan(n_out=B, n_in=B, terms=3, seed=1)
+    return P, K, cts, plan
+
+
+def _sweep_compute(P, K, plan):
+    from oracle import bfv as ob
+    from oracle import rns as orn
+
+    def body(cs):
+        if not cs:
+            return torch.zeros((0, 2, len(P.primes), P.n), dtype=torch.int64)
+        return torch.from_numpy(np.stack([np.stack([c.c0, c.c1]) for c in cs]).view(np.int64))
+
+    def cts_of(t, scale, depth):
+        arr = t.numpy().view(np.uint64)
+        return [ob.Ct(arr[i, 0].copy(), arr[i, 1].copy(), 0, scale, depth) for i in range(arr.shape[0])]
+
+    def ntt_roundtrip(x):
+        out = []
+        for c in cts_of(x, 6, 0):
+            out.append(ob.Ct(orn.intt(orn.ntt(c.c0, P.primes), P.primes), orn.intt(orn.ntt(c.c1, P.primes), P.primes)))
+        return body(out)
+
+    def square(x):
+        return body([ob.mul_ct(P, c, c, K) for c in cts_of(x, 6, 0)])
+
+    def mac_rows(full, lo, hi):
+        ins = cts_of(full, 12, 1)
+        outs = []
+        for o in plan.outputs[lo:hi]:
+            acc = None
+            for tp in o.taps:
+                term = ob.mul_pt(P, ins[tp.in_index], [tp.weight_int % 65537], 0)
+                acc = term if acc is None else ob.add_ct(P, acc, term)
+            outs.append(acc)
+        return body(outs)
+
+    return ntt_roundtrip, square, mac_rows
+
+
+def _sweep_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1811_09953_b200 import sweep
+
+        P, K, cts, plan = _sweep_setup()
+        ntt_roundtrip, square, mac_rows = _sweep_compute(P, K, plan)
+        B = len(cts)
+        lo, hi = fdist.partition(B, world)[rank]
+        x = torch.from_numpy(np.stack([np.stack([c.c0, c.c1]) for c in cts[lo:hi]]).view(np.int64)) if hi > lo else \
+            torch.zeros((0, 2, len(P.primes), P.n), dtype=torch.int64)
+        nt, sq, mac = sweep.primitive_schedule(x, rank, world, B, len(plan.outputs), ntt_roundtrip, square,
+                                               lambda loc, c, b: fdist._torch_gather(loc, c, b), mac_rows)
+        parts = fdist.partition(B, world)
+        blk = parts[0][1] - parts[0][0]
+        full = [fdist._torch_gather(t, B, blk) for t in (nt, sq, mac)]
+        if rank == 0:
+            q.put([t.numpy().tobytes() for t in full])
+    finally:
+        dist.destroy_process_group()
+
+
+def test_cfg5_split_matches_single_process():
+    """SURVEY 8(e)'s cfg5 split (ciphertext shards for the NTT and square +
+    relinearisation, one all-gather of the squares, partitioned MAC rows)
+    at world size 2 is byte-identical to one process."""
+    from paper_1811_09953_b200 import sweep
+
+    P, K, cts, plan = _sweep_setup()
+    ntt_roundtrip, square, mac_rows = _sweep_compute(P, K, plan)
+    x = torch.from_numpy(np.stack([np.stack([c.c0, c.c1]) for c in cts]).view(np.int64))
+    want = sweep.primitive_schedule(x, 0, 1, len(cts), len(plan.outputs), ntt_roundtrip, square,
+                                   lambda loc, c, b: loc, mac_rows)
+    assert torch.equal(want[0], x)  # the NTT round trip is the identity
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sweep_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert got == [t.numpy().tobytes() for t in want]
