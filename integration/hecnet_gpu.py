@@ -129,16 +129,20 @@ def mul_ct(fv, ring, a, b, gp: GpuParams):
 
 def act_square(fv, ring, x, c2: int, c1: int, prec: int, gp: GpuParams):
     """The activation c2 x^2 + c1 x with constant plaintexts in one call
-    (engine.py:744-770 with PlainPoly(t, [c2]), PlainPoly(t, [c1]));
+    (engine.py:744-770 with PlainPoly(t, [c2 mod t]), PlainPoly(t, [c1 mod t]));
     metadata as the reference's chain: mul_ct -> mul_pt(prec) -> add_ct."""
     import torch
 
+    t = int(x.params.t_lanes[x.lane])
+    # the C ABI takes the centred plaintext constants (PlainPoly.centered, fv.py:162-165)
+    c2, c1 = (int(c) % t for c in (c2, c1))
+    c2, c1 = (c - t if c > t // 2 else c for c in (c2, c1))
     X = _dev(x)
     out = torch.empty_like(X)
     L = lib()
     ws = torch.empty(L.fcn_mul_ct_workspace_bytes(gp.ctx, 1) // 8 + 1, dtype=torch.int64, device="cuda")
-    _check(L.fcn_mul_ct_ex(gp.ctx, gp.keys, x.lane, X.data_ptr(), None, out.data_ptr(), 1, FCN_MUL_ACT, int(c2),
-                           int(c1), ws.data_ptr(), ws.numel() * 8, _stream()), fv.FVError)
+    _check(L.fcn_mul_ct_ex(gp.ctx, gp.keys, x.lane, X.data_ptr(), None, out.data_ptr(), 1, FCN_MUL_ACT, c2, c1,
+                           ws.data_ptr(), ws.numel() * 8, _stream()), fv.FVError)
     o = out.cpu().numpy().view(np.uint64)[0]
     return _ct_from(fv, ring, x, o, 2 * x.scale_exponent + prec, x.mul_depth + 1)
 

@@ -311,10 +311,28 @@ class RefState:
         return tot
 
     def hop_totals(self):
-        cfgs = _seeds()  # noqa: F841
-        from paper_1811_09953_b200 import netplan
+        """HOP totals of the plan in batched mode (engine.py:535-581 rules;
+        counted by plan type name, so it reads the reference's plans too)."""
+        from paper_1811_09953_b200.netplan import LayerCounts
 
-        return netplan.plan_hops(self.plan, "batched", self.W.t).totals
+        c = LayerCounts()
+        for p in self.plan.plans:
+            k = _plan_kind(p)
+            if k == "LinearPlan":
+                for o in p.outputs:
+                    c.pt_ct_mul += len(o.taps)
+                    c.ct_ct_add += max(0, len(o.taps) - 1)
+                    c.pt_ct_add += o.bias_int is not None
+            elif k == "PoolPlan":
+                for o in p.outputs:
+                    c.ct_ct_add += max(0, len(o) - 1)
+                    c.pt_ct_mul += p.reciprocal_int is not None
+            elif k == "ActPlan":
+                c.ct_ct_mul += p.nodes
+                c.pt_ct_mul += p.nodes * ((p.a2_int is not None) + (p.a1_mult_int is not None))
+                c.ct_ct_add += p.nodes * (p.a1_mult_int is not None)
+                c.pt_ct_add += p.nodes * (p.a0_add_int is not None)
+        return c
 
 
 # ------------------------------------------------------------------ modes
