@@ -182,6 +182,29 @@ int fcn_linear_mac_multi(const fcn_ctx* ctx, const uint64_t* d_in0, int64_t n_in
                          const int64_t* d_coef, uint64_t* const* d_outs, int n_dst, int64_t n_out, int no_rot,
                          uint64_t max_abs_coef, void* stream);
 
+/* The same linear layer on the tensor cores (csrc/mac_tc.cu) for plans whose
+ * terms are signed constants |c| <= 127 without rotation (the SIMD-batched
+ * encoding of engine.py:698-717's mul_pt + add_ct chain): every residue is
+ * split into P = fcn_tc_planes(ctx) byte planes (limbs in [2^32, 2^64)), the
+ * planes are multiplied by the int8 weights with tcgen05.mma kind::i8 into
+ * exact int32 sums, and the epilogue folds them back mod q_l.  Bit-identical
+ * to fcn_linear_mac_multi on the same plan.
+ *   fcn_split_planes: d_in [count][2][k][n] u64 -> d_planes [count][P][2kn + 256]
+ *     u8 (each plane row padded by 256 bytes: fcn_tc_planes_bytes gives the size).
+ *   fcn_linear_mac_tc: d_groups [n_groups][8] int32 = {row_off, m, k_off,
+ *     n_k, w_off, 0, 0, 0} (m <= 128 output rows d_rows[row_off..+m), inputs
+ *     d_kidx[k_off..+n_k), weights: ceil(n_k/64) 8 KB tiles from tile w_off
+ *     of d_wimg, int8, byte (m, kk) of a tile at (m/8)*512 + (kk/16)*128 +
+ *     (m%8)*16 + kk%16, zero beyond m rows / n_k inputs).  Writes the output
+ *     rows in [row_lo, row_hi) to every destination (row r at r - row_lo).
+ * Returns 0 planes / FCN_ERR_PARAM when the limbs do not fit 5..8 bytes.     */
+int fcn_tc_planes(const fcn_ctx* ctx);
+size_t fcn_tc_planes_bytes(const fcn_ctx* ctx, int64_t count);
+int fcn_split_planes(const fcn_ctx* ctx, const uint64_t* d_in, int64_t count, uint8_t* d_planes, void* stream);
+int fcn_linear_mac_tc(const fcn_ctx* ctx, const uint8_t* d_planes, int64_t n_in, int64_t n_groups,
+                      const int32_t* d_groups, const int32_t* d_kidx, const int32_t* d_rows, const int8_t* d_wimg,
+                      uint64_t* const* d_outs, int n_dst, int64_t row_lo, int64_t row_hi, void* stream);
+
 /* fv.mul_ct (fv.py:498-549): exact tensor in the extended base, exact
  * floor((t*T + q>>1)/q) mod q, base-beta digits of c2', key switching.
  * d_b == NULL computes the square a*a.  `count` ciphertexts [count][2][k][n].

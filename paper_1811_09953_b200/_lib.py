@@ -68,6 +68,10 @@ SIGNATURES = {
     "fcn_linear_mac": (_I, [_P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _I64, _P]),
     "fcn_linear_mac_ex": (_I, [_P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _I64, _I, C.c_uint64, _P]),
     "fcn_linear_mac_multi": (_I, [_P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _I, _I64, _I, C.c_uint64, _P]),
+    "fcn_tc_planes": (_I, [_P]),
+    "fcn_tc_planes_bytes": (C.c_size_t, [_P, _I64]),
+    "fcn_split_planes": (_I, [_P, _P, _I64, _P, _P]),
+    "fcn_linear_mac_tc": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _P, _P, _I, _I64, _I64, _P]),
     "fcn_mul_ct_workspace_bytes": (C.c_size_t, [_P, _I64]),
     "fcn_mul_ct": (_I, [_P, _P, _I, _P, _P, _P, _I64, _P, C.c_size_t, _P]),
     "fcn_mul_ct_ex": (_I, [_P, _P, _I, _P, _P, _P, _I64, _I, _I64, _I64, _P, C.c_size_t, _P]),

@@ -313,6 +313,35 @@ struct Fanout {
   int n = 0;
   uint64_t* dst[kMaxFanout] = {};
 };
+// Tensor-core linear layer (csrc/mac_tc.cu): one output group = up to 128
+// output rows (rows[row_off .. row_off + m)) over the inputs
+// kidx[k_off .. k_off + n_k); its weights are nchunks = ceil(n_k / 64)
+// pre-laid-out 8 KB K-major tiles starting at tile w_off of wimg.
+struct TcGroup {
+  int32_t row_off, m, k_off, n_k, w_off, pad0, pad1, pad2;
+};
+struct TcLaunch {
+  const uint8_t* planes = nullptr;  // [n_in][P][cols] byte planes
+  int64_t cols = 0;                 // residues per ciphertext (2 k n)
+  int planes_n = 0;                 // P
+  int64_t n_groups = 0;
+  const TcGroup* groups = nullptr;
+  const int32_t* kidx = nullptr;
+  const int32_t* rows = nullptr;
+  const int8_t* wimg = nullptr;
+  Fanout out;                        // rows [row_lo, row_hi) of the layer's output
+  int64_t row_lo = 0, row_hi = 0;
+  int logn = 0, k = 0;
+  const LimbConst* lcs = nullptr;
+};
+int launch_mac_tc(const TcLaunch& a, cudaStream_t st);
+// Row pitch (bytes) of one byte plane of one ciphertext: the 2kn columns
+// padded by 256 bytes, so the 64-byte segments the MAC gathers from
+// thousands of planes do not all fall on the same L2 sets (2kn is a power
+// of two times k).
+__host__ __device__ inline int64_t tc_plane_pitch(int64_t cols) { return cols + 256; }
+int launch_split_planes(const uint64_t* in, int64_t rows, int64_t cols, int P, uint8_t* planes, cudaStream_t st);
+
 // Inverse-NTT epilogue (row-aligned with the transformed rows, period/offset
 // limb indexing): mode 1: out = v + add; mode 2: out = c2 (v + add) + c1 lin;
 // mode 3: out = add + c2 v (mod q_l).  Coefficients per limb index: canonical u64 and FP64 {w, w/q}.

@@ -1727,6 +1727,70 @@ extern "C" int fcn_linear_mac_multi(const fcn_ctx* x, const uint64_t* d_in0, int
 
 // workspace per ciphertext in words: EA, EB (2K each), T (3K), R01 (2k),
 // DGN (D k), ACC (2k), raw digit rows (D)
+// ---- tensor-core linear layer (csrc/mac_tc.cu)
+
+static int tc_planes(const fcn_ctx* x) {
+  uint64_t qmax = 0;
+  for (uint64_t q : x->primes) qmax = q > qmax ? q : qmax;
+  const int bits = bitlen64(qmax);
+  return (bits + 7) / 8;
+}
+
+extern "C" int fcn_tc_planes(const fcn_ctx* x) {
+  if (!x) return set_error(FCN_ERR_ARG, "null context");
+  const int P = tc_planes(x);
+  return (P >= 5 && P <= 8) ? P : 0;
+}
+
+extern "C" size_t fcn_tc_planes_bytes(const fcn_ctx* x, int64_t count) {
+  if (!x || count <= 0) return 0;
+  return (size_t)count * (size_t)tc_planes(x) * (size_t)tc_plane_pitch(2LL * x->k * x->n);
+}
+
+extern "C" int fcn_split_planes(const fcn_ctx* x, const uint64_t* d_in, int64_t count, uint8_t* d_planes, void* stream) {
+  if (!x) return set_error(FCN_ERR_ARG, "null context");
+  if (count <= 0) return FCN_OK;
+  if (!d_in || !d_planes) return set_error(FCN_ERR_ARG, "null buffer");
+  const int P = tc_planes(x);
+  if (P < 5 || P > 8) return set_error(FCN_ERR_PARAM, "byte planes need limbs in [2^32, 2^64)");
+  DeviceGuard g(x->device);
+  return launch_split_planes(d_in, count, 2LL * x->k * x->n, P, d_planes, (cudaStream_t)stream);
+}
+
+extern "C" int fcn_linear_mac_tc(const fcn_ctx* x, const uint8_t* d_planes, int64_t n_in, int64_t n_groups,
+                                 const int32_t* d_groups, const int32_t* d_kidx, const int32_t* d_rows,
+                                 const int8_t* d_wimg, uint64_t* const* d_outs, int n_dst, int64_t row_lo,
+                                 int64_t row_hi, void* stream) {
+  if (!x) return set_error(FCN_ERR_ARG, "null context");
+  if (n_groups <= 0 || row_hi <= row_lo) return FCN_OK;
+  if (n_dst < 1 || n_dst > kMaxFanout || !d_outs) return set_error(FCN_ERR_ARG, "1..%d destinations", kMaxFanout);
+  if (!d_planes || !d_groups || !d_kidx || !d_rows || !d_wimg) return set_error(FCN_ERR_ARG, "null argument");
+  if (n_in <= 0) return set_error(FCN_ERR_ARG, "no inputs");
+  const int P = tc_planes(x);
+  if (P < 5 || P > 8) return set_error(FCN_ERR_PARAM, "byte planes need limbs in [2^32, 2^64)");
+  TcLaunch a;
+  a.planes = d_planes;
+  a.cols = 2LL * x->k * x->n;
+  a.planes_n = P;
+  a.n_groups = n_groups;
+  a.groups = reinterpret_cast<const TcGroup*>(d_groups);
+  a.kidx = d_kidx;
+  a.rows = d_rows;
+  a.wimg = d_wimg;
+  a.out.n = n_dst;
+  for (int d = 0; d < n_dst; ++d) {
+    if (!d_outs[d]) return set_error(FCN_ERR_ARG, "null destination %d", d);
+    a.out.dst[d] = d_outs[d];
+  }
+  a.row_lo = row_lo;
+  a.row_hi = row_hi;
+  a.logn = x->logn;
+  a.k = x->k;
+  a.lcs = x->ext->d_lc;
+  DeviceGuard g(x->device);
+  return launch_mac_tc(a, (cudaStream_t)stream);
+}
+
 static int64_t mulct_words_per_ct(const fcn_ctx* x) {
   const int64_t K = x->k + x->m, k = x->k, D = x->ell + 1;
   return (2 * K + 2 * K + 3 * K + 2 * k + D * k + 2 * k + D) * (int64_t)x->n;

@@ -38,6 +38,7 @@ import numpy as np
 from . import _lib
 from . import device as dev
 from . import fv
+from . import mac_tc
 from .encode import FixedPointConfig, decode_fixed, encode_integer, integer_bits, round_half_away
 from .fv import Ciphertext, EncryptionParams, EvalKeys, FVError, PublicKey, SecretKey
 from .netplan import (  # noqa: F401  (re-exported: reference engine API surface)
@@ -266,6 +267,8 @@ class _Mac:
     n_terms: int
     no_rot: bool = False
     max_abs_coef: int = 0
+    host: tuple | None = None  # (rowptr, col, coef) numpy: the tensor-core lowering's input
+    tc: dict = field(default_factory=dict)  # (planes, cols, n_in) -> _TcPlan | None
 
 
 @dataclass
@@ -282,6 +285,7 @@ def _upload_mac(rowptr, col, rot, coef) -> _Mac:
     d = "cuda"
     rot_a = np.asarray(rot, dtype=np.int64)
     coef_a = np.asarray(coef, dtype=np.int64)
+    no_rot = bool(len(rot) == 0 or not np.any(rot_a))
     return _Mac(
         torch.as_tensor(np.asarray(rowptr, dtype=np.int32), device=d),
         torch.as_tensor(np.asarray(col, dtype=np.int32) if len(col) else np.zeros(1, np.int32), device=d),
@@ -289,8 +293,9 @@ def _upload_mac(rowptr, col, rot, coef) -> _Mac:
         torch.as_tensor(coef_a if len(coef) else np.zeros(1, np.int64), device=d),
         len(rowptr) - 1,
         len(col),
-        bool(len(rot) == 0 or not np.any(rot_a)),
+        no_rot,
         int(np.abs(coef_a).max()) if len(coef) else 0,
+        (np.asarray(rowptr, dtype=np.int64), np.asarray(col, dtype=np.int64), coef_a) if no_rot else None,
     )
 
 
@@ -574,6 +579,13 @@ def _layer_range(params, lane, ek, plan, lw, cur, lo: int, hi: int, encoding: st
     kind = lw[0]
     if kind in ("linear", "pool"):
         mac, bias = lw[1], lw[2]
+        tcp = mac_tc.plan_for(params, mac, cur.shape[0]) if mac.host is not None else None
+        if tcp is not None:  # tensor-core MAC (csrc/mac_tc.cu)
+            if out is None:
+                out = dev.empty((hi - lo, 2, len(params.limb_primes), params.n))
+            mac_tc.run(params, tcp, cur, out, fanout, lo, hi)
+            _run_bias(params, lane, out, bias if (lo == 0 and hi == mac.n_out) else _bias_range(bias, lo, hi), fanout)
+            return out
         if lo == 0 and hi == mac.n_out:
             out = _mac_out(params, mac, cur, None, out, fanout)
             _run_bias(params, lane, out, bias, fanout)
