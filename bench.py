@@ -439,6 +439,25 @@ def run_gpu(args, ws, rank, local):
 
         transport = args.transport
         if transport == "p2p":
+            # capability check that cannot fail on one rank only: every rank
+            # votes (symmetric-memory module present, peer access to every
+            # local GPU) before any rank enters the collective rendezvous
+            cap = 1
+            try:
+                import torch.distributed._symmetric_memory  # noqa: F401
+
+                n_local = torch.cuda.device_count()
+                for peer in range(n_local):
+                    if peer != local and not torch.cuda.can_device_access_peer(local, peer):
+                        cap = 0
+            except Exception:  # noqa: BLE001 - vote 0
+                cap = 0
+            flag = torch.tensor([cap], device="cuda", dtype=torch.int32)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0:
+                transport = "nccl"
+                args.transport_note = "p2p capability vote failed on some rank"
+        if transport == "p2p":
             # pre-flight: every rank must be able to map the symmetric buffers
             # and produce the same bytes as the NCCL all-gather schedule
             ok = 1

@@ -58,8 +58,14 @@ def round_half_away(v: float) -> int:
 
 
 def round_half_away_array(v: np.ndarray) -> np.ndarray:
-    """Vectorised `round_half_away` (identical float64 operations, int64 out)."""
+    """Vectorised `round_half_away` (identical float64 operations, int64 out).
+
+    Magnitudes at or above 2^62 (or non-finite values) would wrap in int64;
+    they take the scalar Python-int path instead (an object array, exact like
+    the reference's big-int rounding, encode.py:96-98)."""
     v = np.asarray(v, dtype=np.float64)
+    if v.size and not (np.isfinite(v).all() and np.abs(v).max() < 2.0 ** 62):
+        return np.array([round_half_away(x) for x in v.ravel()], dtype=object).reshape(v.shape)
     mag = np.floor(np.abs(v) + 0.5)
     return np.where(v >= 0, mag, -mag).astype(np.int64)
 
