@@ -38,6 +38,7 @@
 // engine._lower_tc).
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "fcn_common.cuh"
@@ -97,6 +98,16 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try(bar, parity)) {
+  }
+}
+// for the warps off the MMA critical path: back off between polls, so that
+// spinning warps do not steal the shared-memory bandwidth the tensor cores
+// read their operands with (measured: 126 -> ~60 clk per MMA issue)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  unsigned ns = 32;
+  while (!mbar_try(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < 256 ? ns * 2 : 256;
   }
 }
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
@@ -194,6 +205,8 @@ __global__ void __launch_bounds__(256) split_planes_kernel(const uint64_t* __res
 // 5-12 drain the accumulators (two warps per lane quarter); the epilogue of tile i
 // overlaps the loads of tile i+1 and its MMAs wait only for the accumulator
 // to be drained (tmem_empty).
+__device__ unsigned long long g_tc_dbg[8];  // FCN_TC_DBG & 64: MMA-thread cycle counters (block 0)
+
 template <int P>
 struct TcShape {
   static constexpr int kStageBytes = tc::kABytes + P * tc::kBPlaneBytes;
@@ -268,7 +281,7 @@ __global__ void __launch_bounds__(TcShape<P>::kThreads, 1)
       for (int c = 0; c < nchunks; ++c, ++it) {
         const int s = it % kSt;
         const int r = it % kRing;
-        if (it >= kSt) mbar_wait(&empty[s], ((it / kSt) + 1) & 1);
+        if (it >= kSt) mbar_wait_sleep(&empty[s], ((it / kSt) + 1) & 1);
         uint8_t* A = smem + s * S_::kStageBytes;
         uint8_t* B = A + kABytes;
         if (threadIdx.x == 0) {
@@ -279,7 +292,7 @@ __global__ void __launch_bounds__(TcShape<P>::kThreads, 1)
             bulk_g2s(A, wimg + ((int64_t)G.w_off + c) * kABytes, kABytes, &full[s]);
           }
         }
-        mbar_wait(&kfull[r], (it / kRing) & 1);
+        mbar_wait_sleep(&kfull[r], (it / kRing) & 1);
         int32_t cur[kLoadsPerThread];
 #pragma unroll
         for (int i = 0; i < kLoadsPerThread; ++i) {
@@ -313,7 +326,7 @@ __global__ void __launch_bounds__(TcShape<P>::kThreads, 1)
       const int nchunks = (G.n_k + kChunk - 1) / kChunk;
       for (int c = 0; c < nchunks; ++c, ++it) {
         const int r = it % kRing;
-        if (it >= kRing) mbar_wait(&kempty[r], ((it / kRing) + 1) & 1);
+        if (it >= kRing) mbar_wait_sleep(&kempty[r], ((it / kRing) + 1) & 1);
         if (lane < kChunk / 4) cp_async16(kring + r * kChunk + lane * 4, kidx + G.k_off + c * kChunk + lane * 4);
         cp_async_arrive_noinc(&kfull[r]);
       }
@@ -322,14 +335,19 @@ __global__ void __launch_bounds__(TcShape<P>::kThreads, 1)
     // ------------------------------------------------------ MMA issuer
     if (lane == 0) {
       int it = 0, local = 0;
+      unsigned long long w_full = 0, w_tmem = 0, t_start = clock64();
       for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++local) {
         const TcGroup G = groups[t % n_groups];
         const int nchunks = (G.n_k + kChunk - 1) / kChunk;
+        unsigned long long c0 = clock64();
         if (local > 0) mbar_wait(tmem_empty, (local - 1) & 1);  // accumulator drained
+        w_tmem += clock64() - c0;
         tc_fence_after();
         for (int c = 0; c < nchunks; ++c, ++it) {
           const int s = it % kSt;
+          c0 = clock64();
           mbar_wait(&full[s], (it / kSt) & 1);
+          w_full += clock64() - c0;
           // the B tiles were written by the producers' cp.async (generic
           // proxy): make them visible to the tensor cores' async-proxy reads
           if (!(dbg & 16)) fence_proxy_async();
@@ -366,6 +384,12 @@ __global__ void __launch_bounds__(TcShape<P>::kThreads, 1)
         }
         mma_commit(tmem_full);
       }
+      if ((dbg & 64) && blockIdx.x == 0) {
+        g_tc_dbg[0] = clock64() - t_start;
+        g_tc_dbg[1] = w_full;
+        g_tc_dbg[2] = w_tmem;
+        g_tc_dbg[3] = it;
+      }
     }
     __syncwarp();
   } else {
@@ -385,7 +409,7 @@ __global__ void __launch_bounds__(TcShape<P>::kThreads, 1)
       const int64_t orow = live ? (int64_t)rows_tab[G.row_off + m] : -1;
       const bool store = live && orow >= row_lo && orow < row_hi;
       const int64_t obase = (orow - row_lo) * cols + col0;
-      mbar_wait(tmem_full, local & 1);
+      mbar_wait_sleep(tmem_full, local & 1);
       tc_fence_after();
 #pragma unroll 1
       for (int cg = half * (kN / 2); cg < (half + 1) * (kN / 2); cg += 8) {
@@ -445,7 +469,8 @@ __global__ void __launch_bounds__(TcShape<P>::kThreads, 1)
 // FCN_TC_DBG (timing ablations only; results are wrong): 1 = producers skip
 // the byte-plane gathers, 2 = the epilogue skips the fold and the stores,
 // 4 = no weight-tile copies, 8 = weights read from shared memory (SS MMA),
-// 16 = no proxy fence before the MMAs, 32 = stages released without tcgen05.commit
+// 16 = no proxy fence before the MMAs, 32 = stages released without tcgen05.commit,
+// 64 = print the MMA thread's cycle split (block 0) after the launch
 static int tc_debug() {
   static const int v = [] {
     const char* e = getenv("FCN_TC_DBG");
@@ -466,6 +491,13 @@ static int launch_tc_t(const TcLaunch& a, cudaStream_t st) {
                                                                     a.kidx, a.rows, a.wimg, a.out, a.row_lo,
                                                                     a.row_hi, a.logn, a.k, a.lcs, tc_debug());
   FCN_LAUNCH_CHECK("mac_tc_kernel");
+  if (tc_debug() & 64) {
+    unsigned long long h[8];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_tc_dbg, sizeof(h));
+    fprintf(stderr, "[mac_tc] block0: %llu clk total, %llu waiting full, %llu waiting tmem_empty, %llu chunks\n", h[0],
+            h[1], h[2], h[3]);
+  }
   return FCN_OK;
 }
 
