@@ -314,6 +314,60 @@ def _sampled_first_stage(E, name, n_check, seed=5):
         assert int(mid.scales[o]) == y.scale and int(mid.depths[o]) == y.depth
 
 
+def _sampled_every_layer(E, name, n_check, seed=7):
+    """Every layer of a full-size config, final layer included: the GPU runs
+    the compiled plan layer by layer (the same kernels eval_encrypted
+    launches, the tensor-core MAC where the cost model picks it), and for
+    `n_check` sampled outputs of each layer the oracle recomputes the output
+    from that layer's GPU inputs (engine.py:698-770 op for op); the bytes must
+    be identical.  Together with the first-stage check and the whole-network
+    comparison against the reference package (tools/fullpass_parity.py,
+    profiles/r02_fullpass_parity_cfg*.json) this pins every stage."""
+    from paper_1811_09953_b200 import configs
+    from paper_1811_09953_b200 import device as dev
+    from paper_1811_09953_b200 import fv
+
+    W = configs.WORKLOADS[name]
+    P = fv.EncryptionParams(W.n, W.primes, (W.t,), W.beta)
+    OP = ob.Params(W.n, W.primes, (W.t,), W.beta)
+    cfg = W.fixed_point()
+    prec, t = cfg.precision_bits, W.t
+    net = configs.build_network(name)
+    sk, pk, ek = fv.keygen(P, configs.SEED_KEYS)
+    x = configs.build_inputs(name)
+    tensor = E.encrypt_tensor_batched(pk, P, x, cfg, 0, configs.SEED_ENC)
+    comp = E.compile_network(net, cfg)
+    low = E._lowered(comp, t, P.n, "batched")
+    K = ob.Keys(sk.s.host(), pk.p0.host(), pk.p1.host(), [a.host() for a in ek.a], [g.host() for g in ek.g])
+    cur = tensor.buf
+    rng = np.random.default_rng(seed)
+    for plan, lw in zip(comp.plans, low):
+        count = len(plan.outputs) if type(plan).__name__ == "LinearPlan" else plan.nodes
+        nxt = E._layer_range(P, 0, ek, plan, lw, cur, 0, count, "batched")
+        ins = dev.to_host(cur)
+        got = dev.to_host(nxt)
+        picks = sorted(set(rng.choice(count, min(n_check, count), replace=False).tolist()) | {count - 1})
+        for o in picks:
+            if type(plan).__name__ == "LinearPlan":
+                y = None
+                for tp in plan.outputs[o].taps:
+                    term = ob.mul_pt(OP, ob.Ct(ins[tp.in_index, 0], ins[tp.in_index, 1], 0, prec), [tp.weight_int % t],
+                                     prec)
+                    y = term if y is None else ob.add_ct(OP, y, term)
+            else:
+                c = ob.Ct(ins[o, 0], ins[o, 1], 0, prec)
+                sq = ob.mul_ct(OP, c, c, K)
+                y = sq if plan.a2_int is None else ob.mul_pt(OP, sq, [plan.a2_int % t], prec)
+                if plan.a1_mult_int is not None:
+                    y = ob.add_ct(OP, y, ob.mul_pt(OP, c, [plan.a1_mult_int % t], y.scale - c.scale))
+            want = np.zeros_like(got[o]) if y is None else np.stack([y.c0, y.c1])  # empty row: Ciphertext.zero
+            assert np.array_equal(got[o], want), (plan.name, o)
+        cur = nxt
+    # and the layer-by-layer result is the network's result
+    out, _ = E.eval_encrypted(comp, tensor, ek, cfg, encoding="batched")
+    assert np.array_equal(dev.to_host(out.buf), dev.to_host(cur))
+
+
 def test_cfg2_full_network_sampled_parity(E):
     _sampled_first_stage(E, "cfg2", 3)
 
@@ -322,9 +376,26 @@ def test_cfg4_full_network_sampled_parity(E):
     _sampled_first_stage(E, "cfg4", 3)
 
 
+def test_cfg2_every_layer_sampled_parity(E):
+    _sampled_every_layer(E, "cfg2", 2)
+
+
+def test_cfg4_every_layer_sampled_parity(E):
+    _sampled_every_layer(E, "cfg4", 2)
+
+
+def test_cfg1_every_layer_sampled_parity(E):
+    _sampled_every_layer(E, "cfg1", 3)
+
+
 @pytest.mark.slow
 def test_cfg3_full_network_sampled_parity(E):
     _sampled_first_stage(E, "cfg3", 2)
+
+
+@pytest.mark.slow
+def test_cfg3_every_layer_sampled_parity(E):
+    _sampled_every_layer(E, "cfg3", 1)
 
 
 def test_evaluate_stream_matches_eval(E):

@@ -524,3 +524,14 @@ def test_cfg5_full_batch_square_decrypts():
         else:
             want[b, e - n] -= int(d[b]) ** 2
     assert np.array_equal(got, (want % t).astype(np.int64))
+    # bit-exact against the oracle on ciphertexts from inside the batch
+    # (first, middle, last): the batched call equals the reference's mul_ct
+    from oracle import bfv as ob
+
+    OP = ob.Params(n, tuple(W.primes), (t,), W.beta)
+    K = ob.Keys(sk.s.host(), pk.p0.host(), pk.p1.host(), [a.host() for a in ek.a], [g.host() for g in ek.g])
+    xs, ys = dev.to_host(cts), dev.to_host(sq)
+    for b in (0, 2049, B - 1):
+        x = ob.Ct(xs[b, 0], xs[b, 1])
+        w = ob.mul_ct(OP, x, x, K)
+        assert np.array_equal(ys[b], np.stack([w.c0, w.c1])), b
