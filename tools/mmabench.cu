@@ -65,8 +65,10 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, long long* out) {
 // the kernel's pattern: per 64-input chunk 7 planes x 2 K-steps, A/B at
 // distinct shared-memory addresses, accumulators p * 64; SW = 0 no swizzle,
 // 64 = SWIZZLE_64B (layout type 4) with the 64-byte atoms
-template <int SW>
-__global__ void __launch_bounds__(128, 1) bench_rot(int chunks, long long* out) {
+// MODE bit 0: per-chunk tcgen05.commit to a stage barrier (like the kernel);
+// bit 1: the other warps spin on an mbarrier until the MMA lane is done
+template <int SW, int MODE = 0>
+__global__ void __launch_bounds__(448, 1) bench_rot(int chunks, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar;
@@ -75,16 +77,31 @@ __global__ void __launch_bounds__(128, 1) bench_rot(int chunks, long long* out) 
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (threadIdx.x == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+  __shared__ __align__(8) uint64_t stage_bar[5];
+  __shared__ __align__(8) uint64_t done_bar;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&done_bar)));
+    for (int i = 0; i < 5; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&stage_bar[i])));
+  }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = slot;
   constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 16) | ((uint32_t)(64 >> 3) << 17) | (8u << 24);
+  if ((MODE & 2) && threadIdx.x >= 32) {
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                   : "=r"(ok) : "r"(smem_u32(&done_bar)));
+  }
   if (threadIdx.x == 0) {
     const uint32_t base = smem_u32(smem);
     long long t0 = clock64();
     for (int c = 0; c < chunks; ++c) {
+      if (MODE & 1)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(&stage_bar[c % 5])));
       const uint32_t A = base + (c % 5) * 36864, B = A + 8192;
       for (int p = 0; p < 7; ++p)
         for (int ks = 0; ks < 2; ++ks) {
@@ -108,6 +125,7 @@ __global__ void __launch_bounds__(128, 1) bench_rot(int chunks, long long* out) 
                    : "=r"(ok) : "r"(smem_u32(&bar)));
     long long t1 = clock64();
     if (blockIdx.x == 0) out[0] = t1 - t0;
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&done_bar)) : "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -117,19 +135,19 @@ __global__ void __launch_bounds__(128, 1) bench_rot(int chunks, long long* out) 
   }
 }
 
-template <int SW>
-void run_rot(long long* d) {
+template <int SW, int MODE = 0>
+void run_rot(long long* d, int threads = 128) {
   const int smem = 5 * 36864 + 1024;
-  cudaFuncSetAttribute(bench_rot<SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(bench_rot<SW, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int chunks = 2048;
-  bench_rot<SW><<<148, 128, smem>>>(8, d);
+  bench_rot<SW, MODE><<<148, threads, smem>>>(8, d);
   cudaError_t err = cudaDeviceSynchronize();
-  bench_rot<SW><<<148, 128, smem>>>(chunks, d);
+  bench_rot<SW, MODE><<<148, threads, smem>>>(chunks, d);
   err = cudaDeviceSynchronize();
   long long cyc = 0;
   cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
-  printf("rotating operands, %s: %.2f clk/MMA (%s)\n", SW ? "SWIZZLE_64B" : "no swizzle", (double)cyc / (chunks * 14),
-         cudaGetErrorString(err));
+  printf("rotating operands, %s, %d threads, mode %d: %.2f clk/MMA (%s)\n", SW ? "SWIZZLE_64B" : "no swizzle", threads,
+         MODE, (double)cyc / (chunks * 14), cudaGetErrorString(err));
 }
 
 template <int N, bool TS>
@@ -166,5 +184,9 @@ int main() {
   run<256, true>(d);
   run_rot<0>(d);
   run_rot<64>(d);
+  run_rot<0, 0>(d, 448);
+  run_rot<0, 1>(d, 128);
+  run_rot<0, 2>(d, 448);
+  run_rot<0, 3>(d, 448);
   return 0;
 }
