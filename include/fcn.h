@@ -242,6 +242,14 @@ int fcn_key_mac(const fcn_ctx* ctx, const fcn_keys* keys, const uint64_t* d_digi
 
 /* fv.decrypt core (fv.py:337-353): given w = [c0 + c1 s]_q as RNS rows
  * [count][k][n], write m = floor((w t + q>>1)/q) mod t as [count][n].     */
+/* Noise budget (fv.noise_budget, fv.py:356-377) on the GPU: for each of the
+ * `count` polynomials w = c0 + c1 s in d_w ([count][k][n] residues), every
+ * one of `blocks` CTAs writes the largest |centred [t w]_q| of its share of
+ * the coefficients as `out_words` little-endian u64 words (>= the words of
+ * q) to d_out[count][blocks][out_words]; the host takes the maximum over
+ * the blocks and the reference's log2(q) - 1 - log2(worst).               */
+int fcn_noise_max(const fcn_ctx* ctx, int lane, const uint64_t* d_w, int64_t count, uint64_t* d_out, int blocks,
+                  int out_words, void* stream);
 int fcn_decrypt_round(const fcn_ctx* ctx, int lane, const uint64_t* d_w, uint64_t* d_m, int64_t count,
                       void* stream);
 

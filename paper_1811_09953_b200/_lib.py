@@ -77,6 +77,7 @@ SIGNATURES = {
     "fcn_mul_ct_ex": (_I, [_P, _P, _I, _P, _P, _P, _I64, _I, _I64, _I64, _P, C.c_size_t, _P]),
     "fcn_key_mac": (_I, [_P, _P, _P, _P, _I64, _P]),
     "fcn_mul_ct_multi": (_I, [_P, _P, _I, _P, _P, _P, _I, _I64, _I, _I64, _I64, _P, C.c_size_t, _P]),
+    "fcn_noise_max": (_I, [_P, _I, _P, _I64, _P, _I, _I, _P]),
     "fcn_decrypt_round": (_I, [_P, _I, _P, _P, _I64, _P]),
 }
 

@@ -1268,6 +1268,76 @@ __global__ void decrypt_round_kernel(const uint64_t* __restrict__ W, uint64_t* _
   }
 }
 
+// Noise budget (fv.py:356-377): the largest |centred [t w]_q| over the
+// coefficients of each ciphertext's w = c0 + c1 s.  Each thread reconstructs
+// its coefficients' canonical multiword values (CRT through the float64-
+// estimated overflow count, corrected exactly by mw_reduce_q), centres them
+// and keeps the running maximum; the block's maximum is written out and the
+// host reduces the blocks (exact integers) and takes the reference's log2.
+template <int KQ, int NW>
+__global__ void __launch_bounds__(256) noise_max_kernel(const uint64_t* __restrict__ W, int logn,
+                                                        const MulCtConst* __restrict__ cc,
+                                                        const LimbConst* __restrict__ lcs, uint64_t* __restrict__ out,
+                                                        int out_words) {
+  __shared__ uint64_t sm[256][NW];
+  const int n = 1 << logn;
+  const int k = cc->k;
+  const int64_t ct = blockIdx.y;
+  uint64_t best[NW];
+  mw_zero<NW>(best);
+  for (int coef = blockIdx.x * blockDim.x + threadIdx.x; coef < n; coef += gridDim.x * blockDim.x) {
+    uint64_t a[NW];
+    mw_zero<NW>(a);
+    double fu = 0.0;
+#pragma unroll
+    for (int i = 0; i < KQ; ++i) {
+      if (i < k) {
+        const LimbConst& c = lcs[i];
+        const uint64_t x = mulmod(W[(ct * k + i) * n + coef], cc->t % c.q, c);  // [t w]_{q_i}
+        const uint64_t z = shoup(x, cc->qinv[i], cc->qinv_s[i], c.q);
+        fu += (double)z * cc->rq[i];
+        mw_mac<NW>(a, cc->Qw[i], cc->qwords, z);
+      }
+    }
+    mw_reduce_q<NW>(a, cc, (int64_t)floor(fu));
+    uint64_t hw[NW];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) hw[i] = i < MW_LIM ? cc->hw[i] : 0;
+    if (!mw_ge<NW>(hw, a)) {  // a > (q-1)/2: |centred| = q - a
+      uint64_t qa[NW];
+#pragma unroll
+      for (int i = 0; i < NW; ++i) qa[i] = i < MW_LIM ? cc->qw[i] : 0;
+      mw_sub<NW>(qa, a);
+#pragma unroll
+      for (int i = 0; i < NW; ++i) a[i] = qa[i];
+    }
+    if (!mw_ge<NW>(best, a)) {
+#pragma unroll
+      for (int i = 0; i < NW; ++i) best[i] = a[i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NW; ++i) sm[threadIdx.x][i] = best[i];
+  __syncthreads();
+  for (int stride = 128; stride > 0; stride >>= 1) {
+    if ((int)threadIdx.x < stride) {
+      uint64_t o[NW];
+#pragma unroll
+      for (int i = 0; i < NW; ++i) o[i] = sm[threadIdx.x + stride][i];
+      uint64_t mine[NW];
+#pragma unroll
+      for (int i = 0; i < NW; ++i) mine[i] = sm[threadIdx.x][i];
+      if (!mw_ge<NW>(mine, o)) {
+#pragma unroll
+        for (int i = 0; i < NW; ++i) sm[threadIdx.x][i] = o[i];
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < (unsigned)out_words)
+    out[(ct * gridDim.x + blockIdx.x) * out_words + threadIdx.x] = threadIdx.x < NW ? sm[0][threadIdx.x] : 0;
+}
+
 // ------------------------------------------------------ host constants
 
 static Big big_prod(const std::vector<uint64_t>& v, int skip = -1) {
@@ -2390,6 +2460,27 @@ extern "C" int fcn_key_mac(const fcn_ctx* x, const fcn_keys* keys, const uint64_
   if (keys->k != x->k || keys->n != x->n || keys->D != x->ell + 1) return set_error(FCN_ERR_ARG, "keys do not match context");
   DeviceGuard gd(x->device);
   return launch_keymac(d_digits, keys, d_acc, count, keys->D, x->k, x, (cudaStream_t)stream);
+}
+
+extern "C" int fcn_noise_max(const fcn_ctx* x, int lane, const uint64_t* d_w, int64_t count, uint64_t* d_out,
+                             int blocks, int out_words, void* stream) {
+  if (!x || lane < 0 || lane >= x->n_lanes) return set_error(FCN_ERR_ARG, "bad context or lane");
+  if (count <= 0) return FCN_OK;
+  if (!d_w || !d_out || blocks < 1 || count > 65535) return set_error(FCN_ERR_ARG, "bad buffers or sizes");
+  const int qwords = x->host_mc[lane].qwords;
+  if (out_words < qwords || out_words > 256) return set_error(FCN_ERR_ARG, "out_words must be >= %d", qwords);
+  DeviceGuard g(x->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const MulCtConst* mc = x->d_mc + lane;
+  dim3 grid((unsigned)blocks, (unsigned)count);
+  if (x->k <= 4)
+    noise_max_kernel<4, 6><<<grid, 256, 0, st>>>(d_w, x->logn, mc, x->ext->d_lc, d_out, out_words);
+  else if (x->k <= 8)
+    noise_max_kernel<8, 10><<<grid, 256, 0, st>>>(d_w, x->logn, mc, x->ext->d_lc, d_out, out_words);
+  else
+    noise_max_kernel<16, 18><<<grid, 256, 0, st>>>(d_w, x->logn, mc, x->ext->d_lc, d_out, out_words);
+  FCN_LAUNCH_CHECK("noise_max_kernel");
+  return FCN_OK;
 }
 
 extern "C" int fcn_decrypt_round(const fcn_ctx* x, int lane, const uint64_t* d_w, uint64_t* d_m, int64_t count, void* stream) {

@@ -572,17 +572,34 @@ def decrypt(sk: SecretKey, ct: Ciphertext, check_budget: bool = False) -> PlainP
 
 
 def noise_budget(sk: SecretKey, ct: Ciphertext) -> float:
-    """Bits of headroom before noise corrupts decryption (fv.py:356-377)."""
-    params = ct.params
+    """Bits of headroom before noise corrupts decryption (fv.py:356-377).
+
+    w = c0 + c1 s on the GPU; the largest |centred [t w]_q| over the
+    coefficients is found by fcn_noise_max (multiword CRT per coefficient,
+    block maxima) and the host takes the reference's log2 of that exact
+    integer."""
+    return float(noise_budget_batch(sk, ct.params, ct.stacked(), ct.lane)[0])
+
+
+def noise_budget_batch(sk: SecretKey, params: EncryptionParams, buf, lane: int = 0) -> np.ndarray:
+    """noise_budget of every ciphertext of a [B][2][k][n] device buffer."""
+    B = buf.shape[0]
+    w = raw_decrypt_batch(sk, params, buf)
     q = params.q
-    t = int(params.t_lanes[ct.lane])
-    w = ring.poly_add(ct.c0, ring.poly_mul_ntt(ct.c1, sk.s_ntt))
-    worst = 1
-    for v in _crt_coeffs(params, ring.scalar_mul(w, t).host()):
-        if v > q >> 1:
-            v = q - v
-        worst = max(worst, v)
-    return math.log2(q) - 1.0 - math.log2(worst)
+    words = (q.bit_length() + 63) // 64
+    blocks = max(1, min(64, params.n // 256))
+    out = dev.empty((B, blocks, words))
+    _lib.check(_lib.lib().fcn_noise_max(params.native().ptr, lane, w.data_ptr(), B, out.data_ptr(), blocks, words,
+                                        dev.stream_ptr()), FVError)
+    host = dev.to_host(out)
+    res = np.empty(B)
+    for b in range(B):
+        worst = 1
+        for blk in range(blocks):
+            v = sum(int(host[b, blk, i]) << (64 * i) for i in range(words))
+            worst = max(worst, v)
+        res[b] = math.log2(q) - 1.0 - math.log2(worst)
+    return res
 
 
 # --------------------------------------------------------------- evaluation

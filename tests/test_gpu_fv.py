@@ -535,3 +535,32 @@ def test_cfg5_full_batch_square_decrypts():
         x = ob.Ct(xs[b, 0], xs[b, 1])
         w = ob.mul_ct(OP, x, x, K)
         assert np.array_equal(ys[b], np.stack([w.c0, w.c1])), b
+
+
+@pytest.mark.parametrize("k,bits,n", [(4, 50, 1024), (3, 36, 4096), (2, 55, 1024), (6, 50, 2048)])
+def test_noise_budget_on_gpu_matches_oracle(k, bits, n):
+    """fv.noise_budget (fcn_noise_max: multiword CRT + block maxima on the
+    GPU, the reference's log2 on the host; fv.py:356-377) equals the
+    oracle's big-int computation exactly, fresh and after a square."""
+    from oracle import bfv as ob
+    from paper_1811_09953_b200 import configs
+    from paper_1811_09953_b200 import device as dev
+    from paper_1811_09953_b200 import fv as F
+
+    primes = tuple(configs.find_ntt_primes(n, k, bits=bits))
+    P = F.EncryptionParams(n, primes, (65537,), 1 << 32)
+    OP = ob.Params(n, primes, (65537,), 1 << 32)
+    sk, pk, ek = F.keygen(P, 8)
+    K = ob.Keys(sk.s.host(), pk.p0.host(), pk.p1.host(), [a.host() for a in ek.a], [g.host() for g in ek.g])
+    rng = np.random.default_rng(n + k)
+    plain = rng.integers(-300, 300, (5, n))
+    cts = F.encrypt_batch(pk, P, plain, 0, np.random.default_rng(9))
+    sq = F.mul_ct_batch(P, ek, 0, cts)
+    for buf in (cts, sq):
+        got = F.noise_budget_batch(sk, P, buf)
+        host = dev.to_host(buf)
+        for b in range(buf.shape[0]):
+            want = ob.noise_budget(OP, K, ob.Ct(host[b, 0], host[b, 1]))
+            assert got[b] == want, (b, got[b], want)
+    one = F.ciphertext_from_buffer(P, cts[0])
+    assert F.noise_budget(sk, one) == ob.noise_budget(OP, K, ob.Ct(dev.to_host(cts)[0, 0], dev.to_host(cts)[0, 1]))
