@@ -868,6 +868,7 @@ def main():
             # NCCL's own init log (nranks / transport per rank) on stderr
             os.environ.setdefault("NCCL_DEBUG", "INFO")
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries only the JSON line
         dist.init_process_group(backend)
         if backend == "nccl":
             probe = torch.ones(1, device="cuda")
