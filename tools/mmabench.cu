@@ -89,6 +89,40 @@ __global__ void __launch_bounds__(448, 1) bench_rot(int chunks, long long* out) 
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = slot;
   constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 16) | ((uint32_t)(64 >> 3) << 17) | (8u << 24);
+  if (MODE & 4) {  // random operand bytes instead of whatever the shared memory held
+    uint32_t* w = reinterpret_cast<uint32_t*>(smem);
+    uint32_t x = 0x9E3779B9u * (threadIdx.x + 1);
+    for (int i = threadIdx.x; i < 5 * 36864 / 4; i += blockDim.x) {
+      x ^= x << 13;
+      x ^= x >> 17;
+      x ^= x << 5;
+      w[i] = x;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+  }
+  __shared__ __align__(8) uint64_t full_bar[5], empty_bar[5];
+  if (MODE & 8) {
+    if (threadIdx.x == 0)
+      for (int i = 0; i < 5; ++i) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full_bar[i])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty_bar[i])));
+      }
+    __syncthreads();
+    if (threadIdx.x == 32) {  // producer: refill a stage once the MMAs released it
+      for (int c = 0; c < chunks; ++c) {
+        const int st = c % 5;
+        if (c >= 5) {
+          uint32_t ok = 0;
+          const uint32_t par = ((c / 5) + 1) & 1;
+          while (!ok)
+            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                         : "=r"(ok) : "r"(smem_u32(&empty_bar[st])), "r"(par));
+        }
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full_bar[st])) : "memory");
+      }
+    }
+  }
   if ((MODE & 2) && threadIdx.x >= 32) {
     uint32_t ok = 0;
     while (!ok)
@@ -99,6 +133,13 @@ __global__ void __launch_bounds__(448, 1) bench_rot(int chunks, long long* out) 
     const uint32_t base = smem_u32(smem);
     long long t0 = clock64();
     for (int c = 0; c < chunks; ++c) {
+      if (MODE & 8) {
+        uint32_t ok = 0;
+        const uint32_t par = (c / 5) & 1;
+        while (!ok)
+          asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                       : "=r"(ok) : "r"(smem_u32(&full_bar[c % 5])), "r"(par));
+      }
       if (MODE & 1)
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             smem_u32(&stage_bar[c % 5])));
@@ -117,6 +158,9 @@ __global__ void __launch_bounds__(448, 1) bench_rot(int chunks, long long* out) 
                        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + p * 64),
                        "l"(ad), "l"(bd), "r"(idesc), "r"(1));
         }
+      if (MODE & 8)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(&empty_bar[c % 5])));
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
     uint32_t ok = 0;
@@ -136,18 +180,17 @@ __global__ void __launch_bounds__(448, 1) bench_rot(int chunks, long long* out) 
 }
 
 template <int SW, int MODE = 0>
-void run_rot(long long* d, int threads = 128) {
+void run_rot(long long* d, int threads = 128, int chunks = 2048) {
   const int smem = 5 * 36864 + 1024;
   cudaFuncSetAttribute(bench_rot<SW, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const int chunks = 2048;
   bench_rot<SW, MODE><<<148, threads, smem>>>(8, d);
   cudaError_t err = cudaDeviceSynchronize();
   bench_rot<SW, MODE><<<148, threads, smem>>>(chunks, d);
   err = cudaDeviceSynchronize();
   long long cyc = 0;
   cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
-  printf("rotating operands, %s, %d threads, mode %d: %.2f clk/MMA (%s)\n", SW ? "SWIZZLE_64B" : "no swizzle", threads,
-         MODE, (double)cyc / (chunks * 14), cudaGetErrorString(err));
+  printf("rotating operands, %s, %d threads, mode %d, %d chunks: %.2f clk/MMA (%s)\n", SW ? "SWIZZLE_64B" : "no swizzle",
+         threads, MODE, chunks, (double)cyc / (chunks * 14), cudaGetErrorString(err));
 }
 
 template <int N, bool TS>
@@ -188,5 +231,9 @@ int main() {
   run_rot<0, 1>(d, 128);
   run_rot<0, 2>(d, 448);
   run_rot<0, 3>(d, 448);
+  run_rot<0, 4>(d, 128);
+  run_rot<0, 7>(d, 448);
+  run_rot<0, 12>(d, 128);
+  run_rot<0, 14>(d, 448);
   return 0;
 }
