@@ -364,8 +364,7 @@ def _conv_plan_outputs(layer, in_shape, prec: int):
     c_in, h, w = in_shape
     oc, _, kh, kw = layer.weights.shape
     _, oh, ow = _conv_out_shape(layer, in_shape)
-    eff = layer.effective_weights() if hasattr(layer, "effective_weights") else layer.weights
-    wint = round_half_away_array(np.asarray(eff, dtype=np.float64) * float(1 << prec))
+    wint = _affine_weights(layer, prec)
     ci, di, dj = np.meshgrid(np.arange(c_in), np.arange(kh), np.arange(kw), indexing="ij")
     ci, di, dj = ci.ravel(), di.ravel(), dj.ravel()
     outs = []
@@ -384,82 +383,114 @@ def _conv_plan_outputs(layer, in_shape, prec: int):
     return outs
 
 
+@dataclass
+class _Scales:
+    """Fixed-point bookkeeping while lowering (engine.py:437-529): every
+    ciphertext carries value * 2^scale * factor after a layer."""
+
+    prec: int
+    scale: int
+    factor: int
+    shape: tuple
+
+
+def _affine_weights(layer, prec: int) -> np.ndarray:
+    eff = layer.effective_weights() if hasattr(layer, "effective_weights") else layer.weights
+    return round_half_away_array(np.asarray(eff, dtype=np.float64) * float(1 << prec))
+
+
+def _lower_affine(layer, kind: str, st: _Scales, name: str) -> LinearPlan:
+    """Conv2d / Dense: integer taps with zeros elided; bias at the output scale."""
+    if kind == "Conv2d":
+        pairs = _conv_plan_outputs(layer, st.shape, st.prec)
+    else:
+        wint = _affine_weights(layer, st.prec)
+        pairs = [(o, tuple(TapPlan(int(i), int(wint[o, i])) for i in np.flatnonzero(wint[o])))
+                 for o in range(wint.shape[0])]
+    def bias(o):  # same float evaluation order as the reference
+        return None if layer.bias is None else round_half_away(
+            float(layer.bias[o]) * (1 << (st.scale + st.prec)) * st.factor)
+
+    plan = LinearPlan(name, tuple(LinearOut(taps, bias(o)) for o, taps in pairs))
+    st.scale += st.prec
+    st.shape = layer.out_shape(st.shape)
+    return plan
+
+
+def _pool_windows(layer, shape) -> tuple:
+    """Input indices of every window, (channel, row, col) order, the window's
+    row-major cells clipped to the image (engine.py:476-491)."""
+    c, h, w = shape
+    _, oh, ow = layer.out_shape(shape)
+    dr = np.repeat(np.arange(layer.window), layer.window)
+    dc = np.tile(np.arange(layer.window), layer.window)
+    wins = []
+    for ch in range(c):
+        for i in range(oh):
+            rr = i * layer.stride - layer.padding + dr
+            for j in range(ow):
+                cc = j * layer.stride - layer.padding + dc
+                ok = (rr >= 0) & (rr < h) & (cc >= 0) & (cc < w)
+                wins.append(tuple(int(v) for v in (ch * h + rr[ok]) * w + cc[ok]))
+    return tuple(wins)
+
+
+def _lower_pool(layer, kind: str, st: _Scales, name: str) -> PoolPlan:
+    """Sum of each window; 1/k as a reciprocal constant, a power-of-two shift
+    of the scale, or a factor carried to the decoder."""
+    cells = layer.window * layer.window
+    recip, shift, fmult = None, 0, 1
+    if layer.reciprocal:
+        recip = round_half_away((1.0 / cells) * (1 << st.prec))
+        st.scale += st.prec
+    elif cells & (cells - 1) == 0:
+        shift = cells.bit_length() - 1
+        st.scale += shift
+    else:
+        fmult = cells
+        st.factor *= cells
+    plan = PoolPlan(name, _pool_windows(layer, st.shape), cells, shift, fmult, recip)
+    st.shape = layer.out_shape(st.shape)
+    return plan
+
+
+def _lower_poly(layer, kind: str, st: _Scales, name: str) -> ActPlan:
+    """a2 x^2 + a1 x + a0 at the squared scale: a2 multiplies the square (its
+    own precision, elided when 1), a1 and a0 are lifted to the square's scale."""
+    a2, a1, a0 = _act_coeffs(layer)
+    p, s, f = st.prec, st.scale, st.factor
+    bump = 0 if a2 == 1.0 else p
+    plan = ActPlan(
+        name,
+        int(np.prod(st.shape)),
+        None if a2 == 1.0 else round_half_away(a2 * (1 << p)),
+        None if a1 == 0.0 else round_half_away(a1 * (1 << p)) * (1 << (s + bump - p)) * f,
+        None if a0 == 0.0 else round_half_away(a0 * (1 << (2 * s + bump)) * f * f),
+        bump,
+    )
+    st.scale, st.factor = 2 * s + bump, f * f
+    return plan
+
+
+_LOWERINGS = {"Conv2d": _lower_affine, "Dense": _lower_affine, "ScaledAvgPool": _lower_pool,
+              "PolyActivation": _lower_poly}
+
+
 def compile_network(net, cfg: FixedPointConfig) -> CompiledNet:
-    """Lower a network to the reference's integer plan (engine.py:437-529)."""
-    prec = cfg.precision_bits
+    """Lower a network to the reference's integer plan (engine.py:437-529):
+    the same plan objects, field values and layer names as the reference's
+    compile_network (pinned by digest in tests/golden)."""
+    st = _Scales(cfg.precision_bits, cfg.precision_bits, 1, tuple(net.input_shape))
     plans = []
-    shape = tuple(net.input_shape)
-    scale, factor = prec, 1
     for ix, layer in enumerate(net.layers):
         kind = _kind(layer)
-        name = f"{kind.lower()}-{ix}"
         if kind == "BatchNormAffine":
             raise EngineError("fold batch norm before compiling for encryption")
-        if kind in ("Conv2d", "Dense"):
-            if kind == "Conv2d":
-                pairs = _conv_plan_outputs(layer, shape, prec)
-            else:
-                eff = layer.effective_weights() if hasattr(layer, "effective_weights") else layer.weights
-                wint = round_half_away_array(np.asarray(eff, dtype=np.float64) * float(1 << prec))
-                pairs = []
-                for o in range(wint.shape[0]):
-                    nz = np.nonzero(wint[o])[0]
-                    pairs.append((o, tuple(TapPlan(int(i), int(wint[o, i])) for i in nz)))
-            outs = []
-            for o, taps in pairs:
-                b = None
-                if layer.bias is not None:
-                    b = round_half_away(float(layer.bias[o]) * (1 << (scale + prec)) * factor)
-                outs.append(LinearOut(taps, b))
-            plans.append(LinearPlan(name, tuple(outs)))
-            scale += prec
-            shape = layer.out_shape(shape)
-        elif kind == "ScaledAvgPool":
-            c, h, w = shape
-            _, oh, ow = layer.out_shape(shape)
-            outs = []
-            for ch in range(c):
-                for i in range(oh):
-                    for j in range(ow):
-                        r0, c0 = i * layer.stride - layer.padding, j * layer.stride - layer.padding
-                        outs.append(
-                            tuple(
-                                (ch * h + r) * w + cc
-                                for r in range(r0, r0 + layer.window)
-                                for cc in range(c0, c0 + layer.window)
-                                if 0 <= r < h and 0 <= cc < w
-                            )
-                        )
-            k = layer.window * layer.window
-            recip, shift, fmult = None, 0, 1
-            if layer.reciprocal:
-                recip = round_half_away((1.0 / k) * (1 << prec))
-                scale += prec
-            elif k & (k - 1) == 0:
-                shift = k.bit_length() - 1
-                scale += shift
-            else:
-                fmult = k
-                factor *= k
-            plans.append(PoolPlan(name, tuple(outs), k, shift, fmult, recip))
-            shape = layer.out_shape(shape)
-        elif kind == "PolyActivation":
-            a2, a1, a0 = _act_coeffs(layer)
-            nodes = int(np.prod(shape))
-            a2_int = None if a2 == 1.0 else round_half_away(a2 * (1 << prec))
-            bump = 0 if a2 == 1.0 else prec
-            a1m = None
-            if a1 != 0.0:
-                a1m = round_half_away(a1 * (1 << prec)) * (1 << (scale + bump - prec)) * factor
-            a0a = None
-            if a0 != 0.0:
-                a0a = round_half_away(a0 * (1 << (2 * scale + bump)) * factor * factor)
-            plans.append(ActPlan(name, nodes, a2_int, a1m, a0a, bump))
-            scale = 2 * scale + bump
-            factor = factor * factor
-        else:
+        lower = _LOWERINGS.get(kind)
+        if lower is None:
             raise EngineError(f"unknown layer {kind}")
-    return CompiledNet(tuple(plans), prec, scale, factor, tuple(shape))
+        plans.append(lower(layer, kind, st, f"{kind.lower()}-{ix}"))
+    return CompiledNet(tuple(plans), cfg.precision_bits, st.scale, st.factor, tuple(st.shape))
 
 
 def int_is_monomial(z: int) -> bool:
