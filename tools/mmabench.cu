@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, long long* out) {
 // 64 = SWIZZLE_64B (layout type 4) with the 64-byte atoms
 // MODE bit 0: per-chunk tcgen05.commit to a stage barrier (like the kernel);
 // bit 1: the other warps spin on an mbarrier until the MMA lane is done
-template <int SW, int MODE = 0>
+template <int SW, int MODE = 0, int NN = 64, int PL = 7>
 __global__ void __launch_bounds__(448, 1) bench_rot(int chunks, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
@@ -143,19 +143,19 @@ __global__ void __launch_bounds__(448, 1) bench_rot(int chunks, long long* out) 
       if (MODE & 1)
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             smem_u32(&stage_bar[c % 5])));
-      const uint32_t A = base + (c % 5) * 36864, B = A + 8192;
-      for (int p = 0; p < 7; ++p)
+      const uint32_t A = base + (c % 4) * 45056, B = A + 8192;
+      for (int p = 0; p < PL; ++p)
         for (int ks = 0; ks < 2; ++ks) {
           uint64_t ad, bd;
           if (SW == 0) {
             ad = sdesc(A + ks * 256, 128, 512);
-            bd = sdesc(B + p * 4096 + ks * 2048, 512, 128);
+            bd = sdesc(B + p * (NN * 64) + ks * (NN * 32), NN * 8, 128);
           } else {
             ad = sdesc(A + ks * 32, 16, 512) | (4ull << 61);
             bd = sdesc(B + p * 4096 + ks * 2048, 4096, 512) | (4ull << 61);
           }
           asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + p * 64),
+                       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + p * NN),
                        "l"(ad), "l"(bd), "r"(idesc), "r"(1));
         }
       if (MODE & 8)
@@ -179,18 +179,19 @@ __global__ void __launch_bounds__(448, 1) bench_rot(int chunks, long long* out) 
   }
 }
 
-template <int SW, int MODE = 0>
+template <int SW, int MODE = 0, int NN = 64, int PL = 7>
 void run_rot(long long* d, int threads = 128, int chunks = 2048) {
   const int smem = 5 * 36864 + 1024;
-  cudaFuncSetAttribute(bench_rot<SW, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  bench_rot<SW, MODE><<<148, threads, smem>>>(8, d);
+  cudaFuncSetAttribute(bench_rot<SW, MODE, NN, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  bench_rot<SW, MODE, NN, PL><<<148, threads, smem>>>(8, d);
   cudaError_t err = cudaDeviceSynchronize();
-  bench_rot<SW, MODE><<<148, threads, smem>>>(chunks, d);
+  bench_rot<SW, MODE, NN, PL><<<148, threads, smem>>>(chunks, d);
   err = cudaDeviceSynchronize();
   long long cyc = 0;
   cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
-  printf("rotating operands, %s, %d threads, mode %d, %d chunks: %.2f clk/MMA (%s)\n", SW ? "SWIZZLE_64B" : "no swizzle",
-         threads, MODE, chunks, (double)cyc / (chunks * 14), cudaGetErrorString(err));
+  printf("rotating operands, %s, %d threads, mode %d, N=%d x %d planes, %d chunks: %.2f clk/MMA, %.1f clk per 64x128 K-chunk-plane (%s)\n",
+         SW ? "SWIZZLE_64B" : "no swizzle", threads, MODE, NN, PL, chunks, (double)cyc / (chunks * PL * 2),
+         (double)cyc / (chunks * PL * 2) * 64.0 / NN, cudaGetErrorString(err));
 }
 
 template <int N, bool TS>
@@ -235,5 +236,9 @@ int main() {
   run_rot<0, 7>(d, 448);
   run_rot<0, 12>(d, 128);
   run_rot<0, 14>(d, 448);
+  run_rot<0, 12, 128, 4>(d, 128);
+  run_rot<0, 12, 256, 2>(d, 128);
+  run_rot<0, 4, 128, 4>(d, 128);
+  run_rot<0, 4, 256, 2>(d, 128);
   return 0;
 }
