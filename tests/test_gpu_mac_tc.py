@@ -166,3 +166,39 @@ def test_tc_mac_empty_rows():
     torch.cuda.synchronize()
     assert torch.equal(got, want)
     assert int(got[0].abs().sum()) == 0
+
+
+def test_cfg5_split_simulated_on_one_gpu():
+    """sweep.primitive_schedule (SURVEY 8(e)'s cfg5 split) with the GPU
+    kernels, ranks of a world of 2 and 3 computed one after another on one
+    GPU (no rank waits on another) and gathered by concatenation: every
+    rank's pieces equal the single-process pass byte for byte."""
+    from paper_1811_09953_b200 import dist as fdist
+    from paper_1811_09953_b200 import sweep
+
+    P = _params(4, 50)
+    sk, pk, ek = fv.keygen(P, 4)
+    B = 7
+    plan = configs.mac_sweep_plan(n_out=B, n_in=B, terms=4, seed=3)
+    x = sweep.uniform_batch(P, B, seed=5)
+    one = sweep.PrimitivePass(P, ek, plan, 0, 1)
+    want = [t.clone() for t in one.run(x)]
+    for world in (2, 3):
+        passes = [sweep.PrimitivePass(P, ek, plan, r, world) for r in range(world)]
+        parts = fdist.partition(B, world)
+        sq_blocks = [fv.mul_ct_batch(P, ek, 0, x[lo:hi]) if hi > lo else x[:0].clone() for lo, hi in parts]
+        full = torch.cat(sq_blocks)
+        got_nt, got_sq, got_mac = [], [], []
+        for r in range(world):
+            lo, hi = parts[r]
+            nt, sq, mac = sweep.primitive_schedule(
+                x[lo:hi].contiguous(), r, world, B, B, passes[r]._ntt,
+                lambda xl, r=r: sq_blocks[r], lambda loc, c, b: full,
+                lambda f, a, b, r=r: engine._layer_range(P, 0, ek, plan, ("linear",) + tuple(passes[r].low[:2]), f,
+                                                         a, b, "batched") if b > a else f[:0].clone())
+            got_nt.append(nt.clone())
+            got_sq.append(sq)
+            got_mac.append(mac)
+        assert torch.equal(torch.cat(got_nt), want[0])
+        assert torch.equal(torch.cat(got_sq), want[1])
+        assert torch.equal(torch.cat(got_mac), want[2])
