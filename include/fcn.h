@@ -131,7 +131,11 @@ int fcn_ctx_destroy(fcn_ctx* ctx);
 int fcn_ctx_ring(const fcn_ctx* ctx, const fcn_ring** out);
 /* what: 0 n, 1 k, 2 aux count m, 3 ell, 4 n_lanes, 5 log2_beta,
  * 6 whether mul_ct's lift/rescale run the exact-size FP64 kernels (1) or
- * the integer ones (0; a one-line notice goes to stderr at creation).    */
+ * the integer ones (0; a one-line notice goes to stderr at creation),
+ * 7 whether squares relinearise through the shared prime pair (digits
+ * transformed under q_0, q_1 only, the sums of the other limbs rebuilt by a
+ * two-residue CRT; same bytes as the per-limb form, fv.py:524-537;
+ * FCN_PAIR_RELIN=0 at creation turns it off).                             */
 int fcn_ctx_query(const fcn_ctx* ctx, int what, int64_t* value);
 int fcn_ctx_aux_primes(const fcn_ctx* ctx, uint64_t* out_m);
 

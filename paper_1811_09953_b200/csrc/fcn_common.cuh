@@ -360,7 +360,33 @@ struct NttEpi {
   int dbl = 0;
   uint64_t c2[kEpiLimbs], c1[kEpiLimbs];
   double fc2[kEpiLimbs], fc2q[kEpiLimbs], fc1[kEpiLimbs], fc1q[kEpiLimbs];
+  // FP64 epilogue inverse only: input row r belongs to output row
+  // (r / in_per) * out_per + r % in_per of add / out (0: the same row).  The
+  // shared-pair relinearisation transforms only limbs 0 and 1 of every poly
+  // this way (in_per = 2, out_per = k).
+  int in_per = 0, out_per = 0;
 };
+
+// Shared-pair relinearisation (fv.cu): for a limb j >= 2 the
+// key-switching sum V_j = sum_d lift(key_d mod q_j) * D_d is computed as an
+// exact integer through its residues modulo the first two limbs q_0, q_1
+// (|V_j| < q_0 q_1 / 2), so the digits are transformed under two primes
+// instead of k.  ntt_f64_inv_pair inverts the two residue rows of one unit
+// (ct, poly, j), rebuilds V_j = y0 + q_0 ((y1 - y0) q_0^-1 mod q_1) and writes
+// out = add + c2 V_j (mod q_j).
+constexpr int kPairLimbs = 16;
+struct PairEpi {
+  const uint64_t* add = nullptr;  // [C][2][k][n] signed doubles (R0 / R1)
+  Fanout out;                     // [C][2][k][n] canonical u64
+  int kq = 0;                     // limbs per poly (units per poly = kq - 2)
+  double inv01 = 0, inv01q = 0;   // q_0^-1 mod q_1 (signed), / q_1
+  double c0[kPairLimbs], c0q[kPairLimbs];    // q_0 mod q_j (signed), / q_j
+  double fc2[kPairLimbs], fc2q[kPairLimbs];  // c2 mod q_j (signed), / q_j
+};
+// Inverse NTT of `units` row pairs [unit][2][n] (signed doubles, residues
+// modulo limb 0 and limb 1 of ring r) with the CRT epilogue above; scale:
+// multiply by c2.  FP64 rings with 2^10 <= n <= 2^14 only.
+int launch_ntt_pair(const fcn_ring* r, uint64_t* d, int64_t units, bool scale, cudaStream_t st, const PairEpi* epi);
 // Batched NTT over rows; the forward may read row r's input from
 // src + (r / src_div) * n (broadcast of one source row to several limbs).
 int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int offset, bool fwd, cudaStream_t st,

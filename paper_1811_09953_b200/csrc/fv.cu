@@ -80,6 +80,12 @@ struct fcn_ctx {
   // epilogue's c2 multiply folded into the twist), built on first use
   std::mutex twist_mu;
   std::map<int64_t, double2*> ftwist_c2;
+  // Shared-pair relinearisation (decided at creation, pair_relin_setup): the
+  // digits are transformed under q_0 and q_1 only and the key-switching sums
+  // of limbs j >= 2 are rebuilt from their two residues (fcn_common.cuh PairEpi)
+  bool pair = false;
+  double pair_inv01 = 0, pair_inv01q = 0;
+  double pair_c0[fcn::kPairLimbs] = {}, pair_c0q[fcn::kPairLimbs] = {};
 };
 
 struct fcn_keys {
@@ -89,6 +95,12 @@ struct fcn_keys {
   uint64_t* d_a = nullptr;
   double2* d_fg = nullptr;  // FP64 path: {signed w, w / q_l} of d_g / d_a
   double2* d_fa = nullptr;
+  // shared-pair relinearisation: [D][2k-2][n] key words {signed w, w / q_p} in
+  // the NTT domain of q_p, p = v & 1; v = 0, 1: the limb-0 / limb-1 keys
+  // themselves; v = 2 + 2 (j - 2) + p: the centred lift of the limb-j key
+  // residues reduced modulo q_p
+  double2* d_pg = nullptr;
+  double2* d_pa = nullptr;
 };
 
 namespace fcn {
@@ -1230,6 +1242,112 @@ __global__ void __launch_bounds__(256, DMAX <= 8 ? 3 : 2) keymac_f64_kernel(cons
   }
 }
 
+// Shared-pair key table, coefficient domain: row (d, v) of out from the
+// coefficient-domain key w [D][k][n]: v < 2 copies limb v; v = 2 + 2 (j - 2) + p
+// is the centred lift of the limb-j residue reduced modulo q_p (canonical).
+__global__ void pair_key_lift_kernel(const uint64_t* __restrict__ w, uint64_t* __restrict__ out, int D, int k, int logn,
+                                     const LimbConst* __restrict__ lcs) {
+  const int V = 2 * k - 2;
+  const int64_t total = ((int64_t)D * V) << logn;
+  const int n = 1 << logn;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int coef = (int)(e & (n - 1));
+    const int64_t r = e >> logn;
+    const int v = (int)(r % V);
+    const int d = (int)(r / V);
+    const int j = v < 2 ? v : 2 + (v - 2) / 2;
+    const int p = v & 1;
+    const uint64_t x = w[(((int64_t)d * k + j) << logn) + coef];
+    if (v < 2) {
+      out[e] = x;
+      continue;
+    }
+    const uint64_t qj = lcs[j].q, qp = lcs[p].q;
+    // centred representative s of x mod q_j, then s mod q_p
+    uint64_t y;
+    if (x > qj / 2) {
+      const uint64_t neg = (qj - x) % qp;  // -s mod q_p = q_p - neg
+      y = neg ? qp - neg : 0;
+    } else {
+      y = x % qp;
+    }
+    out[e] = y;
+  }
+}
+
+// Key MAC of the shared-pair relinearisation: virtual limb v of PairEpi's
+// layout, modulus q_(v & 1).  Digits DG [C][D][2][n] (NTT domain of q_0 / q_1,
+// signed doubles), keys [D][V][n]; accumulators as signed doubles:
+// v < 2 -> ACCS [C][2][2][n] (the ordinary limb-0 / limb-1 sums), v >= 2 ->
+// ACCP [C][2][k-2][2][n] (the two residue rows of each unit, ntt_f64_inv_pair).
+// Same register scheme as keymac_f64_kernel (LEAN key words).
+template <int DMAX, bool LEAN>
+__global__ void __launch_bounds__(256, DMAX <= 8 ? 3 : 2)
+    keymac_pair_f64_kernel(const uint64_t* __restrict__ DG, const double2* __restrict__ kg, const double2* __restrict__ ka,
+                           uint64_t* __restrict__ ACCS, uint64_t* __restrict__ ACCP, int64_t C, int D, int k, int logn,
+                           const LimbConst* __restrict__ lcs) {
+  const int n = 1 << logn;
+  const int V = 2 * k - 2;
+  const int64_t lc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // v * n + coef
+  if (lc >= (int64_t)V * n) return;
+  const int v = (int)(lc >> logn);
+  const int coef = (int)(lc & (n - 1));
+  const int p = v & 1;
+  const double q = lcs[p].fq, qi = lcs[p].fqi;
+  double2 gk[LEAN ? 1 : DMAX], ak[LEAN ? 1 : DMAX];
+  double gw[LEAN ? DMAX : 1], aw[LEAN ? DMAX : 1];
+#pragma unroll
+  for (int d = 0; d < DMAX; ++d) {
+    const double2 g2 = d < D ? kg[((int64_t)d * V + v) * n + coef] : make_double2(0.0, 0.0);
+    const double2 a2 = d < D ? ka[((int64_t)d * V + v) * n + coef] : make_double2(0.0, 0.0);
+    if (LEAN) {
+      gw[d] = g2.x;
+      aw[d] = a2.x;
+    } else {
+      gk[d] = g2;
+      ak[d] = a2;
+    }
+  }
+  const int64_t per = (C + gridDim.y - 1) / gridDim.y;
+  const int64_t c0 = (int64_t)blockIdx.y * per;
+  const int64_t c1 = c0 + per < C ? c0 + per : C;
+  uint64_t nx[DMAX];
+#pragma unroll
+  for (int d = 0; d < DMAX; ++d) nx[d] = (c0 < c1 && d < D) ? DG[((c0 * D + d) * 2 + p) * n + coef] : 0;
+  // output rows of this virtual limb within one (ct, poly) group, and the group stride
+  uint64_t* const obase = v < 2 ? ACCS + (int64_t)v * n + coef : ACCP + (int64_t)(v - 2) * n + coef;
+  const int64_t gstride = (v < 2 ? 2LL : (int64_t)(V - 2)) * n;
+  for (int64_t ct = c0; ct < c1; ++ct) {
+    double xs[DMAX];
+#pragma unroll
+    for (int d = 0; d < DMAX; ++d) xs[d] = __longlong_as_double((long long)nx[d]);
+    if (ct + 1 < c1) {
+#pragma unroll
+      for (int d = 0; d < DMAX; ++d)
+        if (d < D) nx[d] = DG[(((ct + 1) * D + d) * 2 + p) * n + coef];
+    }
+    double g = 0.0, a = 0.0;
+#pragma unroll
+    for (int d = 0; d < DMAX; ++d) {
+      if (d < D) {
+        if (d > 0 && (LEAN ? d % 3 == 0 : (d & 3) == 0)) {
+          g = fredq(g, qi, q);
+          a = fredq(a, qi, q);
+        }
+        if (LEAN) {
+          g += fmulq_m(xs[d], gw[d], gw[d] * qi, q);
+          a += fmulq_m(xs[d], aw[d], aw[d] * qi, q);
+        } else {
+          g += fmulq_m(xs[d], gk[d].x, gk[d].y, q);
+          a += fmulq_m(xs[d], ak[d].x, ak[d].y, q);
+        }
+      }
+    }
+    obase[(ct * 2 + 0) * gstride] = (uint64_t)__double_as_longlong(fredq(g, qi, q));
+    obase[(ct * 2 + 1) * gstride] = (uint64_t)__double_as_longlong(fredq(a, qi, q));
+  }
+}
+
 // Decrypt rounding m = floor((w t + (q-1)/2)/q) mod t  (fv.py:344-349).
 template <int KQ, int NW>
 __global__ void decrypt_round_kernel(const uint64_t* __restrict__ W, uint64_t* __restrict__ M, int64_t count, int logn,
@@ -1454,6 +1572,42 @@ using namespace fcn;
 // ----------------------------------------------------------------- C ABI
 
 static bool f64_lift_rescale(const fcn_ctx* x);
+static double h_signed(uint64_t w, uint64_t q) { return w > q / 2 ? -(double)(q - w) : (double)w; }
+
+// Shared-pair relinearisation (PairEpi): usable when the digits are plain
+// integers below every limb (beta <= q_min), every q-limb runs the FP64
+// kernels, the key-switching sums |V_j| <= D n (beta - 1) (q_j - 1) / 2 stay
+// below 0.45 q_0 q_1 (so the two-residue CRT is exact, with margin for the
+// 2^-40 slack of the centred residues), and 2D + 4k - 4 transformed rows per
+// ciphertext beat the direct k (D + 2).  FCN_PAIR_RELIN=0 disables it.
+static void pair_relin_setup(fcn_ctx* x) {
+  x->pair = false;
+  const char* ev = getenv("FCN_PAIR_RELIN");
+  if (ev && ev[0] == '0') return;
+  const int k = x->k, D = x->ell + 1, w = x->log2_beta, n = x->n;
+  if (!x->fp || k < 3 || k > kPairLimbs || D > 12 || x->logn < 10 || x->logn > 14) return;
+  if (!f64_lift_rescale(x)) return;  // the square pipeline's signed-double rows come from the FP64 lift / rescale
+  uint64_t qmin = ~0ull, qmax = 0;
+  for (uint64_t q : x->primes) {
+    qmin = q < qmin ? q : qmin;
+    qmax = q > qmax ? q : qmax;
+  }
+  if (w >= 64 || (1ull << w) > qmin || qmax / qmin >= 4) return;
+  if (ntt_family(x->ext, k, 0) != 2) return;
+  if (2 * D + 4 * k - 4 >= k * (D + 2)) return;
+  const uint64_t q0 = x->primes[0], q1 = x->primes[1];
+  const long double vmax = (long double)D * n * (long double)((1ull << w) - 1) * ((long double)(qmax - 1) / 2);
+  if (vmax > 0.45L * (long double)q0 * (long double)q1) return;
+  const uint64_t i01 = h_powmod(q0 % q1, q1 - 2, q1);
+  x->pair_inv01 = h_signed(i01, q1);
+  x->pair_inv01q = x->pair_inv01 / (double)q1;
+  for (int j = 0; j < k; ++j) {
+    const uint64_t qj = x->primes[j];
+    x->pair_c0[j] = h_signed(q0 % qj, qj);
+    x->pair_c0q[j] = x->pair_c0[j] / (double)qj;
+  }
+  x->pair = true;
+}
 
 extern "C" int fcn_ctx_create(int device, int n, int k, const uint64_t* primes, int n_lanes, const uint64_t* t_lanes,
                               int log2_beta, fcn_ctx** out) {
@@ -1574,6 +1728,7 @@ extern "C" int fcn_ctx_create(int device, int n, int k, const uint64_t* primes, 
     fcn_ctx_destroy(x);
     return check_cuda(e, "fcn_ctx_create upload");
   }
+  pair_relin_setup(x);
   *out = x;
   return FCN_OK;
 }
@@ -1608,6 +1763,7 @@ extern "C" int fcn_ctx_query(const fcn_ctx* x, int what, int64_t* value) {
     case 4: *value = x->n_lanes; break;
     case 5: *value = x->log2_beta; break;
     case 6: *value = f64_lift_rescale(x) ? 1 : 0; break;
+    case 7: *value = x->pair ? 1 : 0; break;
     default: return set_error(FCN_ERR_ARG, "unknown query %d", what);
   }
   return FCN_OK;
@@ -1645,7 +1801,31 @@ extern "C" int fcn_keys_create(const fcn_ctx* x, const uint64_t* a, const uint64
     fcn_keys_destroy(kk);
     return check_cuda(e, "fcn_keys_create upload");
   }
-  int rc = launch_ntt(x->ext, kk->d_g, (int64_t)kk->D * kk->k, kk->k, 0, true, 0);
+  int rc = FCN_OK;
+  if (x->pair) {
+    // shared-pair tables from the coefficient-domain words (before the in-place transforms below)
+    const int V = 2 * kk->k - 2;
+    const size_t pwords = (size_t)kk->D * V * kk->n;
+    uint64_t* tmp = nullptr;
+    e = cudaMalloc(&tmp, pwords * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&kk->d_pg, pwords * sizeof(double2));
+    if (e == cudaSuccess) e = cudaMalloc(&kk->d_pa, pwords * sizeof(double2));
+    for (int which = 0; which < 2 && e == cudaSuccess && !rc; ++which) {
+      pair_key_lift_kernel<<<grid_for((int64_t)pwords, 256), 256>>>(which ? kk->d_a : kk->d_g, tmp, kk->D, kk->k, x->logn,
+                                                                    x->ext->d_lc);
+      e = cudaGetLastError();
+      if (e == cudaSuccess) rc = launch_ntt(x->ext, tmp, (int64_t)kk->D * V, 2, 0, true, 0);
+      if (e == cudaSuccess && !rc) {
+        key_to_f64_kernel<<<grid_for((int64_t)pwords, 256), 256>>>(tmp, which ? kk->d_pa : kk->d_pg, (int64_t)pwords, 2,
+                                                                   x->logn, x->ext->d_lc);
+        e = cudaGetLastError();
+      }
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaFree(tmp);
+    if (e != cudaSuccess) rc = check_cuda(e, "fcn_keys_create shared-pair tables");
+  }
+  if (!rc) rc = launch_ntt(x->ext, kk->d_g, (int64_t)kk->D * kk->k, kk->k, 0, true, 0);
   if (!rc) rc = launch_ntt(x->ext, kk->d_a, (int64_t)kk->D * kk->k, kk->k, 0, true, 0);
   if (!rc && x->fp && kk->D <= 12) {
     e = cudaMalloc(&kk->d_fg, words * sizeof(double2));
@@ -1681,6 +1861,8 @@ extern "C" int fcn_keys_destroy(fcn_keys* kk) {
     cudaFree(kk->d_a);
     cudaFree(kk->d_fg);
     cudaFree(kk->d_fa);
+    cudaFree(kk->d_pg);
+    cudaFree(kk->d_pa);
   }
   delete kk;
   return FCN_OK;
@@ -1872,7 +2054,6 @@ extern "C" size_t fcn_mul_ct_workspace_bytes(const fcn_ctx* x, int64_t chunk) {
 }
 
 // signed representative in (-q/2, q/2] as a double (q < 2^51: exact)
-static double h_signed(uint64_t w, uint64_t q) { return w > q / 2 ? -(double)(q - w) : (double)w; }
 
 template <int KQ, int KA>
 static LiftP<KQ, KA> make_lift_params(const fcn_ctx* x, const MulCtConst& mc) {
@@ -2213,6 +2394,31 @@ static int launch_keymac(const uint64_t* DG, const fcn_keys* keys, uint64_t* ACC
   return FCN_OK;
 }
 
+static int launch_keymac_pair(const uint64_t* DG, const fcn_keys* keys, uint64_t* ACCS, uint64_t* ACCP, int64_t C, int D,
+                              int k, const fcn_ctx* x, cudaStream_t st) {
+  const int64_t vn = (int64_t)(2 * k - 2) * x->n;  // one residue of one virtual limb per thread
+  const int bx = (int)((vn + 255) / 256);
+  int64_t split = (148LL * 1024 * 4 + vn - 1) / vn;
+  if (split > C) split = C;
+  if (split < 1) split = 1;
+  dim3 grid(bx, (unsigned)split);
+  switch (D) {
+#define FCN_KMP(DD, LN)                                                                                              \
+  case DD:                                                                                                           \
+    keymac_pair_f64_kernel<DD, LN><<<grid, 256, 0, st>>>(DG, keys->d_pg, keys->d_pa, ACCS, ACCP, C, DD, k, x->logn, \
+                                                         x->ext->d_lc);                                              \
+    break;
+    FCN_KMP(1, 1 >= FCN_KM_LEAN_FROM) FCN_KMP(2, 2 >= FCN_KM_LEAN_FROM) FCN_KMP(3, 3 >= FCN_KM_LEAN_FROM)
+    FCN_KMP(4, 4 >= FCN_KM_LEAN_FROM) FCN_KMP(5, 5 >= FCN_KM_LEAN_FROM) FCN_KMP(6, 6 >= FCN_KM_LEAN_FROM)
+    FCN_KMP(7, 7 >= FCN_KM_LEAN_FROM) FCN_KMP(8, 8 >= FCN_KM_LEAN_FROM) FCN_KMP(9, true) FCN_KMP(10, true)
+    FCN_KMP(11, true) FCN_KMP(12, true)
+#undef FCN_KMP
+    default: return set_error(FCN_ERR_STATE, "shared-pair key MAC: %d digits", D);
+  }
+  FCN_LAUNCH_CHECK("keymac_pair_f64_kernel");
+  return FCN_OK;
+}
+
 // ---- per-stage CUDA-event timing of fcn_mul_ct_multi (fcn_stage_timing):
 // stage ids 0 lift, 1 forward NTT (+ fused tensor), 2 tensor INTT, 3 exact
 // rescale + digits, 4 digit NTT, 5 key MAC, 6 final INTT + epilogue.
@@ -2423,6 +2629,50 @@ extern "C" int fcn_mul_ct_multi(const fcn_ctx* x, const fcn_keys* keys, int lane
     // (v) digits to NTT (broadcast rows when digits are limb-independent), key MAC
     NttEpi dg_epi;
     dg_epi.dbl = dbl;
+    if (x->pair && dbl && direct && keys->d_pg && (epi.mode == 1 || epi.mode == 3)) {
+      // shared-pair relinearisation: digits under q_0, q_1 only (2D rows per
+      // ciphertext instead of D k); limbs 0, 1 finish as usual, limbs j >= 2
+      // through the two-residue CRT of ntt_f64_inv_pair.  The 2D digit rows
+      // and the 4k - 4 accumulator rows share the D k + 2k rows of DGN | ACC.
+      uint64_t* ACCS = DGN + C * 2 * D * n;
+      uint64_t* ACCP = ACCS + C * 4 * n;
+      {
+        StageScope ss(4, st);
+        rc = launch_ntt(x->ext, DGN, C * D * 2, 2, 0, true, st, DGR, 2, &dg_epi);
+      }
+      if (rc) return rc;
+      {
+        StageScope ss(5, st);
+        rc = launch_keymac_pair(DGN, keys, ACCS, ACCP, C, D, k, x, st);
+      }
+      if (rc) return rc;
+      StageScope ss(6, st);
+      epi.add = R01;
+      epi.lin = a;
+      epi.dbl = dbl;
+      epi.in_per = 2;
+      epi.out_per = k;
+      epi.out.n = n_dst;
+      for (int d = 0; d < n_dst; ++d) epi.out.dst[d] = d_outs[d] + off * ct_words;
+      rc = launch_ntt(x->ext, ACCS, C * 4, 2, 0, false, st, nullptr, 1, &epi);
+      if (rc) return rc;
+      PairEpi pe;
+      pe.add = R01;
+      pe.out = epi.out;
+      pe.kq = k;
+      pe.inv01 = x->pair_inv01;
+      pe.inv01q = x->pair_inv01q;
+      const bool scale = epi.mode == 3 || epi.ftwist != nullptr;  // c2 (folded into the single rows' twist or not)
+      for (int l = 0; l < k; ++l) {
+        pe.c0[l] = x->pair_c0[l];
+        pe.c0q[l] = x->pair_c0q[l];
+        pe.fc2[l] = epi.fc2[l];
+        pe.fc2q[l] = epi.fc2q[l];
+      }
+      rc = launch_ntt_pair(x->ext, ACCP, C * 2 * (k - 2), scale, st, &pe);
+      if (rc) return rc;
+      continue;
+    }
     {
       StageScope ss(4, st);
       if (direct)

@@ -649,6 +649,8 @@ int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int o
     return set_error(FCN_ERR_STATE, "a replacement twist needs an FP64 inverse (epilogue mode 0, 1 or 3)");
   if (epi && epi->dbl && (family != 2 || epi->mode == 2))
     return set_error(FCN_ERR_STATE, "double-format rows need the FP64 kernels");
+  if (epi && epi->out_per && (family != 2 || epi->mode == 2 || epi->mode == 0 || fwd || epi->in_per < 1))
+    return set_error(FCN_ERR_STATE, "an output row map needs the FP64 epilogue inverse");
   if (family == 0) {
     const int rc = launch_v1(r, d, n_rows, period, offset, fwd, st, src, src_div);
     return rc ? rc : launch_epi_int(r, d, n_rows, period, offset, st, epi);
@@ -680,6 +682,24 @@ int launch_ntt(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, int o
   }
   FCN_LAUNCH_CHECK(fwd ? "ntt_v2_fwd" : "ntt_v2_inv");
   return launch_epi_int(r, d, n_rows, period, offset, st, epi);
+}
+
+template <int RS>
+int launch_ntt_f64_pair(const fcn_ring* r, uint64_t* d, int64_t units, bool scale, cudaStream_t st, const PairEpi* epi,
+                        int sms);  // ntt_f64.cuh
+
+int launch_ntt_pair(const fcn_ring* r, uint64_t* d, int64_t units, bool scale, cudaStream_t st, const PairEpi* epi) {
+  if (units <= 0) return FCN_OK;
+  if (!epi || epi->kq < 3 || epi->kq > kPairLimbs || r->L < epi->kq)
+    return set_error(FCN_ERR_ARG, "pair inverse: bad epilogue");
+  if (ntt_family(r, epi->kq, 0) != 2) return set_error(FCN_ERR_STATE, "pair inverse needs the FP64 kernels");
+  const uint64_t qmax = r->primes[0] > r->primes[1] ? r->primes[0] : r->primes[1];
+  const int sms = device_sms();
+  switch (f64_schedule(r->logn, qmax)) {
+    case 2: return launch_ntt_f64_pair<2>(r, d, units, scale, st, epi, sms);
+    case 1: return launch_ntt_f64_pair<1>(r, d, units, scale, st, epi, sms);
+    default: return launch_ntt_f64_pair<0>(r, d, units, scale, st, epi, sms);
+  }
 }
 
 int launch_ntt_square_tensor(const fcn_ring* r, const uint64_t* a, const uint64_t* aux, uint64_t* Tout, int64_t C,

@@ -435,6 +435,8 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     const double q = c.fq, qi = c.fqi;
     const double2* tw = tws + (int64_t)limb * N;
     const double2* twist = twists + (int64_t)limb * N;
+    // the add / out row of this input row (shared-pair relinearisation: limbs 0, 1 of every poly)
+    const int64_t orow = E.out_per ? (row / E.in_per) * E.out_per + row % E.in_per : row;
 #pragma unroll
     for (int j = 0; j < 32; ++j) sm[pst + j * (T + T / 32)] = (uint64_t)__double_as_longlong(x[j]);
     __syncthreads();
@@ -465,7 +467,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     for (int j = 0; j < 32; ++j) x[j] = fs[pst + j * (T + T / 32)];
     {
       // own slots only: no barrier between these reads and the cp.async writes
-      const uint64_t* pa = E.add + row * N;
+      const uint64_t* pa = E.add + orow * N;
 #pragma unroll
       for (int j = 0; j < 32; ++j) cp_async8(&sm[pst + j * (T + T / 32)], pa + tid + j * T);
       cp_async_commit();
@@ -473,7 +475,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     inv_ctf<LOGN, RS, 5, LOGN - 5, true>(x, tid, tw, q, qi, w3);
     cp_async_wait_all();
     const double c2 = E.fc2[limb], c2q = E.fc2q[limb];
-    uint64_t* po = E.out.dst[0] + row * N;
+    uint64_t* po = E.out.dst[0] + orow * N;
     const int nd = E.out.n;
     // the next row's element j is requested as soon as x[j] is consumed, so
     // its loads overlap the rest of this epilogue
@@ -488,9 +490,133 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
       const uint64_t v = f2u_canon(fredq(y + (DBL ? __longlong_as_double((long long)ar) : u2f(ar)), qi, q), q);
       po[tid + j * T] = v;
       if (FAN) {  // fan-out to the peers' buffers
-        for (int d = 1; d < nd; ++d) E.out.dst[d][row * N + tid + j * T] = v;
+        for (int d = 1; d < nd; ++d) E.out.dst[d][orow * N + tid + j * T] = v;
       }
       x[j] = __longlong_as_double((long long)pn[tid + j * T]);
+    }
+  }
+}
+
+// Shared-pair relinearisation (fcn_common.cuh PairEpi): unit u = ((ct, poly),
+// j - 2) owns the rows 2u (V_j mod q_0) and 2u + 1 (V_j mod q_1) of `data`
+// (signed doubles from the key MAC).  The CTA inverts row 0, parks its
+// twisted, reduced residues y0 in place (coalesced; read back from L2 by the
+// thread that wrote them), inverts row 1 and combines, per coefficient,
+//   u = (y1 - y0) q_0^-1 mod q_1 (centred),  V = y0 + q_0 u  (|V| < q_0 q_1 / 2),
+//   out = add + c2 (y0 + [q_0]_{q_j} u)  (mod q_j, canonical)
+// with the add row (R0 / R1) streamed into the thread's own shared-memory
+// slots during the last pass, as in ntt_f64_inv_epi.
+template <int LOGN, int RS, bool SCALE, bool FAN>
+__global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
+    ntt_f64_inv_pair(uint64_t* __restrict__ data, int64_t units, const LimbConst* __restrict__ lcs,
+                     const double2* __restrict__ tws, const double2* __restrict__ twists,
+                     const __grid_constant__ PairEpi E) {
+  constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
+  extern __shared__ uint64_t sm[];
+  double* fs = reinterpret_cast<double*>(sm);
+  const int tid = threadIdx.x;
+  const int pst = ps_strided(tid), pgr = ps_group<(RM > 0 ? RM : 0)>(tid);
+  int64_t u = blockIdx.x;
+  if (u >= units) return;
+  double x[32];  // raw bits of the next row between transforms
+  {
+    const uint64_t* p = data + 2 * u * N;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
+  }
+  const int kp = E.kq - 2;
+  for (; u < units; u += gridDim.x) {
+    const int64_t grp = u / kp;
+    const int lj = 2 + (int)(u - grp * kp);
+    const int64_t orow = grp * E.kq + lj;
+    double* row0 = reinterpret_cast<double*>(data + 2 * u * N);
+#pragma unroll 1
+    for (int s = 0; s < 2; ++s) {
+      const LimbConst& c = lcs[s];
+      const double q = c.fq, qi = c.fqi;
+      const double2* tw = tws + (int64_t)s * N;
+      const double2* twist = twists + (int64_t)s * N;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) sm[pst + j * (T + T / 32)] = (uint64_t)__double_as_longlong(x[j]);
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)sm[tid * 33 + j]);
+      inv_ctf<LOGN, RS, 5, 0>(x, 0, tw, q, qi);
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) fs[tid * 33 + j] = x[j];
+      __syncthreads();
+      if (RM > 0) {
+#pragma unroll
+        for (int i = 0; i < 32 / GM; ++i) {
+#pragma unroll
+          for (int j = 0; j < GM; ++j) x[i * GM + j] = fs[pgr + 33 * (i * GM * GM + j)];
+        }
+#pragma unroll
+        for (int i = 0; i < 32 / GM; ++i)
+          inv_ctf<LOGN, RS, (RM > 0 ? RM : 1), 5>(x + i * GM, (tid + i * T) & 31, tw, q, qi);
+#pragma unroll
+        for (int i = 0; i < 32 / GM; ++i) {
+#pragma unroll
+          for (int j = 0; j < GM; ++j) fs[pgr + 33 * (i * GM * GM + j)] = x[i * GM + j];
+        }
+      }
+      const double2 w3 = ld_ftw(tw + (1 << (LOGN - 5)) + tid);
+      if (RM > 0) __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] = fs[pst + j * (T + T / 32)];
+      if (s == 1) {
+        // own slots only: no barrier between these reads and the cp.async writes
+        const uint64_t* pa = E.add + orow * N;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) cp_async8(&sm[pst + j * (T + T / 32)], pa + tid + j * T);
+        cp_async_commit();
+      }
+      inv_ctf<LOGN, RS, 5, LOGN - 5, true>(x, tid, tw, q, qi, w3);
+      if (s == 0) {
+        // y0 = V mod q_0, |y0| <= q_0/2 + 2^-40 q_0: parked in place; row 1 replaces it in x[]
+        const uint64_t* pn = data + (2 * u + 1) * N;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const double2 w = ld_ftw(twist + tid + j * T);
+          __stcg(row0 + tid + j * T, fredq(fmulq(x[j], w.x, w.y, q), qi, q));
+          x[j] = __longlong_as_double((long long)pn[tid + j * T]);
+        }
+      } else {
+        const LimbConst& cj = lcs[lj];
+        const double qj = cj.fq, qji = cj.fqi;
+        const double c0 = E.c0[lj], c0q = E.c0q[lj];
+        const double c2 = E.fc2[lj], c2q = E.fc2q[lj];
+        const double i01 = E.inv01, i01q = E.inv01q;
+        uint64_t* po = E.out.dst[0] + orow * N;
+        const int nd = E.out.n;
+        const int64_t nxt = u + gridDim.x;
+        const uint64_t* pn = data + 2 * (nxt < units ? nxt : u) * N;
+        // parked y0, four coefficients ahead (L2 hits)
+        double y0n[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) y0n[j] = __ldcg(row0 + tid + j * T);
+        cp_async_wait_all();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const double2 w = ld_ftw(twist + tid + j * T);
+          const double y1 = fredq(fmulq(x[j], w.x, w.y, q), qi, q);  // V mod q_1, centred
+          const double y0 = y0n[j & 3];
+          if (j + 4 < 32) y0n[j & 3] = __ldcg(row0 + tid + (j + 4) * T);
+          // u = (y1 - y0) q_0^-1 mod q_1, |u| <= q_1/2 + 2^-40 q_1 (|y1 - y0| < 1.1 max(q_0, q_1))
+          const double uu = fredq(fmulq(y1 - y0, i01, i01q, q), qi, q);
+          // V mod q_j = y0 + [q_0]_{q_j} u: |.| < 1.5 q_j + (q_0/2 reduced mod q_j)
+          double z = fmulq(uu, c0, c0q, qj) + fredq(y0, qji, qj);
+          if (SCALE) z = fmulq(z, c2, c2q, qj);  // |z| < 1.5 q_j
+          const double ar = __longlong_as_double((long long)sm[pst + j * (T + T / 32)]);
+          const uint64_t v = f2u_canon(fredq(z + ar, qji, qj), qj);
+          po[tid + j * T] = v;
+          if (FAN) {
+            for (int d = 1; d < nd; ++d) E.out.dst[d][orow * N + tid + j * T] = v;
+          }
+          x[j] = __longlong_as_double((long long)pn[tid + j * T]);
+        }
+      }
     }
   }
 }
@@ -567,6 +693,36 @@ int launch_ntt_f64(const fcn_ring* r, uint64_t* d, int64_t n_rows, int period, i
     case 12: return f64_launch_t<12, RS>(fwd, sms, d, n_rows, period, offset, r, st, src, src_div, epi);
     case 13: return f64_launch_t<13, RS>(fwd, sms, d, n_rows, period, offset, r, st, src, src_div, epi);
     case 14: return f64_launch_t<14, RS>(fwd, sms, d, n_rows, period, offset, r, st, src, src_div, epi);
+    default: return set_error(FCN_ERR_ARG, "FP64 NTT: unsupported log n %d", r->logn);
+  }
+}
+
+template <int LOGN, int RS>
+static int f64_pair_launch_t(int sms, const fcn_ring* r, uint64_t* d, int64_t units, bool scale, cudaStream_t st,
+                             const PairEpi* epi) {
+  const size_t sm = (size_t)((1 << LOGN) + (1 << LOGN) / 32 + 2) * sizeof(uint64_t);
+  const bool fan = epi->out.n != 1;
+#define FCN_PAIR_GO(V, SC, FN)                                                                                  \
+  if (scale == SC && fan == FN)                                                                                 \
+    return f64_go<LOGN, RS, V>(ntt_f64_inv_pair<LOGN, RS, SC, FN>, sms, units, sm, st, d, units, r->d_lc, r->d_fict, \
+                               r->d_ftwist, *epi);
+  FCN_PAIR_GO(14, false, false)
+  FCN_PAIR_GO(15, true, false)
+  FCN_PAIR_GO(16, false, true)
+  FCN_PAIR_GO(17, true, true)
+#undef FCN_PAIR_GO
+  return FCN_OK;
+}
+
+template <int RS>
+int launch_ntt_f64_pair(const fcn_ring* r, uint64_t* d, int64_t units, bool scale, cudaStream_t st, const PairEpi* epi,
+                        int sms) {
+  switch (r->logn) {
+    case 10: return f64_pair_launch_t<10, RS>(sms, r, d, units, scale, st, epi);
+    case 11: return f64_pair_launch_t<11, RS>(sms, r, d, units, scale, st, epi);
+    case 12: return f64_pair_launch_t<12, RS>(sms, r, d, units, scale, st, epi);
+    case 13: return f64_pair_launch_t<13, RS>(sms, r, d, units, scale, st, epi);
+    case 14: return f64_pair_launch_t<14, RS>(sms, r, d, units, scale, st, epi);
     default: return set_error(FCN_ERR_ARG, "FP64 NTT: unsupported log n %d", r->logn);
   }
 }

@@ -6,4 +6,5 @@ template int launch_ntt_f64<2>(const fcn_ring*, uint64_t*, int64_t, int, int, bo
                                  const NttEpi*, int);
 template int launch_ntt_f64_sq<2>(const fcn_ring*, const uint64_t*, const uint64_t*, uint64_t*, int64_t, int, int,
                                     cudaStream_t, int, bool);
+template int launch_ntt_f64_pair<2>(const fcn_ring*, uint64_t*, int64_t, bool, cudaStream_t, const PairEpi*, int);
 }  // namespace fcn

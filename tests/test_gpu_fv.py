@@ -331,9 +331,9 @@ def test_errors(F):
 
 @pytest.mark.parametrize("env", [{"FCN_NTT_INT": "1"}, {"FCN_SQ_FUSE": "0"}, {"FCN_NTT_RS": "0"},
                                  {"FCN_DBL_ROWS": "0", "FCN_PRESCALE": "0"}, {"FCN_TWIST_C2": "0"},
-                                 {"FCN_PRESCALE": "0"}],
+                                 {"FCN_PRESCALE": "0"}, {"FCN_PAIR_RELIN": "0"}],
                          ids=["integer-kernels", "unfused-square", "ntt-rs0", "u64-rows", "scaling-epilogue",
-                              "no-prescale"])
+                              "no-prescale", "per-limb-relin"])
 def test_kernel_family_subprocess(env):
     """Kernel families the default dispatch does not pick for these shapes,
     each forced in a fresh process (the switches are read once per process):
@@ -343,7 +343,9 @@ def test_kernel_family_subprocess(env):
     FCN_DBL_ROWS=0 / FCN_PRESCALE=0 the square pipeline with canonical u64
     workspace rows and the rescale's first factor in the rescale kernel,
     FCN_TWIST_C2=0 the activation's c2 in the final INTT's epilogue instead
-    of its twist.  Squares (plain and with the fused a2 x^2 + a1 x
+    of its twist, FCN_PAIR_RELIN=0 the per-limb relinearisation (digits
+    transformed under every limb) where the default is the shared prime
+    pair.  Squares (plain and with the fused a2 x^2 + a1 x
     activation) and NTTs on the cfg1/cfg2 shapes must match the oracle.
     Squares and NTTs on the cfg1/cfg2 shapes must match the oracle."""
     import os
@@ -382,6 +384,93 @@ print("ok")
     env = dict(os.environ, PYTHONPATH=repo, **env)
     res = subprocess.run([sys.executable, "-c", code], cwd=repo, env=env, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0 and res.stdout.strip().endswith("ok"), res.stdout[-2000:] + res.stderr[-2000:]
+
+
+def _ctx_query(P, what):
+    import ctypes as C
+
+    from paper_1811_09953_b200 import _lib
+
+    v = C.c_int64()
+    _lib.check(_lib.lib().fcn_ctx_query(P.native().ptr, what, C.byref(v)))
+    return v.value
+
+
+def test_shared_pair_relin_selection(F):
+    """Which parameter sets relinearise squares through the shared prime pair
+    (fcn_ctx_query 7): beta = 2^32 with 50-bit limbs and k >= 3 (cfg2, cfg3,
+    cfg4) do; cfg1 (37-bit limbs: q_0 q_1 is too small for the two-residue
+    CRT), cfg5 (beta = 2^134: the digits are not below the limbs) and a
+    two-limb set keep the per-limb form."""
+    from paper_1811_09953_b200 import configs
+
+    want = {"cfg1": 0, "cfg2": 1, "cfg3": 1, "cfg4": 1, "cfg5": 0}
+    for name, on in want.items():
+        W = configs.WORKLOADS[name]
+        P = F.EncryptionParams(W.n, W.primes, (W.t,), W.beta)
+        assert _ctx_query(P, 7) == on, name
+    P2 = F.EncryptionParams(1024, (1125899906826241, 1125899906820097), (65537,))
+    assert _ctx_query(P2, 7) == 0
+    # three limbs: eligible by size, but (k, K) = (3, 7) has no exact-size FP64 lift / rescale (integer rows)
+    from oracle import nt as ont
+
+    P3 = F.EncryptionParams(1024, tuple(ont.ntt_primes(1024, 3, 50)), (65537,))
+    assert _ctx_query(P3, 7) == 0
+
+
+@pytest.mark.parametrize("n,k", [(1024, 4), (2048, 6)])
+def test_shared_pair_relin_extreme_keys(F, n, k):
+    """Squares relinearised through the shared prime pair with evaluation-key
+    words at the extremes of the centred lift of every limb ((q_j-1)/2,
+    (q_j+1)/2, q_j-1, 0, 1, mixed per coefficient and per limb) and
+    ciphertexts at the extremes too, so the rebuilt integer sums reach both
+    signs at full magnitude: bit-exact against the oracle's per-limb
+    relinearisation (fv.py:524-537), plain and with the fused activation."""
+    from oracle import nt as ont
+    from oracle import rns as orn
+    from paper_1811_09953_b200 import device as dev
+    from paper_1811_09953_b200 import ring
+
+    primes = tuple(ont.ntt_primes(n, k, 50))
+    P = F.EncryptionParams(n, primes, (65537,))
+    assert _ctx_query(P, 7) == 1
+    OP = ob.Params(n, primes, P.t_lanes, P.beta)
+    rng = np.random.default_rng(11)
+    D = P.ell + 1
+
+    def extreme_poly(shift):
+        rows = []
+        for l, q in enumerate(primes):
+            vals = [(q - 1) // 2, (q + 1) // 2, q - 1, 0, 1, (q - 1) // 2, (q + 1) // 2]
+            idx = (np.arange(n) + shift + 3 * l) % len(vals)
+            rows.append(np.array([vals[i] for i in idx], dtype=np.uint64))
+        return np.stack(rows)
+
+    a_h = [extreme_poly(i) if i % 2 == 0 else orn.random_uniform(primes, n, rng) for i in range(D)]
+    g_h = [extreme_poly(2 * i + 1) for i in range(D)]
+    # every key word at +q_j/2 and every digit large: the sums at full magnitude
+    g_h[0] = np.stack([np.full(n, (q - 1) // 2, dtype=np.uint64) for q in primes])
+    a_h[0] = np.stack([np.full(n, (q + 1) // 2, dtype=np.uint64) for q in primes])
+    ek = F.EvalKeys(tuple(ring.RingPoly(P.ctx, x) for x in a_h), tuple(ring.RingPoly(P.ctx, x) for x in g_h))
+    K = ob.Keys(None, None, None, a_h, g_h)
+    q = math.prod(primes)
+    full = lambda v: np.stack([np.full(n, v % p, dtype=np.uint64) for p in primes])
+    cts = [np.stack([orn.random_uniform(primes, n, rng) for _ in range(2)]) for _ in range(3)]
+    cts.append(np.stack([full(q - 1), full((q - 1) // 2)]))
+    cts.append(np.stack([extreme_poly(0), extreme_poly(5)]))
+    x = np.stack(cts)
+    for act in (None, (-3, 5), (12345, -32768)):
+        got = dev.to_host(F.mul_ct_batch(P, ek, 0, dev.to_device(x), act=act, chunk=2))
+        for b in range(len(cts)):
+            c = ob.Ct(x[b, 0], x[b, 1])
+            sq = ob.mul_ct(OP, c, c, K)
+            for p_i, (pa, xa) in enumerate(((sq.c0, x[b, 0]), (sq.c1, x[b, 1]))):
+                for l, ql in enumerate(primes):
+                    if act is None:
+                        want = pa[l].astype(object)
+                    else:
+                        want = (pa[l].astype(object) * (act[0] % ql) + xa[l].astype(object) * (act[1] % ql)) % ql
+                    assert np.array_equal(got[b, p_i, l].astype(object), want), (act, b, p_i, l)
 
 
 def test_empty_and_single_unit_batches(F):
