@@ -319,8 +319,19 @@ def _keyswitch_objects(P, ek, peak, count: int):
     t_ks = st["digit_ntt"] + st["key_mac"] + st["final_intt_add"]
     ks_bytes = 2.5 * count * Pb + keys
     sq_bytes = 2.0 * count * Pb + keys
+    import ctypes as C
+
+    from paper_1811_09953_b200 import _lib
+
+    pv = C.c_int64()
+    _lib.check(_lib.lib().fcn_ctx_query(P.native().ptr, 7, C.byref(pv)))
+    pair = bool(pv.value)
     keyswitch = {
-        "kernel": "relinearisation chain: ntt_f64_fwd (digits) + keymac_f64_kernel + ntt_f64_inv_epi",
+        "kernel": ("relinearisation chain, shared prime pair: ntt_f64_fwd (digits under q_0, q_1) + "
+                   "keymac_pair_f64_kernel + ntt_f64_inv_epi (limbs 0, 1) + ntt_f64_inv_pair (two-residue CRT)") if pair
+        else "relinearisation chain: ntt_f64_fwd (digits) + keymac_f64_kernel + ntt_f64_inv_epi",
+        "shared_pair": pair,
+        "transformed_rows_per_ciphertext": (2 * D + 4 * k - 4) if pair else k * (D + 2),
         "bound": "hbm",
         "achieved": ks_bytes / t_ks / 1e9,
         "peak": peak,
@@ -644,7 +655,8 @@ def run_gpu(args, ws, rank, local):
     ks = _keyswitch_roofline(P, ek)
     keyswitch, square = _keyswitch_objects(P, ek, peak, 256 if P.n <= 8192 else 128)
     keyswitch["inner_product_subkernel"] = {
-        "kernel": "keymac_f64_kernel alone (sum_d key_d * digit_d, NTT domain; bytes = digits + accumulators)",
+        "kernel": "keymac_f64_kernel alone (per-limb form, fcn_key_mac: sum_d key_d * digit_d, NTT domain; "
+                  "bytes = digits + accumulators)",
         "achieved": ks["bytes"] / ks["t_s"] / 1e9, "frac": ks["bytes"] / ks["t_s"] / 1e9 / peak,
         "ciphertexts_per_launch": ks["count"], "ms": ks["t_s"] * 1e3}
     hops = engine.plan_hops(comp, "batched", W.t).totals

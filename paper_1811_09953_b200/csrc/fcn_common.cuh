@@ -213,6 +213,13 @@ __device__ __forceinline__ void cp_async8(uint64_t* smem_dst, const uint64_t* gs
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc));
 }
+// The same copy ordered after the value `dep` is available: the copy
+// overwrites the shared-memory word `dep` was just read from, and naming it
+// as an operand keeps the compiler from scheduling the copy above that read.
+__device__ __forceinline__ void cp_async8_after(uint64_t* smem_dst, const uint64_t* gsrc, double dep) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;  // after %2\n" ::"r"(sa), "l"(gsrc), "d"(dep));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 template <int N>

@@ -2394,6 +2394,9 @@ static int launch_keymac(const uint64_t* DG, const fcn_keys* keys, uint64_t* ACC
   return FCN_OK;
 }
 
+#ifndef FCN_KMP_LEAN_FROM
+#define FCN_KMP_LEAN_FROM FCN_KM_LEAN_FROM
+#endif
 static int launch_keymac_pair(const uint64_t* DG, const fcn_keys* keys, uint64_t* ACCS, uint64_t* ACCP, int64_t C, int D,
                               int k, const fcn_ctx* x, cudaStream_t st) {
   const int64_t vn = (int64_t)(2 * k - 2) * x->n;  // one residue of one virtual limb per thread
@@ -2408,10 +2411,10 @@ static int launch_keymac_pair(const uint64_t* DG, const fcn_keys* keys, uint64_t
     keymac_pair_f64_kernel<DD, LN><<<grid, 256, 0, st>>>(DG, keys->d_pg, keys->d_pa, ACCS, ACCP, C, DD, k, x->logn, \
                                                          x->ext->d_lc);                                              \
     break;
-    FCN_KMP(1, 1 >= FCN_KM_LEAN_FROM) FCN_KMP(2, 2 >= FCN_KM_LEAN_FROM) FCN_KMP(3, 3 >= FCN_KM_LEAN_FROM)
-    FCN_KMP(4, 4 >= FCN_KM_LEAN_FROM) FCN_KMP(5, 5 >= FCN_KM_LEAN_FROM) FCN_KMP(6, 6 >= FCN_KM_LEAN_FROM)
-    FCN_KMP(7, 7 >= FCN_KM_LEAN_FROM) FCN_KMP(8, 8 >= FCN_KM_LEAN_FROM) FCN_KMP(9, true) FCN_KMP(10, true)
-    FCN_KMP(11, true) FCN_KMP(12, true)
+    FCN_KMP(1, 1 >= FCN_KMP_LEAN_FROM) FCN_KMP(2, 2 >= FCN_KMP_LEAN_FROM) FCN_KMP(3, 3 >= FCN_KMP_LEAN_FROM)
+    FCN_KMP(4, 4 >= FCN_KMP_LEAN_FROM) FCN_KMP(5, 5 >= FCN_KMP_LEAN_FROM) FCN_KMP(6, 6 >= FCN_KMP_LEAN_FROM)
+    FCN_KMP(7, 7 >= FCN_KMP_LEAN_FROM) FCN_KMP(8, 8 >= FCN_KMP_LEAN_FROM) FCN_KMP(9, 9 >= FCN_KMP_LEAN_FROM)
+    FCN_KMP(10, 10 >= FCN_KMP_LEAN_FROM) FCN_KMP(11, 11 >= FCN_KMP_LEAN_FROM) FCN_KMP(12, 12 >= FCN_KMP_LEAN_FROM)
 #undef FCN_KMP
     default: return set_error(FCN_ERR_STATE, "shared-pair key MAC: %d digits", D);
   }

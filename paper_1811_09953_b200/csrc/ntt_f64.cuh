@@ -518,12 +518,16 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
   const int pst = ps_strided(tid), pgr = ps_group<(RM > 0 ? RM : 0)>(tid);
   int64_t u = blockIdx.x;
   if (u >= units) return;
-  double x[32];  // raw bits of the next row between transforms
+  // every input row streams into the thread's own strided slots with
+  // cp.async (as in ntt_f64_inv): row 1 while row 0's last pass runs, the next
+  // unit's row 0 slot by slot as the combine consumes the add row
   {
     const uint64_t* p = data + 2 * u * N;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
+    for (int j = 0; j < 32; ++j) cp_async8(&sm[pst + j * (T + T / 32)], p + tid + j * T);
+    cp_async_commit();
   }
+  double x[32];
   const int kp = E.kq - 2;
   for (; u < units; u += gridDim.x) {
     const int64_t grp = u / kp;
@@ -536,13 +540,11 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
       const double q = c.fq, qi = c.fqi;
       const double2* tw = tws + (int64_t)s * N;
       const double2* twist = twists + (int64_t)s * N;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) sm[pst + j * (T + T / 32)] = (uint64_t)__double_as_longlong(x[j]);
+      cp_async_wait_all();
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)sm[tid * 33 + j]);
       inv_ctf<LOGN, RS, 5, 0>(x, 0, tw, q, qi);
-      __syncthreads();
 #pragma unroll
       for (int j = 0; j < 32; ++j) fs[tid * 33 + j] = x[j];
       __syncthreads();
@@ -565,22 +567,21 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
       if (RM > 0) __syncthreads();
 #pragma unroll
       for (int j = 0; j < 32; ++j) x[j] = fs[pst + j * (T + T / 32)];
-      if (s == 1) {
-        // own slots only: no barrier between these reads and the cp.async writes
-        const uint64_t* pa = E.add + orow * N;
+      {
+        // own slots only: no barrier between these reads and the cp.async
+        // writes.  s = 0: row 1 of the unit; s = 1: the add row (R0 / R1)
+        const uint64_t* pa = s == 0 ? data + (2 * u + 1) * N : E.add + orow * N;
 #pragma unroll
         for (int j = 0; j < 32; ++j) cp_async8(&sm[pst + j * (T + T / 32)], pa + tid + j * T);
         cp_async_commit();
       }
       inv_ctf<LOGN, RS, 5, LOGN - 5, true>(x, tid, tw, q, qi, w3);
       if (s == 0) {
-        // y0 = V mod q_0, |y0| <= q_0/2 + 2^-40 q_0: parked in place; row 1 replaces it in x[]
-        const uint64_t* pn = data + (2 * u + 1) * N;
+        // y0 = V mod q_0, |y0| <= q_0/2 + 2^-40 q_0: parked in place
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const double2 w = ld_ftw(twist + tid + j * T);
           __stcg(row0 + tid + j * T, fredq(fmulq(x[j], w.x, w.y, q), qi, q));
-          x[j] = __longlong_as_double((long long)pn[tid + j * T]);
         }
       } else {
         const LimbConst& cj = lcs[lj];
@@ -591,7 +592,8 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
         uint64_t* po = E.out.dst[0] + orow * N;
         const int nd = E.out.n;
         const int64_t nxt = u + gridDim.x;
-        const uint64_t* pn = data + 2 * (nxt < units ? nxt : u) * N;
+        const bool more = nxt < units;
+        const uint64_t* pn = data + 2 * (more ? nxt : u) * N;
         // parked y0, four coefficients ahead (L2 hits)
         double y0n[4];
 #pragma unroll
@@ -600,25 +602,29 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const double2 w = ld_ftw(twist + tid + j * T);
-          const double y1 = fredq(fmulq(x[j], w.x, w.y, q), qi, q);  // V mod q_1, centred
+          const double y1 = fmulq(x[j], w.x, w.y, q);  // V mod q_1, |y1| < 1.5 q_1
           const double y0 = y0n[j & 3];
           if (j + 4 < 32) y0n[j & 3] = __ldcg(row0 + tid + (j + 4) * T);
-          // u = (y1 - y0) q_0^-1 mod q_1, |u| <= q_1/2 + 2^-40 q_1 (|y1 - y0| < 1.1 max(q_0, q_1))
+          // u = (y1 - y0) q_0^-1 mod q_1, |u| <= q_1/2 + 2^-40 q_1 (|y1 - y0| < 1.5 q_1 + 0.51 q_0 < 2^53)
           const double uu = fredq(fmulq(y1 - y0, i01, i01q, q), qi, q);
-          // V mod q_j = y0 + [q_0]_{q_j} u: |.| < 1.5 q_j + (q_0/2 reduced mod q_j)
-          double z = fmulq(uu, c0, c0q, qj) + fredq(y0, qji, qj);
+          // V mod q_j = y0 + [q_0]_{q_j} u: |.| < 1.5 q_j + 0.51 q_0 < 3.6 q_j (limbs within a factor 4)
+          double z = fmulq(uu, c0, c0q, qj) + y0;
           if (SCALE) z = fmulq(z, c2, c2q, qj);  // |z| < 1.5 q_j
           const double ar = __longlong_as_double((long long)sm[pst + j * (T + T / 32)]);
+          // the slot just read takes the next unit's row 0 (the asm names ar,
+          // so the copy cannot be scheduled ahead of the read)
+          if (more) cp_async8_after(&sm[pst + j * (T + T / 32)], pn + tid + j * T, ar);
           const uint64_t v = f2u_canon(fredq(z + ar, qji, qj), qj);
           po[tid + j * T] = v;
           if (FAN) {
             for (int d = 1; d < nd; ++d) E.out.dst[d][orow * N + tid + j * T] = v;
           }
-          x[j] = __longlong_as_double((long long)pn[tid + j * T]);
         }
+        cp_async_commit();
       }
     }
   }
+  cp_async_wait_all();
 }
 
 // ============================================================== dispatch
