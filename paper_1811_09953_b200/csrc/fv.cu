@@ -1152,13 +1152,12 @@ __global__ void key_to_f64_kernel(const uint64_t* __restrict__ w, double2* __res
 // exact) and |.| < 0.75 q; sums are reduced after every 4 products (< 3.5 q).
 // Both outputs' 2D key words stay in registers across the ciphertexts the
 // thread walks; the next ciphertext's D digit loads are issued early.
-// LEAN: only the signed key words stay in registers and
-// each quotient factor is recomputed as w * (1/q) (relative error 3 2^-53:
-// products |.| < 0.875 q, so sums are reduced before every 3rd product).
-// From 5 digits on the kernel runs LEAN: the key words take half the
-// registers, so up to 8 digits fit 3 CTAs per SM (24 warps): more loads in
-// flight, 74% -> 80% of the HBM copy peak at cfg2 (D = 7), against one extra
-// DMUL per product.
+// LEAN: only the signed key words stay in registers and the quotient comes
+// from the rounded product itself (fprod: rint(RN(x w) / q), off by at most
+// 1/2 + 2^-3, so products are |.| < 0.63 q and sums are reduced before every
+// 6th product: < 4.3 q).  From 5 digits on the kernel runs LEAN: the key words
+// take half the registers, so up to 8 digits fit 3 CTAs per SM (24 warps):
+// more loads in flight, 74% -> 80% of the HBM copy peak at cfg2 (D = 7).
 #ifndef FCN_KM_LEAN_FROM
 #define FCN_KM_LEAN_FROM 5
 #endif
@@ -1223,13 +1222,13 @@ __global__ void __launch_bounds__(256, DMAX <= 8 ? 3 : 2) keymac_f64_kernel(cons
 #pragma unroll
     for (int d = 0; d < DMAX; ++d) {
       if (d < D) {
-        if (d > 0 && (LEAN ? d % 3 == 0 : (d & 3) == 0)) {
+        if (d > 0 && (LEAN ? d % 6 == 0 : (d & 3) == 0)) {
           g = fredq(g, qi, q);
           a = fredq(a, qi, q);
         }
         if (LEAN) {
-          g += fmulq_m(xs[d], gw[d], gw[d] * qi, q);
-          a += fmulq_m(xs[d], aw[d], aw[d] * qi, q);
+          g += fprod(xs[d], gw[d], q, qi);
+          a += fprod(xs[d], aw[d], q, qi);
         } else {
           g += fmulq_m(xs[d], gk[d].x, gk[d].y, q);
           a += fmulq_m(xs[d], ak[d].x, ak[d].y, q);
@@ -1330,13 +1329,13 @@ __global__ void __launch_bounds__(256, DMAX <= 8 ? 3 : 2)
 #pragma unroll
     for (int d = 0; d < DMAX; ++d) {
       if (d < D) {
-        if (d > 0 && (LEAN ? d % 3 == 0 : (d & 3) == 0)) {
+        if (d > 0 && (LEAN ? d % 6 == 0 : (d & 3) == 0)) {
           g = fredq(g, qi, q);
           a = fredq(a, qi, q);
         }
         if (LEAN) {
-          g += fmulq_m(xs[d], gw[d], gw[d] * qi, q);
-          a += fmulq_m(xs[d], aw[d], aw[d] * qi, q);
+          g += fprod(xs[d], gw[d], q, qi);
+          a += fprod(xs[d], aw[d], q, qi);
         } else {
           g += fmulq_m(xs[d], gk[d].x, gk[d].y, q);
           a += fmulq_m(xs[d], ak[d].x, ak[d].y, q);
