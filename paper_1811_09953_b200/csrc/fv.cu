@@ -2239,7 +2239,10 @@ static int run_lift_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_
 // The (KQ, KE) instantiation lift_or_rescale picks for a context, and
 // whether its FP64 (exact-size) kernels run.
 static bool f64_lift_rescale(const fcn_ctx* x) {
-  static const int sizes[][2] = {{2, 5}, {2, 6}, {3, 6}, {4, 8}, {4, 9}, {6, 12}, {6, 13}, {8, 16}, {8, 17}, {16, 32}};
+  // every k in 2..8 of 50-bit limbs (K = k + ceil((log2 n + 50.1 k + 4) / 50)) and cfg1's 37-bit (3, 6);
+  // a single limb keeps the integer kernels
+  static const int sizes[][2] = {{2, 5}, {2, 6}, {3, 6}, {3, 7}, {4, 8}, {4, 9}, {5, 11}, {6, 12},
+                                 {6, 13}, {7, 15}, {8, 16}, {8, 17}, {16, 32}};
   for (const auto& sz : sizes)
     if (x->k <= sz[0] && x->m <= sz[1] - sz[0]) return x->fp && x->k == sz[0] && x->k + x->m == sz[1];
   return false;
@@ -2255,10 +2258,13 @@ static int lift_or_rescale(bool lift, const fcn_ctx* x, int lane, const uint64_t
   FCN_TRY(2, 5)
   FCN_TRY(2, 6)
   FCN_TRY(3, 6)
+  FCN_TRY(3, 7)
   FCN_TRY(4, 8)
   FCN_TRY(4, 9)
+  FCN_TRY(5, 11)
   FCN_TRY(6, 12)
   FCN_TRY(6, 13)
+  FCN_TRY(7, 15)
   FCN_TRY(8, 16)
   FCN_TRY(8, 17)
   FCN_TRY(16, 32)

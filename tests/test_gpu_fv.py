@@ -411,14 +411,17 @@ def test_shared_pair_relin_selection(F):
         assert _ctx_query(P, 7) == on, name
     P2 = F.EncryptionParams(1024, (1125899906826241, 1125899906820097), (65537,))
     assert _ctx_query(P2, 7) == 0
-    # three limbs: eligible by size, but (k, K) = (3, 7) has no exact-size FP64 lift / rescale (integer rows)
+    # every k in 3..7 of 50-bit limbs has an exact-size FP64 lift / rescale and so the shared pair
     from oracle import nt as ont
 
-    P3 = F.EncryptionParams(1024, tuple(ont.ntt_primes(1024, 3, 50)), (65537,))
-    assert _ctx_query(P3, 7) == 0
+    for k in (3, 5, 7):
+        Pk = F.EncryptionParams(1024, tuple(ont.ntt_primes(1024, k, 50)), (65537,))
+        assert _ctx_query(Pk, 6) == 1 and _ctx_query(Pk, 7) == 1, k
+    P1 = F.EncryptionParams(1024, tuple(ont.ntt_primes(1024, 1, 50)), (65537,))
+    assert _ctx_query(P1, 6) == 0 and _ctx_query(P1, 7) == 0
 
 
-@pytest.mark.parametrize("n,k", [(1024, 4), (2048, 6)])
+@pytest.mark.parametrize("n,k", [(1024, 3), (1024, 4), (1024, 5), (2048, 6), (1024, 7)])
 def test_shared_pair_relin_extreme_keys(F, n, k):
     """Squares relinearised through the shared prime pair with evaluation-key
     words at the extremes of the centred lift of every limb ((q_j-1)/2,
@@ -471,6 +474,31 @@ def test_shared_pair_relin_extreme_keys(F, n, k):
                     else:
                         want = (pa[l].astype(object) * (act[0] % ql) + xa[l].astype(object) * (act[1] % ql)) % ql
                     assert np.array_equal(got[b, p_i, l].astype(object), want), (act, b, p_i, l)
+
+
+def test_single_limb_square_vs_oracle(F):
+    """k = 1 (one 50-bit limb, two digits; integer lift / rescale kernels):
+    squares against the oracle."""
+    from oracle import nt as ont
+    from oracle import rns as orn
+    from paper_1811_09953_b200 import device as dev
+
+    n = 1024
+    primes = tuple(ont.ntt_primes(n, 1, 50))
+    P = F.EncryptionParams(n, primes, (65537,))
+    OP = ob.Params(n, primes, P.t_lanes, P.beta)
+    sk, pk, ek = F.keygen(P, 4)
+    K = ob.Keys(sk.s.host(), pk.p0.host(), pk.p1.host(), [x.host() for x in ek.a], [x.host() for x in ek.g])
+    rng = np.random.default_rng(8)
+    q = primes[0]
+    cts = [np.stack([orn.random_uniform(primes, n, rng) for _ in range(2)]) for _ in range(2)]
+    cts.append(np.stack([np.full((1, n), q - 1, dtype=np.uint64), np.full((1, n), (q - 1) // 2, dtype=np.uint64)]))
+    x = np.stack(cts)
+    got = dev.to_host(F.mul_ct_batch(P, ek, 0, dev.to_device(x)))
+    for b in range(len(cts)):
+        c = ob.Ct(x[b, 0], x[b, 1])
+        w = ob.mul_ct(OP, c, c, K)
+        assert np.array_equal(got[b], np.stack([w.c0, w.c1])), b
 
 
 def test_empty_and_single_unit_batches(F):
