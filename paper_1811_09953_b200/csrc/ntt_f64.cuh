@@ -15,6 +15,17 @@
 namespace fcn {
 
 __device__ __forceinline__ int phys(int i) { return i + (i >> 5); }
+// Experiment (FCN_NTT_STAGGER_NS > 0): the second resident CTA of every SM
+// starts this many nanoseconds late, so two CTAs that run identical rows do
+// not sit in their memory phases at the same time.
+#ifndef FCN_NTT_STAGGER_NS
+#define FCN_NTT_STAGGER_NS 0
+#endif
+__device__ __forceinline__ void stagger_start() {
+#if FCN_NTT_STAGGER_NS > 0
+  if (blockIdx.x >= (gridDim.x + 1) / 2 && gridDim.x > 148) __nanosleep(FCN_NTT_STAGGER_NS);
+#endif
+}
 // phys(tid + j T) = ps(tid) + j (T + T/32): T is a multiple of 32, so the
 // padding of element tid + j T is known at compile time once ps(tid) is
 // (the compiler does not derive this itself and spent one LEA per access).
@@ -179,6 +190,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
   const int tid = threadIdx.x;
   int64_t row = blockIdx.x;
   if (row >= n_rows) return;
+  stagger_start();
   double x[32];  // raw u64 bits of the next row between iterations
   {
     const uint64_t* p = src + (src_div == 1 ? row : row / src_div) * N;
@@ -242,6 +254,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
   const int tid = threadIdx.x;
   int64_t u = blockIdx.x;
   if (u >= units) return;
+  stagger_start();
   auto src_row = [&](int64_t uu, int ss) -> const uint64_t* {
     const int64_t ct = uu / K;
     const int l = (int)(uu - ct * K);
@@ -340,6 +353,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
   const int pst = ps_strided(tid), pgr = ps_group<(RM > 0 ? RM : 0)>(tid);
   int64_t row = blockIdx.x;
   if (row >= n_rows) return;
+  stagger_start();
   {
     const uint64_t* p = data + row * N;
     {
@@ -423,6 +437,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
   const int pst = ps_strided(tid), pgr = ps_group<(RM > 0 ? RM : 0)>(tid);
   int64_t row = blockIdx.x;
   if (row >= n_rows) return;
+  stagger_start();
   double x[32];  // raw u64 bits of the next row between iterations
   {
     const uint64_t* p = data + row * N;
@@ -518,6 +533,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
   const int pst = ps_strided(tid), pgr = ps_group<(RM > 0 ? RM : 0)>(tid);
   int64_t u = blockIdx.x;
   if (u >= units) return;
+  stagger_start();
   // every input row streams into the thread's own strided slots with
   // cp.async (as in ntt_f64_inv): row 1 while row 0's last pass runs, the next
   // unit's row 0 slot by slot as the combine consumes the add row
