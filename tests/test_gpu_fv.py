@@ -463,7 +463,10 @@ def test_shared_pair_relin_extreme_keys(F, n, k):
     cts.append(np.stack([extreme_poly(0), extreme_poly(5)]))
     x = np.stack(cts)
     for act in (None, (-3, 5), (12345, -32768)):
-        got = dev.to_host(F.mul_ct_batch(P, ek, 0, dev.to_device(x), act=act, chunk=2))
+        # a second destination exercises the fan-out stores of both final inverses (the sharded evaluator's form)
+        peer = dev.empty(x.shape)
+        got = dev.to_host(F.mul_ct_batch(P, ek, 0, dev.to_device(x), act=act, chunk=2, fanout=(peer.data_ptr(),)))
+        assert np.array_equal(dev.to_host(peer), got), act
         for b in range(len(cts)):
             c = ob.Ct(x[b, 0], x[b, 1])
             sq = ob.mul_ct(OP, c, c, K)
