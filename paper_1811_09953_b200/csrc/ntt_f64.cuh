@@ -15,11 +15,53 @@
 namespace fcn {
 
 __device__ __forceinline__ int phys(int i) { return i + (i >> 5); }
+// The forward kernels pad their row buffer by FCN_FWD_PAD words per 32: with
+// 2 every thread's 32 contiguous residues start 16-byte aligned, so the
+// contiguous phases (pass-3 loads, staging stores, per-warp copy-out) move
+// 128 bits per instruction and the copy-out's reads lose their 2-way bank
+// conflict (a quarter of the forward's shared-memory wavefronts per row).
+#ifndef FCN_FWD_PAD
+#define FCN_FWD_PAD 2
+#endif
+constexpr int kFwdRW = 32 + FCN_FWD_PAD;  // words between consecutive threads' contiguous blocks
+__device__ __forceinline__ int physf(int i) { return i + FCN_FWD_PAD * (i >> 5); }
 // Experiment (FCN_NTT_STAGGER_NS > 0): the second resident CTA of every SM
 // starts this many nanoseconds late, so two CTAs that run identical rows do
 // not sit in their memory phases at the same time.
 #ifndef FCN_NTT_STAGGER_NS
 #define FCN_NTT_STAGGER_NS 0
+#endif
+// Experiment (-DFCN_NTT_PROF): warp 0 of every CTA of ntt_f64_fwd timestamps
+// its phase boundaries (clock64) and adds the deltas into fcn_ntt_prof[]
+// (read back with fcn_ntt_prof_read, tools/ntt_phase_prof.py).
+#ifdef FCN_NTT_PROF
+__device__ unsigned long long fcn_ntt_prof[16];
+#define FCN_PROF_DECL unsigned long long pf_t = 0, pf_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define FCN_PROF_ARGS , pf_t, pf_acc
+#define FCN_PROF_PARAMS , unsigned long long &pf_t, unsigned long long (&pf_acc)[8]
+#define FCN_PROF_START                                            \
+  do {                                                            \
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(pf_t)::"memory"); \
+  } while (0)
+#define FCN_PROF_MARK(i)                                          \
+  do {                                                            \
+    unsigned long long pf_n;                                      \
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(pf_n)::"memory"); \
+    pf_acc[i] += pf_n - pf_t;                                     \
+    pf_t = pf_n;                                                  \
+  } while (0)
+#define FCN_PROF_FLUSH                                                                \
+  do {                                                                                \
+    if (threadIdx.x == 0)                                                             \
+      for (int pf_i = 0; pf_i < 8; ++pf_i) atomicAdd(&fcn_ntt_prof[pf_i], pf_acc[pf_i]); \
+  } while (0)
+#else
+#define FCN_PROF_DECL
+#define FCN_PROF_ARGS
+#define FCN_PROF_PARAMS
+#define FCN_PROF_START
+#define FCN_PROF_MARK(i)
+#define FCN_PROF_FLUSH
 #endif
 __device__ __forceinline__ void stagger_start() {
 #if FCN_NTT_STAGGER_NS > 0
@@ -139,19 +181,21 @@ __device__ __forceinline__ void inv_ctf(double* x, int o, const double2* __restr
 // The forward keeps phys() addressing in its exchanges: the precomputed
 // offsets of the inverse (ps_strided / ps_group) made it 4% slower (measured
 // A/B, a different schedule with a small spill).
-#define FW_S(j) phys(tid + (j) * T)
-#define FW_G(i, j) phys((((tid + (i) * T) >> 5) << (5 + RM)) + ((tid + (i) * T) & 31) + (j) * 32)
+#define FW_S(j) physf(tid + (j) * T)
+#define FW_G(i, j) physf((((tid + (i) * T) >> 5) << (5 + RM)) + ((tid + (i) * T) & 31) + (j) * 32)
 template <int LOGN, int RS>
 __device__ __forceinline__ void fwd_body(double* x, int tid, double* fs, const double2* __restrict__ tw,
-                                         const double2* __restrict__ tl, double q, double qi) {
+                                         const double2* __restrict__ tl, double q, double qi FCN_PROF_PARAMS) {
   constexpr int N = 1 << LOGN, T = N / 32, RM = LOGN - 10, GM = 1 << RM;
   (void)N;
   // pass 1: stages 0..4 on t + j*T (twiddles uniform across the CTA)
   fwd_ctf<LOGN, RS, 5, 0>(x, 0, tw, q, qi);
   __syncthreads();  // every warp has copied out the previous row
+  FCN_PROF_MARK(0);  // load wait + conversions + pass 1 + barrier
 #pragma unroll
   for (int j = 0; j < 32; ++j) fs[FW_S(j)] = x[j];
   __syncthreads();
+  FCN_PROF_MARK(1);  // exchange 1: stores + barrier
   if (RM > 0) {
 #pragma unroll
     for (int i = 0; i < 32 / GM; ++i) {
@@ -169,10 +213,22 @@ __device__ __forceinline__ void fwd_body(double* x, int tid, double* fs, const d
   // the first twiddle of pass 3 is requested before the barrier (its L2
   // latency was exposed at the start of the pass)
   const double2 w3 = ld_ftw(tl + tid);
+  FCN_PROF_MARK(2);  // pass 2: loads + butterflies + stores
   if (RM > 0) __syncthreads();
+  FCN_PROF_MARK(3);  // barrier of exchange 2
   // pass 3: the last 5 stages on 32 contiguous residues
+  if (FCN_FWD_PAD == 2) {
+    const double2* v2 = reinterpret_cast<const double2*>(fs + tid * kFwdRW);
 #pragma unroll
-  for (int j = 0; j < 32; ++j) x[j] = fs[tid * 33 + j];
+    for (int i = 0; i < 16; ++i) {
+      const double2 v = v2[i];
+      x[2 * i] = v.x;
+      x[2 * i + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = fs[tid * kFwdRW + j];
+  }
   fwd_ctf_last<LOGN, RS, LOGN - 5>(x, tid, T, tl, q, qi, w3);
 }
 
@@ -197,6 +253,8 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
   }
+  FCN_PROF_DECL
+  FCN_PROF_START;
   for (; row < n_rows; row += gridDim.x) {
     const int limb = offset + (int)(row % period);
     const LimbConst& c = lcs[limb];
@@ -204,18 +262,30 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     const double2* tw = tws + (int64_t)limb * N;
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = u2f((uint64_t)__double_as_longlong(x[j]));
-    fwd_body<LOGN, RS>(x, tid, fs, tw, twl + (int64_t)limb * N, q, qi);
+    fwd_body<LOGN, RS>(x, tid, fs, tw, twl + (int64_t)limb * N, q, qi FCN_PROF_ARGS);
+    if (FCN_FWD_PAD == 2) {
+      ulonglong2* st2 = reinterpret_cast<ulonglong2*>(sm + tid * kFwdRW);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const double y = fredq(x[j], qi, q);
-      sm[tid * 33 + j] = DBL ? (uint64_t)__double_as_longlong(y) : f2u_canon(y, q);
+      for (int i = 0; i < 16; ++i) {
+        const double y0 = fredq(x[2 * i], qi, q), y1 = fredq(x[2 * i + 1], qi, q);
+        st2[i] = DBL ? make_ulonglong2((uint64_t)__double_as_longlong(y0), (uint64_t)__double_as_longlong(y1))
+                     : make_ulonglong2(f2u_canon(y0, q), f2u_canon(y1, q));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const double y = fredq(x[j], qi, q);
+        sm[tid * kFwdRW + j] = DBL ? (uint64_t)__double_as_longlong(y) : f2u_canon(y, q);
+      }
     }
+    FCN_PROF_MARK(4);  // pass 3: loads + butterflies + reduction + staging stores
     // A warp's 32 threads own residues [1024 w, 1024 w + 1024): it copies
     // them out coalesced on its own (no CTA barrier), while the next row's
     // loads are in flight.
     __syncwarp();
     ulonglong2* o2 = reinterpret_cast<ulonglong2*>(data + row * N) + (tid & ~31) * 16 + (tid & 31);
-    const uint64_t* sw = sm + (tid & ~31) * 33 + 2 * (tid & 31) + ((tid & 31) >> 4);
+    // pair 32 i + lane of this warp's block: thread 2 i + (lane >> 4), residues 2 (lane & 15), + 1
+    const uint64_t* sw = sm + ((tid & ~31) + ((tid & 31) >> 4)) * kFwdRW + 2 * (tid & 15);
     const int64_t nxt = row + gridDim.x;
     if (nxt < n_rows) {
       const uint64_t* p = src + (src_div == 1 ? nxt : nxt / src_div) * N;
@@ -223,14 +293,24 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
       for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
     }
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {  // pair 32 i + lane of this warp's block: phys offset 66 i
+    for (int i = 0; i < 16; ++i) {
       ulonglong2 v;
-      v.x = sw[66 * i];
-      v.y = sw[66 * i + 1];
+      if (FCN_FWD_PAD == 2) {
+        v = *reinterpret_cast<const ulonglong2*>(sw + 2 * kFwdRW * i);
+      } else {
+        v.x = sw[2 * kFwdRW * i];
+        v.y = sw[2 * kFwdRW * i + 1];
+      }
       o2[32 * i] = v;
     }
+    FCN_PROF_MARK(5);  // next-row loads issued + per-warp copy-out
   }
+  FCN_PROF_FLUSH;
 }
+
+#ifdef FCN_NTT_PROF
+extern "C" int fcn_ntt_prof_read(unsigned long long* out16, int reset);
+#endif
 
 // Forward NTT of a squared ciphertext's lifted polys fused with the
 // NTT-domain tensor (reference fv.py:511-515 with a = b): a unit (ct, l)
@@ -267,7 +347,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     for (int j = 0; j < 32; ++j) x[j] = __longlong_as_double((long long)p[tid + j * T]);
   }
   const int wb = tid & ~31, ln = tid & 31;
-  const int pofs = wb * 33 + 2 * ln + (ln >> 4);  // this lane's first pair in its warp's block (phys)
+  const int pofs = (wb + (ln >> 4)) * kFwdRW + 2 * (ln & 15);  // this lane's first pair in its warp's block
   int s = 0;
   for (;;) {
     const int64_t ct = u / K;
@@ -278,9 +358,18 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 #pragma unroll
       for (int j = 0; j < 32; ++j) x[j] = u2f((uint64_t)__double_as_longlong(x[j]));
     }
-    fwd_body<LOGN, RS>(x, tid, fs, tws + (int64_t)limb * N, twl + (int64_t)limb * N, q, qi);
+#ifdef FCN_NTT_PROF
+    unsigned long long pf_t = 0, pf_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+    fwd_body<LOGN, RS>(x, tid, fs, tws + (int64_t)limb * N, twl + (int64_t)limb * N, q, qi FCN_PROF_ARGS);
+    if (FCN_FWD_PAD == 2) {
+      double2* st2 = reinterpret_cast<double2*>(fs + tid * kFwdRW);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) fs[tid * 33 + j] = fredq(x[j], qi, q);  // |.| <= q/2 + 2^-40 q
+      for (int i = 0; i < 16; ++i) st2[i] = make_double2(fredq(x[2 * i], qi, q), fredq(x[2 * i + 1], qi, q));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) fs[tid * kFwdRW + j] = fredq(x[j], qi, q);  // |.| <= q/2 + 2^-40 q
+    }
     __syncwarp();
     const int64_t un = s == 0 ? u : u + gridDim.x;
     const bool more = un < units;
@@ -296,8 +385,12 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         ulonglong2 v;
-        v.x = (uint64_t)__double_as_longlong(fw[66 * i]);
-        v.y = (uint64_t)__double_as_longlong(fw[66 * i + 1]);
+        if (FCN_FWD_PAD == 2) {
+          v = *reinterpret_cast<const ulonglong2*>(fw + 2 * kFwdRW * i);
+        } else {
+          v.x = (uint64_t)__double_as_longlong(fw[2 * kFwdRW * i]);
+          v.y = (uint64_t)__double_as_longlong(fw[2 * kFwdRW * i + 1]);
+        }
         o2[32 * i] = v;
       }
     } else {
@@ -315,9 +408,16 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         uint64_t t0[2], t1[2], t2[2];
+        double2 a1;  // this lane's pair of A1
+        if (FCN_FWD_PAD == 2) {
+          a1 = *reinterpret_cast<const double2*>(fw + 2 * kFwdRW * i);
+        } else {
+          a1.x = fw[2 * kFwdRW * i];
+          a1.y = fw[2 * kFwdRW * i + 1];
+        }
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const double x0 = x[2 * i + v], x1 = fw[66 * i + v];
+          const double x0 = x[2 * i + v], x1 = v ? a1.y : a1.x;
           const double p0 = fprod(x0, x0, q, qi), mm = fprod(x0, x1, q, qi), p2 = fprod(x1, x1, q, qi);
           const double p1 = fredq(mm + mm, qi, q);
           // DBL: signed doubles, |.| < 0.6 q (the INTT's input bound assumes <= q)
@@ -671,13 +771,14 @@ static int f64_go(Kern kern, int sms, int64_t n_rows, size_t sm, cudaStream_t st
 template <int LOGN, int RS>
 static int f64_launch_t(bool fwd, int sms, uint64_t* d, int64_t n_rows, int period, int offset, const fcn_ring* r,
                         cudaStream_t st, const uint64_t* src, int src_div, const NttEpi* epi) {
+  const size_t smf = (size_t)((1 << LOGN) + FCN_FWD_PAD * ((1 << LOGN) / 32) + 2) * sizeof(uint64_t);
   const size_t sm = (size_t)((1 << LOGN) + (1 << LOGN) / 32 + 2) * sizeof(uint64_t);
   const bool dbl = epi && epi->dbl;
   if (fwd) {
     if (dbl)
-      return f64_go<LOGN, RS, 7>(ntt_f64_fwd<LOGN, RS, true>, sms, n_rows, sm, st, d, n_rows, period, offset, r->d_lc,
+      return f64_go<LOGN, RS, 7>(ntt_f64_fwd<LOGN, RS, true>, sms, n_rows, smf, st, d, n_rows, period, offset, r->d_lc,
                                  r->d_ffwd, r->d_ffl, src, src_div);
-    return f64_go<LOGN, RS, 0>(ntt_f64_fwd<LOGN, RS, false>, sms, n_rows, sm, st, d, n_rows, period, offset, r->d_lc,
+    return f64_go<LOGN, RS, 0>(ntt_f64_fwd<LOGN, RS, false>, sms, n_rows, smf, st, d, n_rows, period, offset, r->d_lc,
                                r->d_ffwd, r->d_ffl, src, src_div);
   }
   if (!epi || epi->mode == 0) {
@@ -752,7 +853,7 @@ int launch_ntt_f64_pair(const fcn_ring* r, uint64_t* d, int64_t units, bool scal
 template <int LOGN, int RS>
 static int f64_sq_launch_t(int sms, const fcn_ring* r, const uint64_t* a, const uint64_t* aux, uint64_t* Tout,
                            int64_t units, int k, int m, cudaStream_t st, bool dbl) {
-  const size_t sm = (size_t)((1 << LOGN) + (1 << LOGN) / 32 + 2) * sizeof(uint64_t);
+  const size_t sm = (size_t)((1 << LOGN) + FCN_FWD_PAD * ((1 << LOGN) / 32) + 2) * sizeof(uint64_t);
   if (dbl)
     return f64_go<LOGN, RS, 13>(ntt_f64_fwd_sq<LOGN, RS, true>, sms, units, sm, st, a, aux, Tout, units, k, m, r->d_lc,
                                 r->d_ffwd, r->d_ffl);
