@@ -463,6 +463,8 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     cp_async_commit();
   }
   double x[32];
+  FCN_PROF_DECL
+  FCN_PROF_START;
   for (; row < n_rows; row += gridDim.x) {
     const int limb = offset + (int)(row % period);
     const LimbConst& c = lcs[limb];
@@ -471,12 +473,14 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
     const double2* twist = twists + (int64_t)limb * N;
     cp_async_wait_all();
     __syncthreads();
+    FCN_PROF_MARK(0);  // wait for the streamed row + barrier
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = DBL ? __longlong_as_double((long long)sm[tid * 33 + j]) : u2f(sm[tid * 33 + j]);
     inv_ctf<LOGN, RS, 5, 0>(x, 0, tw, q, qi);
 #pragma unroll
     for (int j = 0; j < 32; ++j) fs[tid * 33 + j] = x[j];
     __syncthreads();
+    FCN_PROF_MARK(1);  // loads + pass 1 + stores + barrier
     if (RM > 0) {
 #pragma unroll
       for (int i = 0; i < 32 / GM; ++i) {
@@ -492,7 +496,9 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
       }
     }
     const double2 w3 = ld_ftw(tw + (1 << (LOGN - 5)) + tid);  // pass 3's first twiddle, before the barrier
+    FCN_PROF_MARK(2);  // pass 2
     if (RM > 0) __syncthreads();
+    FCN_PROF_MARK(3);  // barrier of exchange 2
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = fs[pst + j * (T + T / 32)];
     // the next row lands in exactly the slots this thread just read: no barrier
@@ -506,6 +512,7 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
       cp_async_commit();
     }
     inv_ctf<LOGN, RS, 5, LOGN - 5, true>(x, tid, tw, q, qi, w3);
+    FCN_PROF_MARK(4);  // strided loads + next-row copies issued + pass 3 (as scheduled)
     // twist by n^-1 psi^-j, canonicalise, store coalesced
     uint64_t* p = data + row * N;
 #pragma unroll
@@ -514,8 +521,10 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
       const double y = fredq(fmulq(x[j], w.x, w.y, q), qi, q);
       p[tid + j * T] = DBL ? (uint64_t)__double_as_longlong(y) : f2u_canon(y, q);
     }
+    FCN_PROF_MARK(5);  // twist + reduction + stores
   }
   cp_async_wait_all();
+  FCN_PROF_FLUSH;
 }
 
 // Inverse with a fused epilogue out = add + v (SCALE: add + c2 v), out of

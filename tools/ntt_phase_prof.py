@@ -19,8 +19,13 @@ NAMES = ["load wait + conversions + pass 1 + barrier", "exchange 1 stores + barr
          "exchange 2 barrier", "pass 3 + reduction + staging stores", "next-row loads issued + copy-out"]
 
 
+INV_NAMES = ["wait for the streamed row + barrier", "loads + pass 1 + stores + barrier", "pass 2 (loads, butterflies, stores)",
+             "exchange 2 barrier", "strided loads + next-row copies + pass 3", "twist + reduction + stores"]
+
+
 def main():
     wl = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+    inv = len(sys.argv) > 2 and sys.argv[2] == "inv"
     W = configs.WORKLOADS[wl]
     P = fv.EncryptionParams(W.n, W.primes, (W.t,), W.beta)
     h = P.native()
@@ -31,21 +36,23 @@ def main():
     buf = torch.randint(0, 1 << 50, (rows, n), device="cuda", dtype=torch.int64, generator=g)
     L = C.CDLL(os.environ["FCN_LIB_PATH"]) if "FCN_LIB_PATH" in os.environ else _lib.lib()
     lib = _lib.lib()
+    fn = lib.fcn_ntt_inverse if inv else lib.fcn_ntt_forward
+    names = INV_NAMES if inv else NAMES
     st = dev.stream_ptr()
     out = (C.c_ulonglong * 16)()
     for _ in range(2):
-        _lib.check(lib.fcn_ntt_forward(h.ring_ptr, buf.data_ptr(), rows, K, 0, st))
+        _lib.check(fn(h.ring_ptr, buf.data_ptr(), rows, K, 0, st))
     torch.cuda.synchronize()
     lib.fcn_ntt_prof_read.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
     lib.fcn_ntt_prof_read(out, 1)
     iters = 5
     for _ in range(iters):
-        _lib.check(lib.fcn_ntt_forward(h.ring_ptr, buf.data_ptr(), rows, K, 0, st))
+        _lib.check(fn(h.ring_ptr, buf.data_ptr(), rows, K, 0, st))
     torch.cuda.synchronize()
     lib.fcn_ntt_prof_read(out, 0)
     tot = sum(out[i] for i in range(6))
-    print(f"{wl} n={n} rows={rows}: {tot / (rows * iters):.0f} clocks per row (warp 0 of each CTA)")
-    for i, nm in enumerate(NAMES):
+    print(f"{wl} {'inverse' if inv else 'forward'} n={n} rows={rows}: {tot / (rows * iters):.0f} clocks per row (warp 0 of each CTA)")
+    for i, nm in enumerate(names):
         print(f"  {100 * out[i] / tot:5.1f}%  {out[i] / (rows * iters):8.0f} clk  {nm}")
 
 
