@@ -63,8 +63,8 @@ def test_ntt_many_rows_guarded_repeatable(n, k):
             assert torch.equal(fwd, ref), "forward NTT not reproducible"
 
 
-@pytest.mark.parametrize("n,k,count", [(1024, 4, 300), (8192, 4, 40)])
-def test_square_pipeline_guarded_repeatable(n, k, count):
+@pytest.mark.parametrize("n,k,count,chunk", [(1024, 4, 300, 16), (8192, 4, 40, 16), (16384, 6, 48, 48)])
+def test_square_pipeline_guarded_repeatable(n, k, count, chunk):
     primes = tuple(configs.find_ntt_primes(n, k, bits=50))
     P = fv.EncryptionParams(n, primes, (65537,), 1 << 32)
     sk, pk, ek = fv.keygen(P, 7)
@@ -72,11 +72,12 @@ def test_square_pipeline_guarded_repeatable(n, k, count):
     cts = np.stack([np.stack([orn.random_uniform(primes, n, rng) for _ in range(2)]) for _ in range(count)])
     x = dev.to_device(cts)
     buf, out = _guarded(tuple(x.shape))
-    ws_bytes = _lib.lib().fcn_mul_ct_workspace_bytes(P.native().ptr, 16)
+    # the cfg3 shape runs one chunk of 48: 384 (poly, limb) units of the paired inverse over 148 resident CTAs
+    ws_bytes = _lib.lib().fcn_mul_ct_workspace_bytes(P.native().ptr, chunk)
     wbuf, ws = _guarded((ws_bytes // 8 + 1,))
     first = None
     for rep in range(3):
-        fv.mul_ct_batch(P, ek, 0, x, out=out, workspace=ws, act=(8, -2))  # chunks of 16 through the workspace
+        fv.mul_ct_batch(P, ek, 0, x, out=out, workspace=ws, act=(8, -2))  # chunks through the workspace
         assert _guards_intact(buf) and _guards_intact(wbuf)
         if first is None:
             first = out.clone()
