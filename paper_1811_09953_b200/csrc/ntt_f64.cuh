@@ -723,11 +723,17 @@ __global__ void __launch_bounds__((1 << LOGN) / 32, FCN_NTT_MINB(LOGN))
         double y0n[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) y0n[j] = __ldcg(row0 + tid + j * T);
-        cp_async_wait_all();
+        // the twist in a loop of its own: nothing but x[] is live, so the
+        // table loads (L2) run several coefficients ahead of their products
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const double2 w = ld_ftw(twist + tid + j * T);
-          const double y1 = fmulq(x[j], w.x, w.y, q);  // V mod q_1, |y1| < 1.5 q_1
+          x[j] = fmulq(x[j], w.x, w.y, q);  // V mod q_1, |y1| < 1.5 q_1
+        }
+        cp_async_wait_all();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const double y1 = x[j];
           const double y0 = y0n[j & 3];
           if (j + 4 < 32) y0n[j & 3] = __ldcg(row0 + tid + (j + 4) * T);
           // u = (y1 - y0) q_0^-1 mod q_1, |u| <= q_1/2 + 2^-40 q_1 (|y1 - y0| < 1.5 q_1 + 0.51 q_0 < 2^53)
