@@ -4,6 +4,7 @@
 // translation unit (ntt_f64_s{0,1,2}.cu) so the three compile in parallel.
 #pragma once
 
+#include <cstdlib>
 #include <mutex>
 
 #include "fcn_common.cuh"
@@ -777,6 +778,14 @@ static int f64_go(Kern kern, int sms, int64_t n_rows, size_t sm, cudaStream_t st
   const int occ = F64Occ<LOGN, RS, V>::get((const void*)kern, sm, &err);
   if (err != cudaSuccess) return check_cuda(err, "FP64 NTT attributes");
   int64_t g = (int64_t)sms * occ;
+  {
+    // experiment: FCN_NTT_GRID_CAP limits the resident CTAs (e.g. 148: one per SM)
+    static const int cap = [] {
+      const char* ev = getenv("FCN_NTT_GRID_CAP");
+      return ev ? atoi(ev) : 0;
+    }();
+    if (cap > 0 && g > cap) g = cap;
+  }
   if (g > n_rows) g = n_rows;
   kern<<<(int)g, (1 << LOGN) / 32, sm, st>>>(args...);
   FCN_LAUNCH_CHECK("ntt_f64");
