@@ -121,15 +121,18 @@ class ClockSampler:
             if len(parts) < 8:
                 continue
             try:
-                rows.append((float(parts[0]), float(parts[1]), parts[4:8]))
+                rows.append((float(parts[0]), float(parts[1]), parts[4:8], float(parts[2])))
             except ValueError:
                 continue
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, _, fl in rows for i, f in enumerate(fl) if f.lower() == "active"})
+        reasons = sorted({names[i] for r in rows for i, f in enumerate(r[2]) if f.lower() == "active"})
         sm = sorted(r[0] for r in rows)
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons, "samples": len(rows)}
+        pw = sorted(r[3] for r in rows)
+        # power: the FP64 step runs at the board's limit, which is what sw_power_cap reports
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons, "samples": len(rows),
+                "power_w": pw[len(pw) // 2], "power_w_max": pw[-1]}
 
 
 def _peaks():
